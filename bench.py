@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""Throughput of the fused renewal tau-leap (BASELINE.json metric: Giga-NUPS).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c1]
+  python bench.py --impl reference ...      # the reference path on the host CPU
+
+A "step" is one synchronous tau-leap over every node of the workload graph.
+Default workload = BASELINE config C2 (configs[1]): SEIR with log-normal
+holding times on a uniform-degree (k=10) random graph, N = 1e6, fp32
+storage, CUDA-graph-capturable engine.  Synthetic inputs: the reference's
+own generator with graph seed 1, simulation seed 7.
+
+value     device NUPS: K single steps, each bracketed by CUDA events on the
+          launch stream, with L2 flushed (a 512 MiB write) before every step
+          so the graph/state stream from HBM; max over ranks.
+e2e       the public API end to end: run_renewal() from a host CsrGraph —
+          CSR upload, device init, CUDA-graph batches to t_final, per-batch
+          log download, trajectory record — NUPS = N * steps / wall
+          (the reference's `spreadsim bench` definition, cli.py:563-573).
+roofline  B_alg = 112 B per node-update (fp32 reference layout)
+          x N / mean step time, against MEASURED_PEAKS.json hbm_gbs.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+B_ALG = {False: 112.0, True: 78.0}  # bytes per node-update, fp32 / mixed
+WORKLOADS = {
+    "c1": dict(desc="C1: SEIR log-normal, uniform-degree k=10, N=1e4", kind="fixed", n=10_000, k=10, model="seir"),
+    "c2": dict(desc="C2: SEIR log-normal, uniform-degree k=10, N=1e6, CUDA graph", kind="fixed", n=1_000_000, k=10,
+               model="seir"),
+    "c3": dict(desc="C3: SEIR Weibull/Erlang, Barabasi-Albert m=5, N=1e6, edge-merge dispatch", kind="ba",
+               n=1_000_000, k=5, model="seir_we"),
+}
+GRAPH_SEED, SIM_SEED = 1, 7
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def build_inputs(w):
+    import paper_2604_22092_b200 as fs
+
+    if w["kind"] == "fixed":
+        g = fs.gen_fixed_degree(w["n"], w["k"], seed=GRAPH_SEED)
+    else:
+        g = fs.gen_barabasi_albert(w["n"], w["k"], seed=GRAPH_SEED)
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0) if w["model"] == "seir" else fs.seir_weibull_erlang(0.25)
+    return g, m
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ncu_traffic(workload: str):
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text()).get(workload, {})
+    return d.get("dram_bytes_per_launch")
+
+
+def cpu_baseline(w, g, m, steps: int) -> dict:
+    """The oracle port (numpy restatement of the reference, 1 thread) on a
+    bounded sample: `steps` full steps of the same workload."""
+    import paper_2604_22092_b200 as fs
+    from oracle import spreadsim_port as O
+
+    cfg = fs.RenewalConfig()
+    st = O.init_state(g, m, cfg, SIM_SEED)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        O.step(st, g, m, cfg, SIM_SEED)
+    dt = time.perf_counter() - t0
+    return {"value": g.num_nodes * steps / dt / 1e9, "unit": "G-NUPS", "cores": 1, "kind": "port",
+            "sample": f"{steps} steps x N={g.num_nodes} of {w['desc'][:2]} from t=0, oracle/spreadsim_port.py (numpy, 1 thread)"}
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    w = WORKLOADS[args.workload]
+    g, m = build_inputs(w)
+    import paper_2604_22092_b200 as fs
+    from oracle import spreadsim_port as O
+
+    cfg = fs.RenewalConfig()
+    st = O.init_state(g, m, cfg, SIM_SEED)
+    for _ in range(args.warmup):
+        O.step(st, g, m, cfg, SIM_SEED)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.step(st, g, m, cfg, SIM_SEED)
+    dt = time.perf_counter() - t0
+    v = g.num_nodes * args.steps / dt / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": "Giga-NUPS (node updates/s)", "value": v, "unit": "G-NUPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
+        "config": {"workload": w["desc"], "n": g.num_nodes, "edges": g.num_edges, "graph_seed": GRAPH_SEED,
+                   "sim_seed": SIM_SEED},
+        "cpu_baseline": {"value": v, "unit": "G-NUPS", "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} steps after {args.warmup} warm-up, numpy oracle port of renewal_step"},
+        "e2e": {"value": v, "unit": "G-NUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    torch.cuda.set_device(local)
+    import paper_2604_22092_b200 as fs
+    from paper_2604_22092_b200 import renewal as R
+
+    w = WORKLOADS[args.workload]
+    g, m = build_inputs(w)
+    cfg = fs.RenewalConfig()
+    n = g.num_nodes
+
+    # ---------------- device throughput (value) ----------------
+    st = fs.init_renewal_state(g, m, cfg, SIM_SEED)
+    plan = R._build_plan(g, m, cfg, st.mixed_precision)
+    eng = st._bind(plan, SIM_SEED, materialize=False)
+    kernels_per_step = 2 if plan.strategy == fs.Strategy.EDGE_MERGE else 1
+    eng.step(args.warmup, False, False)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            starts[k].record()
+            eng.step(1, False, False)
+            ends[k].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = torch.tensor([sum(per_step)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    total_ms = float(total_ms.item())
+    ms_per_step = total_ms / args.steps
+    value = world * n * args.steps / (total_ms / 1e3) / 1e9
+
+    # L2-warm back-to-back CUDA-graph replay (reported beside, not the headline)
+    nb = max(1, args.steps // cfg.steps_per_batch)
+    eng.run_batch(False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(nb):
+        eng.run_batch(False)
+    e1.record()
+    torch.cuda.synchronize()
+    warm_ms = e0.elapsed_time(e1) / (nb * cfg.steps_per_batch)
+    sim = st.step_counter
+    st._unbind()
+
+    # ---------------- end to end through the public API ----------------
+    e2e = None
+    if not args.no_e2e:
+        t_final = 50.0
+        g.__dict__.pop("_fs_device_cache", None)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rec = fs.run_renewal(g, m, cfg, SIM_SEED, t_final)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        steps_run = int(np.ceil(rec.summary["step_count"] / cfg.steps_per_batch) * cfg.steps_per_batch)
+        h2d = g.row_offsets.nbytes + g.col_indices.nbytes
+        d2h = 8 * (2 + m.num_compartments) * steps_run
+        e2e = {"value": n * steps_run / wall / 1e9, "unit": "G-NUPS", "h2d_bytes_per_step": h2d / steps_run,
+               "d2h_bytes_per_step": d2h / steps_run, "steps": steps_run, "wall_s": wall,
+               "what": f"run_renewal(t_final={t_final}) from a host CsrGraph: CSR H2D + init + {steps_run} steps in "
+                       f"CUDA-graph batches + per-batch log D2H + record",
+               "final_R": rec.summary["final_R"], "peak_I": rec.summary["peak_I"]}
+
+    pk = peaks()
+    mixed = bool(cfg.mixed_precision)
+    achieved = B_ALG[mixed] * n / (ms_per_step / 1e3) / 1e9
+    out = {
+        "metric": "Giga-NUPS (node updates/s)",
+        "value": value,
+        "unit": "G-NUPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 (f64 hazard/q)",
+        "data": "synthetic (reference generators, graph seed 1, sim seed 7)",
+        "config": {"workload": w["desc"], "n": n, "edges": g.num_edges, "strategy": plan.strategy.value,
+                   "gather": "count (1-bit mask)" if plan.count_mode else "f32", "precision": "fp32 storage",
+                   "l2": "flushed (512 MiB write) before every timed step", "parallelism": f"replicas x{world}",
+                   "steps_from": f"t=0 after {args.warmup} warm-up steps"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(args.workload),
+                     "bytes_per_update": B_ALG[mixed], "peak_source": pk["source"]},
+        "value_l2_warm": {"value": n / (warm_ms / 1e3) / 1e9, "ms_per_step": warm_ms,
+                          "what": f"{nb} back-to-back CUDA-graph batches of {cfg.steps_per_batch} steps, no flush"},
+        "gpu_launches": args.steps * kernels_per_step,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 or rank == 0:
+        out["cpu_baseline"] = cpu_baseline(w, g, m, args.cpu_steps) if world == 1 else None
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,216 @@
+/*
+ * flashspread.h — C ABI of libflashspread_b200.so, the sm_100a renewal
+ * tau-leaping engine (FlashSpread, arxiv 2604.22092) behind the
+ * `spreadsim.renewal` Python API.
+ *
+ * The reference package ships no native code: its hot path is the numpy
+ * function `renewal_step` (/root/reference/pkg/src/spreadsim/renewal.py:483-580)
+ * driven by `run_batch` / `run_renewal` (renewal.py:600-663).  Each entry
+ * point below replaces one reference interface; the Python mirror in
+ * paper_2604_22092_b200/renewal.py binds them with ctypes.
+ *
+ * Conventions
+ *  - plain C types only; device pointers are raw addresses of CUDA memory
+ *    owned by the caller (torch tensors) unless stated otherwise;
+ *  - every function returns 0 on success and a negative FS_E* code on
+ *    failure; fs_last_error() returns a thread-local message;
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *  - no C++ exception crosses the ABI.
+ */
+#ifndef FLASHSPREAD_H
+#define FLASHSPREAD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FS_ABI_VERSION 1
+#define FS_MAX_COMPARTMENTS 16
+
+/* error codes */
+#define FS_OK 0
+#define FS_EINVAL (-1)   /* bad argument (ValueError on the Python side) */
+#define FS_ECUDA (-2)    /* CUDA runtime error */
+#define FS_ENOMEM (-3)   /* device allocation failed */
+#define FS_ESTATE (-4)   /* engine misuse (e.g. reconfigure after start) */
+#define FS_ECONSERVE (-5)/* compartment counts no longer sum to N */
+#define FS_EREPR (-6)    /* infectivity not representable by the count gather */
+
+/* element types of the arrays that cross the boundary */
+enum fs_dtype {
+  FS_I8 = 1, FS_I32 = 2, FS_I64 = 3, FS_F16 = 4, FS_BF16 = 5,
+  FS_F32 = 6, FS_F64 = 7, FS_U32 = 8, FS_U64 = 9
+};
+
+/* CSR traversal strategy — graph.py:61-67 `Strategy` */
+enum fs_strategy { FS_PER_NODE = 0, FS_LANE = 1, FS_MERGE = 2, FS_AUTO = 3 };
+
+/* holding-time hazard of a nodal compartment — models.py:35-51 `Holding`
+ * (weibull / erlang are north_star extensions absent from the reference) */
+enum fs_hazard {
+  FS_HZ_NONE = 0,        /* absorbing, or the edge-driven S compartment */
+  FS_HZ_EXPONENTIAL = 1, /* p0 = rate                                  */
+  FS_HZ_LOGNORMAL = 2,   /* p0 = mu, p1 = sigma  (hazards.py:122-132)  */
+  FS_HZ_WEIBULL = 3,     /* p0 = shape k, p1 = scale lambda            */
+  FS_HZ_ERLANG = 4       /* p0 = shape k (integer), p1 = rate r        */
+};
+
+/* transmission profile s(tau) — hazards.py:161-218 `Shedding` */
+enum fs_shedding { FS_SHED_CONSTANT = 0, FS_SHED_LN_HAZARD = 1, FS_SHED_DENSITY_PEAK = 2 };
+
+/* counter-based uniform source */
+enum fs_rng {
+  FS_RNG_SPLITMIX = 0, /* reference mixer, rng.py:48-67 (bit-exact parity) */
+  FS_RNG_PHILOX = 1    /* Philox4x32-10, key=seed, counter=(node, step)    */
+};
+
+/* precision of the hazard / shedding evaluation */
+enum fs_hazard_precision { FS_HAZ_F64 = 0, FS_HAZ_F32 = 1 };
+
+typedef struct fs_graph {
+  int64_t num_nodes;
+  int64_t num_edges;
+  const int64_t* row_offsets;   /* device, int64[N+1] (graph.py:77-93)        */
+  const int32_t* col_indices;   /* device, int32[E], slices sorted by source  */
+  const void* weights;          /* device, f32[E] or bf16[E]; NULL if uniform */
+  int32_t weights_dtype;        /* FS_F32 | FS_BF16                           */
+  int32_t weights_uniform;      /* 1: every weight == uniform_weight          */
+  float uniform_weight;         /* the common weight (already bf16-rounded in mixed mode) */
+  int32_t d_max;                /* max in-degree                               */
+} fs_graph;
+
+typedef struct fs_compartment {
+  int32_t succ;      /* successor compartment when the transition fires */
+  int32_t terminal;  /* absorbing: age frozen, rate 0                  */
+  int32_t hazard;    /* enum fs_hazard                                  */
+  int32_t pad_;
+  double p0, p1;     /* hazard parameters, see enum fs_hazard           */
+} fs_compartment;
+
+typedef struct fs_model {   /* models.py:54-101 `ModelSpec` */
+  int32_t num_compartments;
+  int32_t edge_from;         /* S: rate = pressure  */
+  int32_t edge_to;           /* first infected successor */
+  int32_t infectious;        /* compartment exerting pressure */
+  double beta;
+  int32_t shedding;          /* enum fs_shedding */
+  int32_t pad_;
+  double shed_mu, shed_sigma;/* log-normal parameters of the profile */
+  double shed_peak;          /* f(mode) for FS_SHED_DENSITY_PEAK     */
+  fs_compartment comp[FS_MAX_COMPARTMENTS];
+} fs_model;
+
+typedef struct fs_config {  /* renewal.py:75-99 `RenewalConfig` (+ rng, hazard_precision) */
+  double epsilon, tau_max, delta;
+  int32_t steps_per_batch;
+  int32_t strategy;          /* resolved enum fs_strategy (never FS_AUTO here) */
+  int32_t compaction;
+  int32_t mixed_precision;   /* states i8 / ages f16 / infectivity bf16        */
+  int32_t lanes_per_node;
+  int32_t edges_per_block;
+  int32_t hazard_chunk;      /* accepted; results are chunk-independent        */
+  int32_t chunk_skip;        /* accepted; results are skip-independent         */
+  int32_t carry_tau;
+  int32_t rng;               /* enum fs_rng                                    */
+  int32_t hazard_precision;  /* enum fs_hazard_precision                       */
+  int32_t count_gather;      /* -1 auto, 0 force general f32 gather, 1 require count gather */
+} fs_config;
+
+/* device-resident engine scalars; mirrors the scalar fields of
+ * `RenewalState` (renewal.py:114-126) */
+typedef struct fs_scalars {
+  double clock;         /* simulated time                         */
+  double tau_next;      /* tau_prev of the reference: next step's tau */
+  int64_t step;         /* step_counter                           */
+  uint64_t seed;        /* RNG seed of the run                     */
+  float last_max_rate;  /* max rate of the last step              */
+  int32_t started;
+  int64_t counts[FS_MAX_COMPARTMENTS];
+} fs_scalars;
+
+/* per-node state arrays (device, caller-owned) */
+typedef struct fs_state_buffers {
+  void* states;          /* int32[N] (int8[N] mixed)                         */
+  void* ages;            /* f32[N]   (f16[N] mixed)                          */
+  void* infectivity[2];  /* general gather: f32/bf16[N] double buffer         */
+  uint32_t* imask[2];    /* count gather: infectious bit-mask double buffer,
+                            uint32[ceil(N/32)] each                          */
+  float* pressure;       /* f32[N], written on materialising steps            */
+  float* rates;          /* f32[N], written on materialising steps            */
+} fs_state_buffers;
+
+typedef struct fs_engine fs_engine;
+
+int fs_abi_version(void);
+const char* fs_last_error(void);
+int fs_device_sm_count(int device);
+
+/* Engine: renewal.py:321-355 `_build_plan` + the device side of
+ * `init_renewal_state` (370-410).  Reads `*scal` (host) as the initial
+ * scalars.  count_gather resolution: the bit-mask gather is used when the
+ * transmission is constant and the weights uniform (exact). */
+int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c,
+                     const fs_state_buffers* buf, const fs_scalars* scal,
+                     int device, fs_engine** out);
+void fs_engine_destroy(fs_engine* e);
+/* 1 if the engine gathers from the infectious bit-mask, 0 for the f32 gather */
+int fs_engine_uses_count_gather(const fs_engine* e);
+/* which of the two infectivity / mask buffers holds the current step's input */
+int fs_engine_current_buffer(fs_engine* e, void* stream);
+
+/* renewal.py:583-597 `_begin_batch`: tau reset (carry_tau off) and, with
+ * compaction, rates zeroing + active-tile refresh */
+int fs_engine_begin_batch(fs_engine* e, void* stream);
+/* renewal.py:483-580 `renewal_step` x nsteps, launched eagerly; the last
+ * step materialises pressure/rates when `materialize` is nonzero; with
+ * `use_active` only the tiles of the last begin_batch refresh are stepped
+ * (the `active=` argument of renewal_step) */
+int fs_engine_step(fs_engine* e, int32_t nsteps, int32_t materialize, int32_t use_active, void* stream);
+/* renewal.py:600-629 `run_batch`: begin_batch + steps_per_batch steps,
+ * replayed from a CUDA graph captured on first use */
+int fs_engine_run_batch(fs_engine* e, int32_t materialize, void* stream);
+/* Per-step log of steps [first_step, first_step+n): clock[n], tau[n] and
+ * counts[n][M] (host arrays, any may be NULL) — the recorder of run_batch
+ * (renewal.py:622-627).  The ring holds max(256, 4*steps_per_batch) steps. */
+int fs_engine_read_log(fs_engine* e, int64_t first_step, int32_t n,
+                       double* clocks, double* taus, int64_t* counts, void* stream);
+int fs_engine_get_scalars(fs_engine* e, fs_scalars* out, void* stream);
+int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream);
+/* re-derive the infectious mask / general buffer from a freshly uploaded
+ * infectivity array (host edits between steps); `inf` has the storage dtype */
+int fs_engine_load_infectivity(fs_engine* e, const void* inf, void* stream);
+/* expand the current infectivity to the storage dtype (for reads) */
+int fs_engine_store_infectivity(fs_engine* e, void* inf_out, void* stream);
+
+/* renewal.py:264-313 `pressure_gather`: p_i = sum_e f32(inf[col[e]] * w[e])
+ * folded in CSR order with an f32 accumulator, any strategy, bit-exact. */
+int fs_pressure_gather(const fs_graph* g, const void* infectivity, int32_t inf_dtype,
+                       float* out, int32_t strategy, int32_t lanes_per_node,
+                       int32_t edges_per_block, void* stream);
+
+/* rng.py:60-67 `uniform_array` (splitmix) or Philox4x32-10; streams==NULL
+ * means streams = arange(n) */
+int fs_uniform_fill(uint64_t seed, uint64_t step, const uint64_t* streams, int64_t n,
+                    int32_t rng, double* out, void* stream);
+
+/* hazards.py:122-132 `_hazard_f64` (and the weibull / erlang extensions):
+ * out[i] = h(tau[i]) in f64 (precision FS_HAZ_F64) or fp32 math widened */
+int fs_hazard_eval(const fs_compartment* c, const double* tau, int64_t n, double* out,
+                   int32_t precision, void* stream);
+/* hazards.py:108-119 `erfcx_stable` */
+int fs_erfcx_eval(const double* z, int64_t n, double* out, void* stream);
+
+/* renewal.py:426-432 `refresh_active`: sorted ids of non-terminal nodes.
+ * `terminal` is a host array of num_compartments bytes. out_ids has N+pad
+ * entries (zero-padded); *num_active is written (host). */
+int fs_refresh_active(const void* states, int32_t states_dtype, int64_t n,
+                      const uint8_t* terminal, int32_t num_compartments,
+                      int32_t* out_ids, int64_t capacity, int64_t* num_active,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLASHSPREAD_H */

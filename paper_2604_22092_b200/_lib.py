@@ -1,0 +1,197 @@
+"""ctypes binding of libflashspread_b200.so (include/flashspread.h).
+
+The structures below mirror the C layouts field for field (natural C
+alignment, which ctypes reproduces).  Every call goes through `check`, which
+turns a negative return code into the Python exception the reference would
+raise.  There is no fallback: if the shared library or a CUDA device is
+missing, importing the engine raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import FlashSpreadNativeError, InvalidConfigError, ReconfigureAfterStartError
+
+MAX_COMPARTMENTS = 16
+ABI_VERSION = 1
+
+# enum fs_dtype
+I8, I32, I64, F16, BF16, F32, F64, U32, U64 = 1, 2, 3, 4, 5, 6, 7, 8, 9
+# enum fs_strategy
+PER_NODE, LANE, MERGE, AUTO = 0, 1, 2, 3
+# enum fs_hazard
+HZ_NONE, HZ_EXPONENTIAL, HZ_LOGNORMAL, HZ_WEIBULL, HZ_ERLANG = 0, 1, 2, 3, 4
+# enum fs_shedding
+SHED_CONSTANT, SHED_LN_HAZARD, SHED_DENSITY_PEAK = 0, 1, 2
+# enum fs_rng
+RNG_SPLITMIX, RNG_PHILOX = 0, 1
+# enum fs_hazard_precision
+HAZ_F64, HAZ_F32 = 0, 1
+
+FS_EINVAL, FS_ECUDA, FS_ENOMEM, FS_ESTATE, FS_ECONSERVE, FS_EREPR = -1, -2, -3, -4, -5, -6
+
+_c_i32, _c_i64, _c_u64, _c_f32, _c_f64, _vp = (
+    ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float, ctypes.c_double, ctypes.c_void_p,
+)
+
+
+class FsGraph(ctypes.Structure):
+    _fields_ = [
+        ("num_nodes", _c_i64),
+        ("num_edges", _c_i64),
+        ("row_offsets", _vp),
+        ("col_indices", _vp),
+        ("weights", _vp),
+        ("weights_dtype", _c_i32),
+        ("weights_uniform", _c_i32),
+        ("uniform_weight", _c_f32),
+        ("d_max", _c_i32),
+    ]
+
+
+class FsCompartment(ctypes.Structure):
+    _fields_ = [
+        ("succ", _c_i32),
+        ("terminal", _c_i32),
+        ("hazard", _c_i32),
+        ("pad_", _c_i32),
+        ("p0", _c_f64),
+        ("p1", _c_f64),
+    ]
+
+
+class FsModel(ctypes.Structure):
+    _fields_ = [
+        ("num_compartments", _c_i32),
+        ("edge_from", _c_i32),
+        ("edge_to", _c_i32),
+        ("infectious", _c_i32),
+        ("beta", _c_f64),
+        ("shedding", _c_i32),
+        ("pad_", _c_i32),
+        ("shed_mu", _c_f64),
+        ("shed_sigma", _c_f64),
+        ("shed_peak", _c_f64),
+        ("comp", FsCompartment * MAX_COMPARTMENTS),
+    ]
+
+
+class FsConfig(ctypes.Structure):
+    _fields_ = [
+        ("epsilon", _c_f64),
+        ("tau_max", _c_f64),
+        ("delta", _c_f64),
+        ("steps_per_batch", _c_i32),
+        ("strategy", _c_i32),
+        ("compaction", _c_i32),
+        ("mixed_precision", _c_i32),
+        ("lanes_per_node", _c_i32),
+        ("edges_per_block", _c_i32),
+        ("hazard_chunk", _c_i32),
+        ("chunk_skip", _c_i32),
+        ("carry_tau", _c_i32),
+        ("rng", _c_i32),
+        ("hazard_precision", _c_i32),
+        ("count_gather", _c_i32),
+    ]
+
+
+class FsScalars(ctypes.Structure):
+    _fields_ = [
+        ("clock", _c_f64),
+        ("tau_next", _c_f64),
+        ("step", _c_i64),
+        ("seed", _c_u64),
+        ("last_max_rate", _c_f32),
+        ("started", _c_i32),
+        ("counts", _c_i64 * MAX_COMPARTMENTS),
+    ]
+
+
+class FsStateBuffers(ctypes.Structure):
+    _fields_ = [
+        ("states", _vp),
+        ("ages", _vp),
+        ("infectivity", _vp * 2),
+        ("imask", _vp * 2),
+        ("pressure", _vp),
+        ("rates", _vp),
+    ]
+
+
+_SIGNATURES = {
+    "fs_abi_version": (_c_i32, []),
+    "fs_last_error": (ctypes.c_char_p, []),
+    "fs_device_sm_count": (_c_i32, [_c_i32]),
+    "fs_engine_create": (_c_i32, [ctypes.POINTER(FsGraph), ctypes.POINTER(FsModel), ctypes.POINTER(FsConfig),
+                                   ctypes.POINTER(FsStateBuffers), ctypes.POINTER(FsScalars), _c_i32,
+                                   ctypes.POINTER(_vp)]),
+    "fs_engine_destroy": (None, [_vp]),
+    "fs_engine_uses_count_gather": (_c_i32, [_vp]),
+    "fs_engine_current_buffer": (_c_i32, [_vp, _vp]),
+    "fs_engine_begin_batch": (_c_i32, [_vp, _vp]),
+    "fs_engine_step": (_c_i32, [_vp, _c_i32, _c_i32, _c_i32, _vp]),
+    "fs_engine_run_batch": (_c_i32, [_vp, _c_i32, _vp]),
+    "fs_engine_read_log": (_c_i32, [_vp, _c_i64, _c_i32, _vp, _vp, _vp, _vp]),
+    "fs_engine_get_scalars": (_c_i32, [_vp, ctypes.POINTER(FsScalars), _vp]),
+    "fs_engine_set_scalars": (_c_i32, [_vp, ctypes.POINTER(FsScalars), _vp]),
+    "fs_engine_load_infectivity": (_c_i32, [_vp, _vp, _vp]),
+    "fs_engine_store_infectivity": (_c_i32, [_vp, _vp, _vp]),
+    "fs_pressure_gather": (_c_i32, [ctypes.POINTER(FsGraph), _vp, _c_i32, _vp, _c_i32, _c_i32, _c_i32, _vp]),
+    "fs_uniform_fill": (_c_i32, [_c_u64, _c_u64, _vp, _c_i64, _c_i32, _vp, _vp]),
+    "fs_hazard_eval": (_c_i32, [ctypes.POINTER(FsCompartment), _vp, _c_i64, _vp, _c_i32, _vp]),
+    "fs_erfcx_eval": (_c_i32, [_vp, _c_i64, _vp, _vp]),
+    "fs_refresh_active": (_c_i32, [_vp, _c_i32, _c_i64, _vp, _c_i32, _vp, _c_i64, ctypes.POINTER(_c_i64), _vp]),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+LIB_PATH = Path(__file__).resolve().parent / "libflashspread_b200.so"
+_lib = None
+
+
+def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
+    """Load (once) and type the shared library; raises if it is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise FlashSpreadNativeError(
+            f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)"
+        )
+    lib = ctypes.CDLL(str(p))
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.fs_abi_version() != ABI_VERSION:
+        raise FlashSpreadNativeError(f"ABI version mismatch: {lib.fs_abi_version()} != {ABI_VERSION}")
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(rc: int) -> int:
+    """Map a C return code onto the reference's exception types."""
+    if rc >= 0:
+        return rc
+    msg = load().fs_last_error().decode(errors="replace")
+    if rc == FS_EINVAL:
+        raise InvalidConfigError(msg)
+    if rc == FS_ESTATE:
+        raise ReconfigureAfterStartError(msg)
+    if rc == FS_ECONSERVE:
+        raise AssertionError(msg)
+    raise FlashSpreadNativeError(f"libflashspread_b200 error {rc}: {msg}")
+
+
+def ptr(t) -> int | None:
+    """Raw device address of a torch tensor (None for empty / missing)."""
+    if t is None or t.numel() == 0:
+        return None
+    return t.data_ptr()

@@ -1,0 +1,1118 @@
+// fs_engine.cu — the fused renewal tau-leap for sm_100a and its C ABI.
+//
+// One launch = one `renewal_step` of the reference
+// (/root/reference/pkg/src/spreadsim/renewal.py:483-580):
+//   CSR pressure gather -> per-compartment rate (pressure / exponential /
+//   log-normal, Weibull, Erlang hazard) -> Bernoulli on a counter-based
+//   uniform -> successor state, age reset / advance / freeze -> next-step
+//   infectivity -> block max-rate and count deltas -> the last CTA to finish
+//   folds the per-CTA partials into the device scalars (clock, step, tau',
+//   counts) and the per-step log.  Nothing round-trips to the host inside a
+//   batch, so `run_batch` is one CUDA-graph replay.
+//
+// Gather encodings:
+//   COUNT_SMEM / COUNT_GLOBAL — constant transmission and uniform weights:
+//     every contribution is the same f32 value c or 0, so the CSR-order f32
+//     fold equals ptab[k], the k-fold sequential f32 sum of c, where k is the
+//     number of infectious in-neighbours.  Infectivity travels as a 1-bit
+//     mask (N/8 bytes), staged whole into shared memory when it fits.
+//   F32  — general weights / age-dependent shedding: per-node sequential
+//     f32 fold of f32(inf[col]*w) in CSR order (no FMA), bit-exact.
+//   PRE  — pressure gathered by the edge-chunked merge kernel beforehand.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <cstdarg>
+#include <string>
+#include <vector>
+#include <algorithm>
+#include "fs_device.cuh"
+#include "fs_internal.h"
+
+namespace fs {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kCntStride = FS_MAX_COMPARTMENTS;
+// shared-memory budget for the staged mask: leaves room for the static
+// tables on a 227 KB CTA
+constexpr size_t kMaxSmemMaskBytes = 220u * 1024u;
+
+enum Gather { G_COUNT_SMEM = 0, G_COUNT_GLOBAL = 1, G_F32 = 2, G_PRE = 3 };
+enum Strat { S_THREAD = 0, S_WARP = 1 };
+
+struct StepParams {
+  // graph (renewal.py:264-313 inputs)
+  const int64_t* ro;
+  const int32_t* col;
+  const void* w;          // f32 or bf16; unused when uniform
+  int w_bf16;
+  int w_uniform;
+  float w_val;
+  int64_t n;
+  int64_t ntiles;         // ceil(N/32)
+  // state
+  void* states;
+  void* ages;
+  void* inf[2];
+  uint32_t* mask[2];
+  float* pressure;
+  float* rates;
+  fs_scalars* S;
+  // engine scratch
+  unsigned* part_max;
+  int* part_cnt;
+  unsigned* ticket;
+  double* log_clock;
+  double* log_tau;
+  int64_t* log_counts;
+  int64_t log_cap;
+  const float* ptab;
+  const int32_t* active_tiles;   // compaction: tile ids, or nullptr
+  const int64_t* num_active;
+  const float* pre;              // G_PRE: gathered pressure
+  int count_mode;
+  // model / config
+  fs_model model;
+  double eps, tau_max, delta;
+  int rng;
+  int hprec;
+  float inf_val;                 // stored infectivity of an I node (count mode), promoted
+};
+
+struct MergeParams {
+  const int64_t* ro;
+  const int32_t* col;
+  const void* w;
+  int w_bf16;
+  int w_uniform;
+  float w_val;
+  int64_t n;
+  int64_t e;
+  int64_t epb;
+  int64_t nchunks;
+  const int64_t* chunk_first;    // first node whose slice starts at/after chunk start
+  const void* inf[2];            // general gather input (promoted on load)
+  int inf_bf16;
+  const uint32_t* mask[2];       // count gather input
+  const float* ptab;
+  const fs_scalars* S;           // parity source; nullptr -> buffer 0
+  float* out;
+  int64_t nwords;
+};
+
+// ---------------------------------------------------------------------------
+// gather primitives
+// ---------------------------------------------------------------------------
+template <bool SMEM>
+__device__ __forceinline__ int mask_bit(const uint32_t* __restrict__ m, int32_t c) {
+  uint32_t w = SMEM ? m[c >> 5] : __ldg(m + (c >> 5));
+  return (int)((w >> (c & 31)) & 1u);
+}
+
+template <typename IT>
+__device__ __forceinline__ float load_inf(const void* inf, int32_t c) {
+  return to_f32<IT>(__ldg(reinterpret_cast<const IT*>(inf) + c));
+}
+
+__device__ __forceinline__ float load_w(const void* w, int w_bf16, int64_t e) {
+  if (w_bf16) return __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(w) + e));
+  return __ldg(reinterpret_cast<const float*>(w) + e);
+}
+
+// thread-per-node infectious-neighbour count (order-free integer sum)
+template <bool SMEM>
+__device__ __forceinline__ int count_thread(const int32_t* __restrict__ col, const uint32_t* m,
+                                            int64_t lo, int64_t hi) {
+  int cnt = 0;
+  int64_t e = lo;
+  for (; e + 4 <= hi; e += 4) {
+    int32_t c0 = __ldg(col + e), c1 = __ldg(col + e + 1), c2 = __ldg(col + e + 2), c3 = __ldg(col + e + 3);
+    cnt += mask_bit<SMEM>(m, c0) + mask_bit<SMEM>(m, c1) + mask_bit<SMEM>(m, c2) + mask_bit<SMEM>(m, c3);
+  }
+  for (; e < hi; ++e) cnt += mask_bit<SMEM>(m, __ldg(col + e));
+  return cnt;
+}
+
+// warp-cooperative count of one slice; every lane returns the total
+template <bool SMEM>
+__device__ __forceinline__ int count_warp(const int32_t* __restrict__ col, const uint32_t* m,
+                                          int64_t lo, int64_t hi, int lane) {
+  int cnt = 0;
+  for (int64_t e = lo + lane; e < hi; e += 32) cnt += mask_bit<SMEM>(m, __ldg(col + e));
+  return __reduce_add_sync(kFull, cnt);
+}
+
+// thread-per-node sequential f32 fold in CSR order: acc = f32(acc + f32(inf*w))
+// (renewal.py:289 + 60-68; T/test_renewal.py:27-37)
+template <typename IT>
+__device__ __forceinline__ float fold_thread(const int32_t* __restrict__ col, const void* inf,
+                                             const void* w, int w_bf16, int w_uniform, float w_val,
+                                             int64_t lo, int64_t hi) {
+  float acc = 0.0f;
+  for (int64_t e = lo; e < hi; ++e) {
+    float wv = w_uniform ? w_val : load_w(w, w_bf16, e);
+    acc = __fadd_rn(acc, __fmul_rn(load_inf<IT>(inf, __ldg(col + e)), wv));
+  }
+  return acc;
+}
+
+// warp-cooperative fold of one slice, still in CSR order: lanes load 32
+// consecutive contributions, then every lane folds them in lane order
+// (renewal.py:221-242 semantics; padding lanes contribute +0).
+template <typename IT>
+__device__ __forceinline__ float fold_warp(const int32_t* __restrict__ col, const void* inf,
+                                           const void* w, int w_bf16, int w_uniform, float w_val,
+                                           int64_t lo, int64_t hi, int lane) {
+  float acc = 0.0f;
+  for (int64_t base = lo; base < hi; base += 32) {
+    int64_t e = base + lane;
+    float v = 0.0f;
+    if (e < hi) {
+      float wv = w_uniform ? w_val : load_w(w, w_bf16, e);
+      v = __fmul_rn(load_inf<IT>(inf, __ldg(col + e)), wv);
+    }
+    const int live = (hi - base) < 32 ? (int)(hi - base) : 32;
+    for (int l = 0; l < live; ++l) acc = __fadd_rn(acc, __shfl_sync(kFull, v, l));
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------------------
+// the fused step
+// ---------------------------------------------------------------------------
+template <typename ST, typename AT, typename IT, int GATHER, int STRAT, bool MAT, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const StepParams p) {
+  extern __shared__ __align__(16) uint32_t s_mask[];
+  __shared__ int s_succ[FS_MAX_COMPARTMENTS], s_term[FS_MAX_COMPARTMENTS], s_kind[FS_MAX_COMPARTMENTS];
+  __shared__ double s_p0[FS_MAX_COMPARTMENTS], s_p1[FS_MAX_COMPARTMENTS];
+  __shared__ int s_cnt[FS_MAX_COMPARTMENTS];
+  __shared__ float s_wmax[BLOCK / 32];
+  constexpr int WARPS = BLOCK / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int M = p.model.num_compartments;
+
+  if (tid < FS_MAX_COMPARTMENTS) {
+    const fs_compartment& c = p.model.comp[tid];
+    s_succ[tid] = c.succ;
+    s_term[tid] = c.terminal;
+    s_kind[tid] = c.hazard;
+    s_p0[tid] = c.p0;
+    s_p1[tid] = c.p1;
+    s_cnt[tid] = 0;
+  }
+  // step scalars (written by the previous launch's last CTA)
+  const fs_scalars* S = p.S;
+  const double tau = S->tau_next;
+  const int64_t step = S->step;
+  const uint64_t seed = S->seed;
+  const int cur = (int)(step & 1);
+  const uint32_t* mask_cur = p.mask[cur];
+  uint32_t* mask_nxt = p.mask[cur ^ 1];
+  const void* inf_cur = p.inf[cur];
+  IT* inf_nxt = reinterpret_cast<IT*>(p.inf[cur ^ 1]);
+
+  if (GATHER == G_COUNT_SMEM) {
+    // stage the whole infectious mask (N/8 bytes) in shared memory
+    const int64_t nwords = p.ntiles;
+    const int64_t nvec = nwords >> 2;
+    const uint4* src4 = reinterpret_cast<const uint4*>(mask_cur);
+    uint4* dst4 = reinterpret_cast<uint4*>(s_mask);
+    for (int64_t i = tid; i < nvec; i += BLOCK) dst4[i] = __ldg(src4 + i);
+    for (int64_t i = (nvec << 2) + tid; i < nwords; i += BLOCK) s_mask[i] = __ldg(mask_cur + i);
+  }
+  __syncthreads();
+
+  const float tau_f = __double2float_rn(tau);  // np.float32(tau), renewal.py:541
+  const uint64_t key = splitmix_step_key(seed, (uint64_t)step);
+  const int edge_from = p.model.edge_from;
+  const int infectious = p.model.infectious;
+  const int shed = p.model.shedding;
+  const float beta_f = __double2float_rn(p.model.beta);
+  const uint32_t* gmask = (GATHER == G_COUNT_SMEM) ? s_mask : mask_cur;
+  float lmax = 0.0f;
+
+  const int64_t ntiles = p.active_tiles ? *p.num_active : p.ntiles;
+  for (int64_t t = (int64_t)blockIdx.x * WARPS + warp; t < ntiles; t += (int64_t)gridDim.x * WARPS) {
+    const int64_t tile = p.active_tiles ? (int64_t)p.active_tiles[t] : t;
+    const int64_t n = tile * 32 + lane;
+    const bool valid = n < p.n;
+    const int s = valid ? (int)reinterpret_cast<const ST*>(p.states)[n] : -1;
+    const float age = valid ? to_f32<AT>(reinterpret_cast<const AT*>(p.ages)[n]) : 0.0f;
+    const bool isS = (s == edge_from);
+    const bool need = valid && (isS || MAT);
+
+    // ---- (1) pressure gather -------------------------------------------
+    float pressure = 0.0f;
+    if (GATHER == G_PRE) {
+      if (need) pressure = __ldg(p.pre + n);
+    } else {
+      int64_t lo = 0, hi = 0;
+      if (need) { lo = __ldg(p.ro + n); hi = __ldg(p.ro + n + 1); }
+      if (STRAT == S_THREAD) {
+        if (need) {
+          if (GATHER == G_F32) {
+            pressure = fold_thread<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lo, hi);
+          } else {
+            int k = count_thread<GATHER == G_COUNT_SMEM>(p.col, gmask, lo, hi);
+            pressure = __ldg(p.ptab + k);
+          }
+        }
+      } else {
+        unsigned todo = __ballot_sync(kFull, need);
+        while (todo) {
+          const int j = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int64_t lj = __shfl_sync(kFull, lo, j), hj = __shfl_sync(kFull, hi, j);
+          float pj;
+          if (GATHER == G_F32) {
+            pj = fold_warp<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lj, hj, lane);
+          } else {
+            int k = count_warp<GATHER == G_COUNT_SMEM>(p.col, gmask, lj, hj, lane);
+            pj = __ldg(p.ptab + k);
+          }
+          if (lane == j) pressure = pj;
+        }
+      }
+    }
+
+    // ---- (2) rate: pressure for S, f32(r) / hazard(age) otherwise --------
+    float rate = 0.0f;
+    if (valid) {
+      if (isS) rate = pressure;
+      else {
+        const int kind = s_kind[s];
+        if (kind != FS_HZ_NONE) rate = nodal_rate(kind, s_p0[s], s_p1[s], age, p.hprec);
+      }
+    }
+    lmax = fmaxf(lmax, rate);
+
+    // ---- (3) Bernoulli on the counter-based uniform ----------------------
+    bool fire = false;
+    if (rate > 0.0f) {
+      const double u = (p.rng == FS_RNG_SPLITMIX) ? splitmix_uniform(key, (uint64_t)n)
+                                                  : philox_uniform(seed, (uint64_t)step, (uint64_t)n);
+      fire = bernoulli_fire(u, rate, tau);
+    }
+
+    // ---- (4) transition, age reset / advance / freeze --------------------
+    int ns = s;
+    if (valid) {
+      const bool term = s_term[s] != 0;
+      float nage = age;
+      if (fire) {
+        ns = s_succ[s];
+        nage = 0.0f;
+        reinterpret_cast<ST*>(p.states)[n] = (ST)ns;
+        atomicAdd(&s_cnt[ns], 1);
+        atomicAdd(&s_cnt[s], -1);
+      } else if (!term) {
+        nage = __fadd_rn(age, tau_f);
+      }
+      if (fire || !term) reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
+      if (!(GATHER == G_COUNT_SMEM || GATHER == G_COUNT_GLOBAL) && !p.count_mode) {
+        // ---- (5a) next-step infectivity, cast on store (renewal.py:556-575)
+        float v = 0.0f;
+        if (ns == infectious) {
+          if (shed == FS_SHED_CONSTANT) v = beta_f;
+          else v = __double2float_rn(__dmul_rn(p.model.beta,
+                       shedding_f64(shed, p.model.shed_mu, p.model.shed_sigma, p.model.shed_peak, (double)nage)));
+        }
+        inf_nxt[n] = from_f32<IT>(v);
+      }
+      if (MAT) { p.pressure[n] = pressure; p.rates[n] = rate; }
+    }
+    if (GATHER == G_COUNT_SMEM || GATHER == G_COUNT_GLOBAL || p.count_mode) {
+      // ---- (5b) next-step infectious bit-mask, one word per warp tile
+      const unsigned word = __ballot_sync(kFull, valid && ns == infectious);
+      if (lane == 0) mask_nxt[tile] = word;
+    }
+  }
+
+  // ---- (6) block max-rate / count deltas, last CTA folds the partials ----
+#pragma unroll
+  for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(kFull, lmax, o));
+  if (lane == 0) s_wmax[warp] = lmax;
+  __syncthreads();
+  if (warp != 0) return;
+  float bmax = lane < WARPS ? s_wmax[lane] : 0.0f;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(kFull, bmax, o));
+  if (lane == 0) p.part_max[blockIdx.x] = __float_as_uint(bmax);  // rates >= 0: bit order == value order
+  if (lane < FS_MAX_COMPARTMENTS) p.part_cnt[blockIdx.x * kCntStride + lane] = s_cnt[lane];
+  __threadfence();
+  unsigned ticket = 0;
+  if (lane == 0) ticket = atomicAdd(p.ticket, 1u);
+  ticket = __shfl_sync(kFull, ticket, 0);
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  unsigned mbits = 0;
+  for (unsigned b = lane; b < gridDim.x; b += 32) mbits = max(mbits, __ldcg(p.part_max + b));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mbits = max(mbits, __shfl_xor_sync(kFull, mbits, o));
+  const int64_t slot = step % p.log_cap;
+  const double clock1 = S->clock + tau;  // renewal.py:497-498
+  for (int c = 0; c < M; ++c) {
+    long long d = 0;
+    for (unsigned b = lane; b < gridDim.x; b += 32) d += __ldcg(p.part_cnt + b * kCntStride + c);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(kFull, d, o);
+    if (lane == 0) {
+      const int64_t v = p.S->counts[c] + d;
+      p.S->counts[c] = v;
+      p.log_counts[slot * kCntStride + c] = v;
+    }
+  }
+  if (lane == 0) {
+    const float maxf = __uint_as_float(mbits);
+    // tau' = min(tau_max, eps / (max rate + delta)) in f64 (renewal.py:577-578)
+    const double cand = __ddiv_rn(p.eps, __dadd_rn((double)maxf, p.delta));
+    fs_scalars* W = p.S;
+    W->last_max_rate = maxf;
+    W->tau_next = (p.tau_max <= cand) ? p.tau_max : cand;
+    W->clock = clock1;
+    W->step = step + 1;
+    W->started = 1;
+    p.log_clock[slot] = clock1;
+    p.log_tau[slot] = tau;
+    __threadfence();
+    *p.ticket = 0u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// edge-chunked merge gather (renewal.py:245-261, 291-302): warp per chunk of
+// `epb` edges.  A node belongs to the chunk holding its first edge; slices
+// of <= 32 edges are folded by one lane, longer or straddling slices by the
+// whole warp, always in CSR order, so the result is bit-identical to the
+// per-node fold.  Writes pressure for every node owning >= 1 edge.
+// ---------------------------------------------------------------------------
+template <typename IT, int MODE /*0 f32, 1 count-smem, 2 count-global*/, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_gather_merge(const MergeParams q) {
+  extern __shared__ __align__(16) uint32_t s_mask[];
+  constexpr int WARPS = BLOCK / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cur = q.S ? (int)(q.S->step & 1) : 0;
+  const uint32_t* mask_cur = q.mask[cur];
+  const void* inf_cur = q.inf[cur];
+  if (MODE == 1) {
+    const int64_t nvec = q.nwords >> 2;
+    const uint4* src4 = reinterpret_cast<const uint4*>(mask_cur);
+    uint4* dst4 = reinterpret_cast<uint4*>(s_mask);
+    for (int64_t i = tid; i < nvec; i += BLOCK) dst4[i] = __ldg(src4 + i);
+    for (int64_t i = (nvec << 2) + tid; i < q.nwords; i += BLOCK) s_mask[i] = __ldg(mask_cur + i);
+    __syncthreads();
+  }
+  const uint32_t* gmask = (MODE == 1) ? s_mask : mask_cur;
+  for (int64_t c = (int64_t)blockIdx.x * WARPS + warp; c < q.nchunks; c += (int64_t)gridDim.x * WARPS) {
+    const int64_t e1 = min(q.e, (c + 1) * q.epb);
+    const int64_t n_lo = __ldg(q.chunk_first + c), n_hi = __ldg(q.chunk_first + c + 1);
+    for (int64_t base = n_lo; base < n_hi; base += 32) {
+      const int64_t n = base + lane;
+      int64_t lo = 0, hi = 0;
+      if (n < n_hi) { lo = __ldg(q.ro + n); hi = __ldg(q.ro + n + 1); }
+      const bool small = (n < n_hi) && (hi - lo <= 32) && (hi <= e1);
+      if (small) {
+        float v;
+        if (MODE == 0) v = fold_thread<IT>(q.col, inf_cur, q.w, q.w_bf16, q.w_uniform, q.w_val, lo, hi);
+        else v = __ldg(q.ptab + count_thread<MODE == 1>(q.col, gmask, lo, hi));
+        q.out[n] = v;
+      }
+      unsigned big = __ballot_sync(kFull, (n < n_hi) && !small);
+      while (big) {
+        const int j = __ffs(big) - 1;
+        big &= big - 1;
+        const int64_t lj = __shfl_sync(kFull, lo, j), hj = __shfl_sync(kFull, hi, j);
+        float v;
+        if (MODE == 0) v = fold_warp<IT>(q.col, inf_cur, q.w, q.w_bf16, q.w_uniform, q.w_val, lj, hj, lane);
+        else v = __ldg(q.ptab + count_warp<MODE == 1>(q.col, gmask, lj, hj, lane));
+        if (lane == j) q.out[n] = v;
+      }
+    }
+  }
+}
+
+// first node n with row_offsets[n] >= chunk start, for every chunk boundary
+__global__ void k_chunk_first(const int64_t* __restrict__ ro, int64_t n, int64_t e, int64_t epb,
+                              int64_t nchunks, int64_t* __restrict__ out) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= nchunks; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t target = (c == nchunks) ? e + 1 : c * epb;  // last boundary: past the end
+    int64_t lo = 0, hi = n;  // search ro[0..n-1]
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (__ldg(ro + mid) < target) lo = mid + 1; else hi = mid;
+    }
+    out[c] = lo;
+  }
+}
+
+// ptab[k] = k-fold sequential f32 sum of c (count-gather pressure table)
+__global__ void k_ptab(float* ptab, int64_t len, float c) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    float acc = 0.0f;
+    ptab[0] = 0.0f;
+    for (int64_t k = 1; k < len; ++k) { acc = __fadd_rn(acc, c); ptab[k] = acc; }
+  }
+}
+
+// batch prologue (renewal.py:583-597)
+__global__ void k_begin_batch(fs_scalars* S, double tau_max, int carry_tau) {
+  if (threadIdx.x == 0 && blockIdx.x == 0 && !carry_tau) S->tau_next = tau_max;
+}
+
+// compaction refresh at tile granularity: a 32-node tile is active if any of
+// its nodes is non-terminal (renewal.py:426-432 at node granularity; results
+// are identical because terminal nodes do rate-0 work either way)
+template <typename ST>
+__global__ void k_refresh_tiles(const ST* __restrict__ states, int64_t n, int64_t ntiles, uint32_t term_bits,
+                                int32_t* __restrict__ tiles, int64_t* __restrict__ num_active) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t0 = warp_g * 32; t0 < ntiles; t0 += nwarps * 32) {
+    // lane l inspects tile t0 + l
+    const int64_t t = t0 + lane;
+    bool act = false;
+    if (t < ntiles) {
+      for (int k = 0; k < 32; ++k) {
+        const int64_t nd = t * 32 + k;
+        if (nd >= n) break;
+        if (!((term_bits >> (int)states[nd]) & 1u)) { act = true; break; }
+      }
+    }
+    const unsigned b = __ballot_sync(kFull, act);
+    int64_t base = 0;
+    if (lane == 0 && b) base = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(num_active), (unsigned long long)__popc(b));
+    base = __shfl_sync(kFull, base, 0);
+    if (act) tiles[base + __popc(b & ((1u << lane) - 1u))] = (int32_t)t;
+  }
+}
+
+__global__ void k_zero_i64(int64_t* p) { *p = 0; }
+
+// copy the current double-buffer half (parity of S->step) onto the other
+template <typename T>
+__global__ void k_sync_buffers(const fs_scalars* S, T* b0, T* b1, int64_t n) {
+  const int cur = (int)(S->step & 1);
+  const T* src = cur ? b1 : b0;
+  T* dst = cur ? b0 : b1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+template <typename T>
+__global__ void k_fill(T* p, int64_t n, T v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// count mode: mask <- (inf != 0); flags values that are neither 0 nor c
+template <typename IT>
+__global__ void k_load_mask(const IT* __restrict__ inf, int64_t n, float c, uint32_t* m0, uint32_t* m1,
+                            int* bad) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ((n + 31) & ~31LL);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = i < n ? to_f32<IT>(inf[i]) : 0.0f;
+    const bool on = v != 0.0f;
+    if (on && v != c) atomicExch(bad, 1);
+    const unsigned w = __ballot_sync(kFull, on);
+    if (lane == 0) { m0[i >> 5] = w; m1[i >> 5] = w; }
+  }
+}
+
+template <typename IT>
+__global__ void k_store_mask(const uint32_t* __restrict__ m, int64_t n, IT c, IT* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = ((m[i >> 5] >> (i & 31)) & 1u) ? c : from_f32<IT>(0.0f);
+}
+
+// ---------------------------------------------------------------------------
+// kernel selection
+// ---------------------------------------------------------------------------
+using StepFn = void (*)(const StepParams);
+using MergeFn = void (*)(const MergeParams);
+
+template <typename ST, typename AT, typename IT, bool MAT>
+StepFn pick_step2(int gather, int strat, int& block) {
+  switch (gather) {
+    case G_COUNT_SMEM:
+      block = 1024;
+      return strat == S_WARP ? k_step<ST, AT, IT, G_COUNT_SMEM, S_WARP, MAT, 1024>
+                             : k_step<ST, AT, IT, G_COUNT_SMEM, S_THREAD, MAT, 1024>;
+    case G_COUNT_GLOBAL:
+      block = 512;
+      return strat == S_WARP ? k_step<ST, AT, IT, G_COUNT_GLOBAL, S_WARP, MAT, 512>
+                             : k_step<ST, AT, IT, G_COUNT_GLOBAL, S_THREAD, MAT, 512>;
+    case G_F32:
+      block = 512;
+      return strat == S_WARP ? k_step<ST, AT, IT, G_F32, S_WARP, MAT, 512>
+                             : k_step<ST, AT, IT, G_F32, S_THREAD, MAT, 512>;
+    default:
+      block = 512;
+      return k_step<ST, AT, IT, G_PRE, S_THREAD, MAT, 512>;
+  }
+}
+
+StepFn pick_step(bool mixed, int gather, int strat, bool mat, int& block) {
+  if (mixed)
+    return mat ? pick_step2<int8_t, __half, __nv_bfloat16, true>(gather, strat, block)
+               : pick_step2<int8_t, __half, __nv_bfloat16, false>(gather, strat, block);
+  return mat ? pick_step2<int32_t, float, float, true>(gather, strat, block)
+             : pick_step2<int32_t, float, float, false>(gather, strat, block);
+}
+
+MergeFn pick_merge(bool inf_bf16, int mode, int& block) {
+  if (mode == 1) { block = 1024; return inf_bf16 ? k_gather_merge<__nv_bfloat16, 1, 1024> : k_gather_merge<float, 1, 1024>; }
+  block = 512;
+  if (mode == 2) return inf_bf16 ? k_gather_merge<__nv_bfloat16, 2, 512> : k_gather_merge<float, 2, 512>;
+  return inf_bf16 ? k_gather_merge<__nv_bfloat16, 0, 512> : k_gather_merge<float, 0, 512>;
+}
+
+}  // namespace fs
+
+// ===========================================================================
+// engine object + C ABI
+// ===========================================================================
+using namespace fs;
+
+struct fs_engine {
+  int device = 0;
+  int sms = 0;
+  fs_graph g{};
+  fs_model m{};
+  fs_config c{};
+  fs_state_buffers b{};
+  bool count_mode = false;
+  bool mask_smem = false;
+  bool mixed = false;
+  int gather = G_F32;
+  int strat = S_THREAD;
+  bool merge = false;
+  int64_t ntiles = 0;
+  float inf_val = 0.0f;  // promoted stored value of an I node (count mode)
+  // launch shapes
+  StepFn step_fn[2] = {nullptr, nullptr};
+  int step_block = 512, step_grid = 0;
+  size_t step_smem = 0;
+  MergeFn merge_fn = nullptr;
+  int merge_block = 512, merge_grid = 0;
+  size_t merge_smem = 0;
+  int64_t nchunks = 0;
+  // engine-owned device scratch
+  fs_scalars* S = nullptr;
+  unsigned* part_max = nullptr;
+  int* part_cnt = nullptr;
+  unsigned* ticket = nullptr;
+  double* log_clock = nullptr;
+  double* log_tau = nullptr;
+  int64_t* log_counts = nullptr;
+  int64_t log_cap = 0;
+  float* ptab = nullptr;
+  int64_t ptab_len = 0;
+  int32_t* active_tiles = nullptr;
+  int64_t* num_active = nullptr;
+  int64_t* chunk_first = nullptr;
+  float* pre = nullptr;
+  int* bad_flag = nullptr;
+  // CUDA graphs of one batch (index: materialise last step)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t batch_exec[2] = {nullptr, nullptr};
+  bool compaction_ready = false;
+};
+
+namespace {
+
+#define FS_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t err__ = (call);                                                               \
+    if (err__ != cudaSuccess)                                                                 \
+      return set_error(FS_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(err__), \
+                       __FILE__, __LINE__);                                                   \
+  } while (0)
+
+template <typename T>
+int dalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t err = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (err != cudaSuccess) return set_error(FS_ENOMEM, "cudaMalloc(%zu B): %s", count * sizeof(T), cudaGetErrorString(err));
+  return 0;
+}
+
+StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active) {
+  StepParams p{};
+  p.ro = e->g.row_offsets;
+  p.col = e->g.col_indices;
+  p.w = e->g.weights;
+  p.w_bf16 = e->g.weights_dtype == FS_BF16;
+  p.w_uniform = e->g.weights_uniform;
+  p.w_val = e->g.uniform_weight;
+  p.n = e->g.num_nodes;
+  p.ntiles = e->ntiles;
+  p.states = e->b.states;
+  p.ages = e->b.ages;
+  p.inf[0] = e->b.infectivity[0];
+  p.inf[1] = e->b.infectivity[1];
+  p.mask[0] = e->b.imask[0];
+  p.mask[1] = e->b.imask[1];
+  p.pressure = e->b.pressure;
+  p.rates = e->b.rates;
+  p.S = e->S;
+  p.part_max = e->part_max;
+  p.part_cnt = e->part_cnt;
+  p.ticket = e->ticket;
+  p.log_clock = e->log_clock;
+  p.log_tau = e->log_tau;
+  p.log_counts = e->log_counts;
+  p.log_cap = e->log_cap;
+  p.ptab = e->ptab;
+  p.active_tiles = (use_active && e->c.compaction) ? e->active_tiles : nullptr;
+  p.num_active = e->num_active;
+  p.pre = use_pre ? e->pre : nullptr;
+  p.count_mode = e->count_mode;
+  p.model = e->m;
+  p.eps = e->c.epsilon;
+  p.tau_max = e->c.tau_max;
+  p.delta = e->c.delta;
+  p.rng = e->c.rng;
+  p.hprec = e->c.hazard_precision;
+  p.inf_val = e->inf_val;
+  return p;
+}
+
+MergeParams make_merge_params(const fs_engine* e) {
+  MergeParams q{};
+  q.ro = e->g.row_offsets;
+  q.col = e->g.col_indices;
+  q.w = e->g.weights;
+  q.w_bf16 = e->g.weights_dtype == FS_BF16;
+  q.w_uniform = e->g.weights_uniform;
+  q.w_val = e->g.uniform_weight;
+  q.n = e->g.num_nodes;
+  q.e = e->g.num_edges;
+  q.epb = e->c.edges_per_block;
+  q.nchunks = e->nchunks;
+  q.chunk_first = e->chunk_first;
+  q.inf[0] = e->b.infectivity[0];
+  q.inf[1] = e->b.infectivity[1];
+  q.inf_bf16 = e->mixed;
+  q.mask[0] = e->b.imask[0];
+  q.mask[1] = e->b.imask[1];
+  q.ptab = e->ptab;
+  q.S = e->S;
+  q.out = e->pre;
+  q.nwords = e->ntiles;
+  return q;
+}
+
+int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_active, cudaStream_t st) {
+  for (int k = 0; k < nsteps; ++k) {
+    const bool mat = materialize_last && (k == nsteps - 1);
+    if (e->merge) {
+      MergeParams q = make_merge_params(e);
+      e->merge_fn<<<e->merge_grid, e->merge_block, e->merge_smem, st>>>(q);
+    }
+    StepParams p = make_step_params(e, e->merge, use_active);
+    e->step_fn[mat]<<<e->step_grid, e->step_block, e->step_smem, st>>>(p);
+  }
+  FS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_begin_batch(fs_engine* e, cudaStream_t st) {
+  k_begin_batch<<<1, 32, 0, st>>>(e->S, e->c.tau_max, e->c.carry_tau);
+  if (e->c.compaction) {
+    uint32_t term_bits = 0;
+    for (int i = 0; i < e->m.num_compartments; ++i)
+      if (e->m.comp[i].terminal) term_bits |= 1u << i;
+    const int64_t n = e->g.num_nodes;
+    // rates are zeroed once per batch under compaction (renewal.py:594)
+    if (e->b.rates) k_fill<float><<<e->sms * 4, 256, 0, st>>>(e->b.rates, n, 0.0f);
+    if (e->b.pressure) k_fill<float><<<e->sms * 4, 256, 0, st>>>(e->b.pressure, n, 0.0f);
+    k_zero_i64<<<1, 1, 0, st>>>(e->num_active);
+    const int blocks = (int)std::min<int64_t>((e->ntiles + 255) / 256 + 1, (int64_t)e->sms * 8);
+    if (e->mixed)
+      k_refresh_tiles<int8_t><<<blocks, 256, 0, st>>>((const int8_t*)e->b.states, n, e->ntiles, term_bits,
+                                                      e->active_tiles, e->num_active);
+    else
+      k_refresh_tiles<int32_t><<<blocks, 256, 0, st>>>((const int32_t*)e->b.states, n, e->ntiles, term_bits,
+                                                       e->active_tiles, e->num_active);
+    // inactive tiles are never rewritten: make both buffers agree on them
+    const int blocks2 = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
+    if (e->count_mode)
+      k_sync_buffers<uint32_t><<<blocks2, 256, 0, st>>>(e->S, e->b.imask[0], e->b.imask[1], e->ntiles);
+    else if (e->mixed)
+      k_sync_buffers<__nv_bfloat16><<<blocks2, 256, 0, st>>>(e->S, (__nv_bfloat16*)e->b.infectivity[0],
+                                                             (__nv_bfloat16*)e->b.infectivity[1], n);
+    else
+      k_sync_buffers<float><<<blocks2, 256, 0, st>>>(e->S, (float*)e->b.infectivity[0], (float*)e->b.infectivity[1], n);
+  }
+  FS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fs_abi_version(void) { return FS_ABI_VERSION; }
+const char* fs_last_error(void) { return g_last_error.c_str(); }
+
+int fs_device_sm_count(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return v;
+}
+
+int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, const fs_state_buffers* buf,
+                     const fs_scalars* scal, int device, fs_engine** out) {
+  if (!g || !m || !c || !buf || !scal || !out) return set_error(FS_EINVAL, "null argument");
+  *out = nullptr;
+  if (g->num_nodes < 1 || g->num_nodes > 2147483647LL) return set_error(FS_EINVAL, "num_nodes %lld outside [1, 2^31-1]", (long long)g->num_nodes);
+  if (m->num_compartments < 1 || m->num_compartments > FS_MAX_COMPARTMENTS)
+    return set_error(FS_EINVAL, "num_compartments %d outside [1, %d]", m->num_compartments, FS_MAX_COMPARTMENTS);
+  if (c->strategy < FS_PER_NODE || c->strategy > FS_MERGE) return set_error(FS_EINVAL, "strategy must be resolved (got %d)", c->strategy);
+  if (c->steps_per_batch < 1) return set_error(FS_EINVAL, "steps_per_batch must be >= 1");
+  if (c->edges_per_block < 1) return set_error(FS_EINVAL, "edges_per_block must be >= 1");
+  if (!buf->states || !buf->ages) return set_error(FS_EINVAL, "state buffers missing");
+  FS_CUDA(cudaSetDevice(device));
+  fs_engine* e = new fs_engine();
+  e->device = device;
+  e->sms = fs_device_sm_count(device);
+  e->g = *g;
+  e->m = *m;
+  e->c = *c;
+  e->b = *buf;
+  e->mixed = c->mixed_precision != 0;
+  const int64_t n = g->num_nodes;
+  e->ntiles = (n + 31) / 32;
+  const bool can_count = (m->shedding == FS_SHED_CONSTANT) && (g->weights_uniform || g->num_edges == 0);
+  e->count_mode = can_count && c->count_gather != 0;
+  if (c->count_gather == 1 && !can_count) { delete e; return set_error(FS_EINVAL, "count gather requires constant transmission and uniform weights"); }
+  if (e->count_mode && (!buf->imask[0] || !buf->imask[1])) { delete e; return set_error(FS_EINVAL, "count gather needs the two mask buffers"); }
+  if (!e->count_mode && (!buf->infectivity[0] || !buf->infectivity[1])) { delete e; return set_error(FS_EINVAL, "f32 gather needs the two infectivity buffers"); }
+  // stored value of an infectious node and the per-edge contribution
+  {
+    float bf = (float)m->beta;
+    if (e->mixed) bf = __bfloat162float(__float2bfloat16_rn(bf));
+    e->inf_val = bf;
+  }
+  e->mask_smem = e->count_mode && (size_t)e->ntiles * 4 <= kMaxSmemMaskBytes;
+  e->merge = c->strategy == FS_MERGE && g->num_edges > 0;
+  e->strat = c->strategy == FS_LANE ? S_WARP : S_THREAD;
+  if (e->merge) e->gather = G_PRE;
+  else if (e->count_mode) e->gather = e->mask_smem ? G_COUNT_SMEM : G_COUNT_GLOBAL;
+  else e->gather = G_F32;
+
+  int rc = 0;
+#define TRY(x) do { rc = (x); if (rc) { fs_engine_destroy(e); return rc; } } while (0)
+  for (int mat = 0; mat < 2; ++mat) e->step_fn[mat] = pick_step(e->mixed, e->gather, e->strat, mat != 0, e->step_block);
+  e->step_smem = (e->gather == G_COUNT_SMEM) ? (size_t)e->ntiles * 4 : 0;
+  int occ = 1;
+  for (int mat = 0; mat < 2; ++mat) {
+    if (e->step_smem > 0)
+      TRY(cudaFuncSetAttribute((const void*)e->step_fn[mat], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->step_smem) == cudaSuccess ? 0 : set_error(FS_ECUDA, "smem attribute"));
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)e->step_fn[1], e->step_block, e->step_smem) != cudaSuccess || occ < 1) occ = 1;
+  // the step loops over 32-node tiles; do not launch CTAs with no tile
+  {
+    const int64_t warps_needed = e->ntiles;
+    const int64_t ctas_needed = (warps_needed + e->step_block / 32 - 1) / (e->step_block / 32);
+    e->step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sms * occ, ctas_needed));
+  }
+  if (e->merge) {
+    const int mode = e->count_mode ? (e->mask_smem ? 1 : 2) : 0;
+    e->merge_fn = pick_merge(e->mixed, mode, e->merge_block);
+    e->merge_smem = mode == 1 ? (size_t)e->ntiles * 4 : 0;
+    if (e->merge_smem)
+      TRY(cudaFuncSetAttribute((const void*)e->merge_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->merge_smem) == cudaSuccess ? 0 : set_error(FS_ECUDA, "smem attribute"));
+    int mocc = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mocc, (const void*)e->merge_fn, e->merge_block, e->merge_smem) != cudaSuccess || mocc < 1) mocc = 1;
+    e->nchunks = (g->num_edges + c->edges_per_block - 1) / c->edges_per_block;
+    const int64_t ctas_needed = (e->nchunks + e->merge_block / 32 - 1) / (e->merge_block / 32);
+    e->merge_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sms * mocc, ctas_needed));
+  }
+
+  TRY(dalloc(&e->S, 1));
+  TRY(dalloc(&e->part_max, e->step_grid));
+  TRY(dalloc(&e->part_cnt, (size_t)e->step_grid * kCntStride));
+  TRY(dalloc(&e->ticket, 1));
+  e->log_cap = std::max<int64_t>(256, 4 * (int64_t)c->steps_per_batch);
+  TRY(dalloc(&e->log_clock, e->log_cap));
+  TRY(dalloc(&e->log_tau, e->log_cap));
+  TRY(dalloc(&e->log_counts, (size_t)e->log_cap * kCntStride));
+  TRY(dalloc(&e->num_active, 1));
+  TRY(dalloc(&e->bad_flag, 1));
+  if (c->compaction) TRY(dalloc(&e->active_tiles, e->ntiles));
+  FS_CUDA(cudaMemset(e->ticket, 0, sizeof(unsigned)));
+  FS_CUDA(cudaMemset(e->num_active, 0, sizeof(int64_t)));
+  FS_CUDA(cudaMemcpy(e->S, scal, sizeof(fs_scalars), cudaMemcpyHostToDevice));
+  if (e->count_mode) {
+    e->ptab_len = (int64_t)g->d_max + 1;
+    TRY(dalloc(&e->ptab, e->ptab_len));
+    volatile float a_ = e->inf_val, w_ = g->uniform_weight;
+    const float cval = a_ * w_;  // f32(inf * w): one IEEE single multiply
+    k_ptab<<<1, 1>>>(e->ptab, e->ptab_len, cval);
+  }
+  if (e->merge) {
+    TRY(dalloc(&e->chunk_first, e->nchunks + 1));
+    TRY(dalloc(&e->pre, n));
+    FS_CUDA(cudaMemset(e->pre, 0, n * sizeof(float)));
+    k_chunk_first<<<(int)std::min<int64_t>((e->nchunks + 256) / 256, 4096), 256>>>(g->row_offsets, n, g->num_edges,
+                                                                                  c->edges_per_block, e->nchunks, e->chunk_first);
+  }
+  FS_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+  FS_CUDA(cudaGetLastError());
+  FS_CUDA(cudaDeviceSynchronize());
+#undef TRY
+  *out = e;
+  return 0;
+}
+
+void fs_engine_destroy(fs_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  for (auto& x : e->batch_exec) if (x) cudaGraphExecDestroy(x);
+  if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+  void* ptrs[] = {e->S, e->part_max, e->part_cnt, e->ticket, e->log_clock, e->log_tau, e->log_counts, e->ptab,
+                  e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag};
+  for (void* q : ptrs) if (q) cudaFree(q);
+  delete e;
+}
+
+int fs_engine_uses_count_gather(const fs_engine* e) { return e && e->count_mode ? 1 : 0; }
+
+int fs_engine_current_buffer(fs_engine* e, void* stream) {
+  fs_scalars s;
+  int rc = fs_engine_get_scalars(e, &s, stream);
+  if (rc) return rc;
+  return (int)(s.step & 1);
+}
+
+int fs_engine_begin_batch(fs_engine* e, void* stream) {
+  if (!e) return set_error(FS_EINVAL, "null engine");
+  FS_CUDA(cudaSetDevice(e->device));
+  return launch_begin_batch(e, (cudaStream_t)stream);
+}
+
+int fs_engine_step(fs_engine* e, int32_t nsteps, int32_t materialize, int32_t use_active, void* stream) {
+  if (!e) return set_error(FS_EINVAL, "null engine");
+  if (nsteps < 0) return set_error(FS_EINVAL, "nsteps < 0");
+  if (materialize && (!e->b.pressure || !e->b.rates)) return set_error(FS_EINVAL, "materialize needs pressure/rates buffers");
+  FS_CUDA(cudaSetDevice(e->device));
+  if (use_active && !e->c.compaction) return set_error(FS_EINVAL, "engine built without compaction");
+  return launch_steps(e, nsteps, materialize != 0, use_active != 0, (cudaStream_t)stream);
+}
+
+int fs_engine_run_batch(fs_engine* e, int32_t materialize, void* stream) {
+  if (!e) return set_error(FS_EINVAL, "null engine");
+  if (materialize && (!e->b.pressure || !e->b.rates)) return set_error(FS_EINVAL, "materialize needs pressure/rates buffers");
+  FS_CUDA(cudaSetDevice(e->device));
+  const int k = materialize ? 1 : 0;
+  if (!e->batch_exec[k]) {
+    cudaGraph_t graph = nullptr;
+    FS_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = launch_begin_batch(e, e->cap_stream);
+    if (!rc) rc = launch_steps(e, e->c.steps_per_batch, materialize != 0, e->c.compaction != 0, e->cap_stream);
+    cudaError_t err = cudaStreamEndCapture(e->cap_stream, &graph);
+    if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+    if (err != cudaSuccess) return set_error(FS_ECUDA, "graph capture: %s", cudaGetErrorString(err));
+    err = cudaGraphInstantiate(&e->batch_exec[k], graph, 0);
+    cudaGraphDestroy(graph);
+    if (err != cudaSuccess) return set_error(FS_ECUDA, "graph instantiate: %s", cudaGetErrorString(err));
+  }
+  FS_CUDA(cudaGraphLaunch(e->batch_exec[k], (cudaStream_t)stream));
+  return 0;
+}
+
+int fs_engine_read_log(fs_engine* e, int64_t first_step, int32_t n, double* clocks, double* taus, int64_t* counts,
+                       void* stream) {
+  if (!e || n < 0) return set_error(FS_EINVAL, "bad log request");
+  if (n > e->log_cap) return set_error(FS_EINVAL, "log request of %d steps exceeds capacity %lld", n, (long long)e->log_cap);
+  FS_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<double> lc(e->log_cap), lt(e->log_cap);
+  std::vector<int64_t> lk((size_t)e->log_cap * kCntStride);
+  FS_CUDA(cudaMemcpyAsync(lc.data(), e->log_clock, lc.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FS_CUDA(cudaMemcpyAsync(lt.data(), e->log_tau, lt.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FS_CUDA(cudaMemcpyAsync(lk.data(), e->log_counts, lk.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FS_CUDA(cudaStreamSynchronize(st));
+  const int M = e->m.num_compartments;
+  for (int i = 0; i < n; ++i) {
+    const int64_t slot = (first_step + i) % e->log_cap;
+    if (clocks) clocks[i] = lc[slot];
+    if (taus) taus[i] = lt[slot];
+    if (counts) for (int c2 = 0; c2 < M; ++c2) counts[(size_t)i * M + c2] = lk[slot * kCntStride + c2];
+  }
+  return 0;
+}
+
+int fs_engine_get_scalars(fs_engine* e, fs_scalars* out, void* stream) {
+  if (!e || !out) return set_error(FS_EINVAL, "null argument");
+  FS_CUDA(cudaSetDevice(e->device));
+  FS_CUDA(cudaMemcpyAsync(out, e->S, sizeof(fs_scalars), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  FS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return 0;
+}
+
+int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream) {
+  if (!e || !in) return set_error(FS_EINVAL, "null argument");
+  FS_CUDA(cudaSetDevice(e->device));
+  FS_CUDA(cudaMemcpyAsync(e->S, in, sizeof(fs_scalars), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  FS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return 0;
+}
+
+int fs_engine_load_infectivity(fs_engine* e, const void* inf, void* stream) {
+  if (!e || !inf) return set_error(FS_EINVAL, "null argument");
+  FS_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = e->g.num_nodes;
+  if (e->count_mode) {
+    FS_CUDA(cudaMemsetAsync(e->bad_flag, 0, sizeof(int), st));
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
+    if (e->mixed)
+      k_load_mask<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)inf, n, e->inf_val, e->b.imask[0], e->b.imask[1], e->bad_flag);
+    else
+      k_load_mask<float><<<blocks, 256, 0, st>>>((const float*)inf, n, e->inf_val, e->b.imask[0], e->b.imask[1], e->bad_flag);
+    int bad = 0;
+    FS_CUDA(cudaMemcpyAsync(&bad, e->bad_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FS_CUDA(cudaStreamSynchronize(st));
+    if (bad) return set_error(FS_EREPR, "infectivity values are not in {0, beta}: the count gather cannot represent them");
+    return 0;
+  }
+  const size_t bytes = (size_t)n * (e->mixed ? 2 : 4);
+  FS_CUDA(cudaMemcpyAsync(e->b.infectivity[0], inf, bytes, cudaMemcpyDeviceToDevice, st));
+  FS_CUDA(cudaMemcpyAsync(e->b.infectivity[1], inf, bytes, cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+int fs_engine_store_infectivity(fs_engine* e, void* out, void* stream) {
+  if (!e || !out) return set_error(FS_EINVAL, "null argument");
+  FS_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  fs_scalars s;
+  int rc = fs_engine_get_scalars(e, &s, stream);
+  if (rc) return rc;
+  const int cur = (int)(s.step & 1);
+  const int64_t n = e->g.num_nodes;
+  if (e->count_mode) {
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
+    if (e->mixed)
+      k_store_mask<__nv_bfloat16><<<blocks, 256, 0, st>>>(e->b.imask[cur], n, __float2bfloat16_rn(e->inf_val), (__nv_bfloat16*)out);
+    else
+      k_store_mask<float><<<blocks, 256, 0, st>>>(e->b.imask[cur], n, e->inf_val, (float*)out);
+    FS_CUDA(cudaGetLastError());
+    return 0;
+  }
+  FS_CUDA(cudaMemcpyAsync(out, e->b.infectivity[cur], (size_t)n * (e->mixed ? 2 : 4), cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// standalone pressure gather (renewal.py:264-313) on a caller buffer
+// ---------------------------------------------------------------------------
+namespace fs {
+template <typename IT, int STRAT>
+__global__ void __launch_bounds__(256) k_gather_nodes(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
+                                                      const void* w, int w_bf16, int w_uniform, float w_val,
+                                                      const void* inf, int64_t n, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp_g; t * 32 < n; t += nwarps) {
+    const int64_t i = t * 32 + lane;
+    int64_t lo = 0, hi = 0;
+    if (i < n) { lo = __ldg(ro + i); hi = __ldg(ro + i + 1); }
+    if (STRAT == S_THREAD) {
+      if (i < n) out[i] = fold_thread<IT>(col, inf, w, w_bf16, w_uniform, w_val, lo, hi);
+    } else {
+      unsigned todo = __ballot_sync(kFull, i < n);
+      float mine = 0.0f;
+      while (todo) {
+        const int j = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int64_t lj = __shfl_sync(kFull, lo, j), hj = __shfl_sync(kFull, hi, j);
+        const float v = fold_warp<IT>(col, inf, w, w_bf16, w_uniform, w_val, lj, hj, lane);
+        if (lane == j) mine = v;
+      }
+      if (i < n) out[i] = mine;
+    }
+  }
+}
+}  // namespace fs
+
+extern "C" int fs_pressure_gather(const fs_graph* g, const void* inf, int32_t inf_dtype, float* out,
+                                  int32_t strategy, int32_t lanes_per_node, int32_t edges_per_block,
+                                  void* stream) {
+  (void)lanes_per_node;  // lane width changes the partition only, never the bits
+  if (!g || !out) return set_error(FS_EINVAL, "null argument");
+  if (inf_dtype != FS_F32 && inf_dtype != FS_BF16) return set_error(FS_EINVAL, "infectivity dtype must be f32 or bf16");
+  if (strategy < FS_PER_NODE || strategy > FS_MERGE) return set_error(FS_EINVAL, "strategy must be resolved");
+  const int64_t n = g->num_nodes;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0) return 0;
+  if (g->num_edges == 0) { FS_CUDA(cudaMemsetAsync(out, 0, n * sizeof(float), st)); return 0; }
+  if (!inf) return set_error(FS_EINVAL, "null infectivity");
+  const bool bf = inf_dtype == FS_BF16;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    sms = std::max(1, fs_device_sm_count(dev));
+  }
+  if (strategy == FS_MERGE) {
+    if (edges_per_block < 1) return set_error(FS_EINVAL, "edges_per_block must be >= 1");
+    const int64_t nchunks = (g->num_edges + edges_per_block - 1) / edges_per_block;
+    int64_t* cf = nullptr;
+    FS_CUDA(cudaMallocAsync((void**)&cf, (nchunks + 1) * sizeof(int64_t), st));
+    FS_CUDA(cudaMemsetAsync(out, 0, n * sizeof(float), st));
+    k_chunk_first<<<(int)std::min<int64_t>((nchunks + 256) / 256, 4096), 256, 0, st>>>(g->row_offsets, n, g->num_edges,
+                                                                                      edges_per_block, nchunks, cf);
+    MergeParams q{};
+    q.ro = g->row_offsets;
+    q.col = g->col_indices;
+    q.w = g->weights;
+    q.w_bf16 = g->weights_dtype == FS_BF16;
+    q.w_uniform = g->weights_uniform;
+    q.w_val = g->uniform_weight;
+    q.n = n;
+    q.e = g->num_edges;
+    q.epb = edges_per_block;
+    q.nchunks = nchunks;
+    q.chunk_first = cf;
+    q.inf[0] = q.inf[1] = inf;
+    q.inf_bf16 = bf;
+    q.S = nullptr;
+    q.out = out;
+    int block = 512;
+    MergeFn fn = pick_merge(bf, 0, block);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nchunks + block / 32 - 1) / (block / 32), (int64_t)sms * 2));
+    fn<<<grid, block, 0, st>>>(q);
+    FS_CUDA(cudaFreeAsync(cf, st));
+  } else {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+    const int s = strategy == FS_LANE ? S_WARP : S_THREAD;
+    if (bf) {
+      if (s == S_WARP) k_gather_nodes<__nv_bfloat16, S_WARP><<<grid, 256, 0, st>>>(g->row_offsets, g->col_indices, g->weights, g->weights_dtype == FS_BF16, g->weights_uniform, g->uniform_weight, inf, n, out);
+      else k_gather_nodes<__nv_bfloat16, S_THREAD><<<grid, 256, 0, st>>>(g->row_offsets, g->col_indices, g->weights, g->weights_dtype == FS_BF16, g->weights_uniform, g->uniform_weight, inf, n, out);
+    } else {
+      if (s == S_WARP) k_gather_nodes<float, S_WARP><<<grid, 256, 0, st>>>(g->row_offsets, g->col_indices, g->weights, g->weights_dtype == FS_BF16, g->weights_uniform, g->uniform_weight, inf, n, out);
+      else k_gather_nodes<float, S_THREAD><<<grid, 256, 0, st>>>(g->row_offsets, g->col_indices, g->weights, g->weights_dtype == FS_BF16, g->weights_uniform, g->uniform_weight, inf, n, out);
+    }
+  }
+  FS_CUDA(cudaGetLastError());
+  return 0;
+}
