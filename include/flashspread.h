@@ -73,6 +73,8 @@ typedef struct fs_graph {
   int64_t num_nodes;
   int64_t num_edges;
   const int64_t* row_offsets;   /* device, int64[N+1] (graph.py:77-93)        */
+  const int32_t* row_offsets32; /* optional int32 copy (E < 2^31) read by the
+                                   hot kernels instead; NULL = use row_offsets */
   const int32_t* col_indices;   /* device, int32[E], slices sorted by source  */
   const void* weights;          /* device, f32[E] or bf16[E]; NULL if uniform */
   int32_t weights_dtype;        /* FS_F32 | FS_BF16                           */
@@ -136,7 +138,8 @@ typedef struct fs_state_buffers {
   void* ages;            /* f32[N]   (f16[N] mixed)                          */
   void* infectivity[2];  /* general gather: f32/bf16[N] double buffer         */
   uint32_t* imask[2];    /* count gather: infectious bit-mask double buffer,
-                            uint32[ceil(N/32)] each                          */
+                            uint32[ceil(N/32)] each, allocated to a 16-byte
+                            multiple and 16-byte aligned (TMA bulk staging) */
   float* pressure;       /* f32[N], written on materialising steps            */
   float* rates;          /* f32[N], written on materialising steps            */
 } fs_state_buffers;

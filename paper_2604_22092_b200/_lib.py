@@ -43,6 +43,7 @@ class FsGraph(ctypes.Structure):
         ("num_nodes", _c_i64),
         ("num_edges", _c_i64),
         ("row_offsets", _vp),
+        ("row_offsets32", _vp),
         ("col_indices", _vp),
         ("weights", _vp),
         ("weights_dtype", _c_i32),

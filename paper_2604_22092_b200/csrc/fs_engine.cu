@@ -47,7 +47,7 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kCntStride = FS_MAX_COMPARTMENTS;
 // shared-memory budget for the staged mask: leaves room for the static
 // tables on a 227 KB CTA
-constexpr size_t kMaxSmemMaskBytes = 220u * 1024u;
+constexpr size_t kMaxSmemMaskBytes = 188u * 1024u;  // + ~34 KB static (queues) <= 227 KB
 
 enum Gather { G_COUNT_SMEM = 0, G_COUNT_GLOBAL = 1, G_F32 = 2, G_PRE = 3 };
 enum Strat { S_THREAD = 0, S_WARP = 1 };
@@ -55,6 +55,7 @@ enum Strat { S_THREAD = 0, S_WARP = 1 };
 struct StepParams {
   // graph (renewal.py:264-313 inputs)
   const int64_t* ro;
+  const int32_t* ro32;     // int32 offsets when E < 2^31, else nullptr
   const int32_t* col;
   const void* w;          // f32 or bf16; unused when uniform
   int w_bf16;
@@ -79,6 +80,8 @@ struct StepParams {
   int64_t* log_counts;
   int64_t log_cap;
   const float* ptab;
+  int ptab_mul;                  // ptab[k] == f32(k * c) for every k <= d_max
+  float ptab_c;
   const int32_t* active_tiles;   // compaction: tile ids, or nullptr
   const int64_t* num_active;
   const float* pre;              // G_PRE: gathered pressure
@@ -93,6 +96,7 @@ struct StepParams {
 
 struct MergeParams {
   const int64_t* ro;
+  const int32_t* ro32;
   const int32_t* col;
   const void* w;
   int w_bf16;
@@ -154,6 +158,117 @@ __device__ __forceinline__ int count_warp(const int32_t* __restrict__ col, const
   return __reduce_add_sync(kFull, cnt);
 }
 
+// ---------------------------------------------------------------------------
+// TMA bulk staging of the infectious mask (cp.async.bulk + mbarrier)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// one elected thread launches the copy of `bytes` (16-byte multiple) in
+// <= 64 KB pieces; every thread later waits on the barrier's phase 0
+__device__ __forceinline__ void stage_mask_async(uint32_t* dst, const uint32_t* src, uint32_t bytes, uint64_t* bar) {
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(bar, bytes);
+    for (uint32_t off = 0; off < bytes; off += 65536u) {
+      const uint32_t len = min(65536u, bytes - off);
+      tma_bulk_g2s(reinterpret_cast<char*>(dst) + off, reinterpret_cast<const char*>(src) + off, len, bar);
+    }
+  }
+}
+
+// [lo, hi) of node n: int32 copy when present; neighbouring lanes share
+// boundaries, so each lane loads one offset and takes hi from lane+1
+__device__ __forceinline__ void load_slice(const int64_t* __restrict__ ro, const int32_t* __restrict__ ro32,
+                                           int64_t n, bool valid, int lane, int64_t& lo, int64_t& hi) {
+  int64_t v = 0;
+  if (valid) v = ro32 ? (int64_t)__ldg(ro32 + n) : __ldg(ro + n);
+  int64_t up = __shfl_down_sync(0xffffffffu, v, 1);
+  const int next_valid = __shfl_down_sync(0xffffffffu, (int)valid, 1);
+  if (valid && (lane == 31 || !next_valid)) up = ro32 ? (int64_t)__ldg(ro32 + n + 1) : __ldg(ro + n + 1);
+  lo = v;
+  hi = valid ? up : v;
+}
+
+// tile-cooperative count: the warp streams the contiguous edge range of its
+// 32 nodes 32 edges per group (coalesced loads, 8 groups in flight), tests
+// the sources in the mask and ballots.  Lane g keeps group g's ballot word;
+// afterwards every lane fetches only the words its own slice spans and
+// popcounts them.  Integer counts are order-free: exact for any partition.
+__device__ __forceinline__ uint32_t bmsk(int start, int width) {
+  uint32_t r;
+  asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(r) : "r"(start), "r"(width));
+  return r;
+}
+
+template <bool SMEM>
+__device__ __forceinline__ int count_tile(const int32_t* __restrict__ col, const uint32_t* m, int64_t lo, int64_t hi,
+                                          bool need, unsigned need_mask, int lane) {
+  const int j0 = __ffs(need_mask) - 1, j1 = 31 - __clz(need_mask);
+  const int64_t E0 = __shfl_sync(0xffffffffu, lo, j0), E1 = __shfl_sync(0xffffffffu, hi, j1);
+  const int32_t* __restrict__ cp = col + E0;
+  const int L = (int)(E1 - E0);
+  // my slice relative to E0 (empty for lanes that need no count)
+  const int a = need ? (int)(lo - E0) : 0, b = need ? (int)(hi - E0) : 0;
+  int cnt = 0;
+  for (int w0 = 0; w0 < L; w0 += 1024) {  // windows of 32 groups
+    const int wl = min(L - w0, 1024);
+    unsigned mine = 0;
+    for (int gb = 0; gb < wl; gb += 256) {
+      int32_t c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = gb + 32 * u + lane;
+        c[u] = e < wl ? __ldg(cp + w0 + e) : 0;  // out-of-range bits are never counted
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int g = gb + 32 * u;
+        if (g >= wl) break;  // warp-uniform
+        uint32_t word = SMEM ? m[(uint32_t)c[u] >> 5] : __ldg(m + ((uint32_t)c[u] >> 5));
+        const unsigned W = __ballot_sync(0xffffffffu, __funnelshift_r(word, word, c[u]) & 1u);
+        if (lane == (g >> 5)) mine = W;
+      }
+    }
+    const int sa = max(a - w0, 0), sb = min(b - w0, wl);
+    const int gf = sa >> 5;
+    const int span = sa < sb ? ((sb - 1) >> 5) - gf + 1 : 0;
+    const int most = __reduce_max_sync(0xffffffffu, span);
+    for (int k = 0; k < most; ++k) {
+      const int gq = gf + k;
+      const unsigned W = __shfl_sync(0xffffffffu, mine, gq & 31);
+      if (k < span) {
+        const int lo_b = max(sa - 32 * gq, 0), hi_b = min(sb - 32 * gq, 32);
+        cnt += __popc(W & bmsk(lo_b, hi_b - lo_b));
+      }
+    }
+  }
+  return cnt;
+}
+
 // thread-per-node sequential f32 fold in CSR order: acc = f32(acc + f32(inf*w))
 // (renewal.py:289 + 60-68; T/test_renewal.py:27-37)
 template <typename IT>
@@ -192,6 +307,25 @@ __device__ __forceinline__ float fold_warp(const int32_t* __restrict__ col, cons
 // ---------------------------------------------------------------------------
 // the fused step
 // ---------------------------------------------------------------------------
+template <typename ST, typename AT>
+struct NodeIn {
+  int s;
+  float age;
+  int64_t lo, hi;
+};
+
+constexpr int kQueue = 64;  // per-warp deferral queue capacity (entries)
+
+// One launch = one reference renewal_step.  Two phases per warp:
+//  A (per 32-node tile, dense): node loads (one tile ahead), pressure
+//    gather, and the cheap outcomes: terminal nodes do nothing, S nodes with
+//    zero pressure only age.  Every node that may fire (S with pressure > 0,
+//    any nodal compartment) is appended to the warp's shared-memory queue;
+//    the tile's next-step mask word is written assuming no deferred node
+//    changes infectious status.
+//  B (whenever >= 32 queued, and once at the end): 32 queued nodes at a time,
+//    all lanes busy: rate (pressure or f64 hazard), counter-based uniform,
+//    Bernoulli, successor / age writes, infectivity / mask fix-up.
 template <typename ST, typename AT, typename IT, int GATHER, int STRAT, bool MAT, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const StepParams p) {
   extern __shared__ __align__(16) uint32_t s_mask[];
@@ -199,10 +333,17 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   __shared__ double s_p0[FS_MAX_COMPARTMENTS], s_p1[FS_MAX_COMPARTMENTS];
   __shared__ int s_cnt[FS_MAX_COMPARTMENTS];
   __shared__ float s_wmax[BLOCK / 32];
+  __shared__ __align__(8) uint64_t s_bar;
   constexpr int WARPS = BLOCK / 32;
+  __shared__ int q_node[WARPS][kQueue];
+  __shared__ int q_state[WARPS][kQueue];
+  __shared__ float q_age[WARPS][kQueue];
+  __shared__ float q_press[WARPS][kQueue];
+  constexpr bool COUNT = (GATHER == G_COUNT_SMEM || GATHER == G_COUNT_GLOBAL);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = p.model.num_compartments;
 
+  if (GATHER == G_COUNT_SMEM && tid == 0) mbar_init(&s_bar, 1);
   if (tid < FS_MAX_COMPARTMENTS) {
     const fs_compartment& c = p.model.comp[tid];
     s_succ[tid] = c.succ;
@@ -222,17 +363,11 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   uint32_t* mask_nxt = p.mask[cur ^ 1];
   const void* inf_cur = p.inf[cur];
   IT* inf_nxt = reinterpret_cast<IT*>(p.inf[cur ^ 1]);
-
-  if (GATHER == G_COUNT_SMEM) {
-    // stage the whole infectious mask (N/8 bytes) in shared memory
-    const int64_t nwords = p.ntiles;
-    const int64_t nvec = nwords >> 2;
-    const uint4* src4 = reinterpret_cast<const uint4*>(mask_cur);
-    uint4* dst4 = reinterpret_cast<uint4*>(s_mask);
-    for (int64_t i = tid; i < nvec; i += BLOCK) dst4[i] = __ldg(src4 + i);
-    for (int64_t i = (nvec << 2) + tid; i < nwords; i += BLOCK) s_mask[i] = __ldg(mask_cur + i);
-  }
   __syncthreads();
+  // stage the whole infectious mask (N/8 bytes) in shared memory with TMA
+  // bulk copies; the first tile's node loads below overlap the transfer
+  if (GATHER == G_COUNT_SMEM) stage_mask_async(s_mask, mask_cur, (uint32_t)(((p.ntiles + 3) & ~3LL) * 4), &s_bar);
+  bool mask_ready = GATHER != G_COUNT_SMEM;
 
   const float tau_f = __double2float_rn(tau);  // np.float32(tau), renewal.py:541
   const uint64_t key = splitmix_step_key(seed, (uint64_t)step);
@@ -241,15 +376,89 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   const int shed = p.model.shedding;
   const float beta_f = __double2float_rn(p.model.beta);
   const uint32_t* gmask = (GATHER == G_COUNT_SMEM) ? s_mask : mask_cur;
+  const bool write_inf = !COUNT && !p.count_mode;
   float lmax = 0.0f;
+  int qn = 0;  // queued entries of this warp (warp-uniform)
+
+  // next-step infectivity of a node in compartment ns at age nage (f32 gather)
+  auto inf_value = [&](int ns, float nage) -> float {
+    if (ns != infectious) return 0.0f;
+    if (shed == FS_SHED_CONSTANT) return beta_f;
+    return __double2float_rn(__dmul_rn(p.model.beta, shedding_f64(shed, p.model.shed_mu, p.model.shed_sigma,
+                                                                    p.model.shed_peak, (double)nage)));
+  };
+
+  // ---- phase B: settle `cnt` queued nodes, one per lane ------------------
+  auto drain = [&](int cnt) {
+    __syncwarp();
+    const bool ok = lane < cnt;
+    const int n = ok ? q_node[warp][lane] : 0;
+    const int s = ok ? q_state[warp][lane] : 0;
+    const float age = ok ? q_age[warp][lane] : 0.0f;
+    float rate = 0.0f;
+    if (ok) {
+      if (s == edge_from) rate = q_press[warp][lane];
+      else rate = nodal_rate(s_kind[s], s_p0[s], s_p1[s], age, p.hprec);
+    }
+    lmax = fmaxf(lmax, rate);
+    bool fire = false;
+    if (rate > 0.0f) {
+      const double u = (p.rng == FS_RNG_SPLITMIX) ? splitmix_uniform(key, (uint64_t)n)
+                                                  : philox_uniform(seed, (uint64_t)step, (uint64_t)n);
+      fire = bernoulli_fire(u, rate, tau);
+    }
+    if (ok) {
+      int ns = s;
+      float nage;
+      if (fire) {
+        ns = s_succ[s];
+        nage = 0.0f;
+        reinterpret_cast<ST*>(p.states)[n] = (ST)ns;
+        atomicAdd(&s_cnt[ns], 1);
+        atomicAdd(&s_cnt[s], -1);
+        if (!write_inf && ((ns == infectious) != (s == infectious)))
+          atomicXor(mask_nxt + (n >> 5), 1u << (n & 31));
+      } else {
+        nage = __fadd_rn(age, tau_f);  // queued nodes are never terminal
+      }
+      reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
+      if (write_inf) inf_nxt[n] = from_f32<IT>(inf_value(ns, nage));
+      if (MAT) p.rates[n] = rate;
+    }
+    __syncwarp();
+  };
 
   const int64_t ntiles = p.active_tiles ? *p.num_active : p.ntiles;
-  for (int64_t t = (int64_t)blockIdx.x * WARPS + warp; t < ntiles; t += (int64_t)gridDim.x * WARPS) {
-    const int64_t tile = p.active_tiles ? (int64_t)p.active_tiles[t] : t;
+  const int64_t stride = (int64_t)gridDim.x * WARPS;
+  // per-node inputs of one 32-node tile, loaded one tile ahead so the next
+  // tile's state/age/offset loads overlap this tile's gather
+  auto load_in = [&](int64_t tile, NodeIn<ST, AT>& in) {
     const int64_t n = tile * 32 + lane;
     const bool valid = n < p.n;
-    const int s = valid ? (int)reinterpret_cast<const ST*>(p.states)[n] : -1;
-    const float age = valid ? to_f32<AT>(reinterpret_cast<const AT*>(p.ages)[n]) : 0.0f;
+    in.s = valid ? (int)reinterpret_cast<const ST*>(p.states)[n] : -1;
+    in.age = valid ? to_f32<AT>(reinterpret_cast<const AT*>(p.ages)[n]) : 0.0f;
+    in.lo = in.hi = 0;
+    if (GATHER != G_PRE) load_slice(p.ro, p.ro32, n, valid, lane, in.lo, in.hi);
+  };
+  auto tile_of = [&](int64_t t) -> int64_t { return p.active_tiles ? (int64_t)p.active_tiles[t] : t; };
+
+  int64_t t = (int64_t)blockIdx.x * WARPS + warp;
+  NodeIn<ST, AT> nxt{};
+  int64_t tile_n = 0;
+  if (t < ntiles) {
+    tile_n = tile_of(t);
+    load_in(tile_n, nxt);
+  }
+  for (; t < ntiles; t += stride) {
+    const NodeIn<ST, AT> in = nxt;
+    const int64_t tile = tile_n;
+    if (t + stride < ntiles) {
+      tile_n = tile_of(t + stride);
+      load_in(tile_n, nxt);
+    }
+    const int64_t n = tile * 32 + lane;
+    const bool valid = n < p.n;
+    const int s = in.s;
     const bool isS = (s == edge_from);
     const bool need = valid && (isS || MAT);
 
@@ -258,87 +467,79 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
     if (GATHER == G_PRE) {
       if (need) pressure = __ldg(p.pre + n);
     } else {
-      int64_t lo = 0, hi = 0;
-      if (need) { lo = __ldg(p.ro + n); hi = __ldg(p.ro + n + 1); }
+      if (GATHER == G_COUNT_SMEM && !mask_ready) {
+        mbar_wait_parity(&s_bar, 0);
+        mask_ready = true;
+      }
+      const unsigned todo = __ballot_sync(kFull, need);
       if (STRAT == S_THREAD) {
-        if (need) {
-          if (GATHER == G_F32) {
-            pressure = fold_thread<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lo, hi);
-          } else {
-            int k = count_thread<GATHER == G_COUNT_SMEM>(p.col, gmask, lo, hi);
-            pressure = __ldg(p.ptab + k);
-          }
+        if (GATHER == G_F32) {
+          if (need) pressure = fold_thread<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo, in.hi);
+        } else if (todo) {
+          const int k = count_tile<GATHER == G_COUNT_SMEM>(p.col, gmask, in.lo, in.hi, need, todo, lane);
+          if (need) pressure = p.ptab_mul ? __fmul_rn((float)k, p.ptab_c) : __ldg(p.ptab + k);
         }
       } else {
-        unsigned todo = __ballot_sync(kFull, need);
-        while (todo) {
-          const int j = __ffs(todo) - 1;
-          todo &= todo - 1;
-          const int64_t lj = __shfl_sync(kFull, lo, j), hj = __shfl_sync(kFull, hi, j);
+        unsigned rest = todo;
+        while (rest) {
+          const int j = __ffs(rest) - 1;
+          rest &= rest - 1;
+          const int64_t lj = __shfl_sync(kFull, in.lo, j), hj = __shfl_sync(kFull, in.hi, j);
           float pj;
           if (GATHER == G_F32) {
             pj = fold_warp<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lj, hj, lane);
           } else {
-            int k = count_warp<GATHER == G_COUNT_SMEM>(p.col, gmask, lj, hj, lane);
-            pj = __ldg(p.ptab + k);
+            const int k = count_warp<GATHER == G_COUNT_SMEM>(p.col, gmask, lj, hj, lane);
+            pj = p.ptab_mul ? __fmul_rn((float)k, p.ptab_c) : __ldg(p.ptab + k);
           }
           if (lane == j) pressure = pj;
         }
       }
     }
 
-    // ---- (2) rate: pressure for S, f32(r) / hazard(age) otherwise --------
-    float rate = 0.0f;
-    if (valid) {
-      if (isS) rate = pressure;
-      else {
-        const int kind = s_kind[s];
-        if (kind != FS_HZ_NONE) rate = nodal_rate(kind, s_p0[s], s_p1[s], age, p.hprec);
-      }
+    // ---- (2) cheap outcomes now, possible transitions to the queue -------
+    const bool term = valid && s_term[s] != 0;
+    const bool defer = valid && !term && (!isS || pressure > 0.0f);
+    if (valid && !term && !defer) {  // S with zero pressure: rate 0, ages
+      const float nage = __fadd_rn(in.age, tau_f);
+      reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
+      if (write_inf) inf_nxt[n] = from_f32<IT>(inf_value(s, nage));
+    } else if (term && write_inf) {
+      inf_nxt[n] = from_f32<IT>(inf_value(s, in.age));
     }
-    lmax = fmaxf(lmax, rate);
-
-    // ---- (3) Bernoulli on the counter-based uniform ----------------------
-    bool fire = false;
-    if (rate > 0.0f) {
-      const double u = (p.rng == FS_RNG_SPLITMIX) ? splitmix_uniform(key, (uint64_t)n)
-                                                  : philox_uniform(seed, (uint64_t)step, (uint64_t)n);
-      fire = bernoulli_fire(u, rate, tau);
+    if (MAT && valid) {
+      p.pressure[n] = pressure;
+      if (!defer) p.rates[n] = 0.0f;
     }
-
-    // ---- (4) transition, age reset / advance / freeze --------------------
-    int ns = s;
-    if (valid) {
-      const bool term = s_term[s] != 0;
-      float nage = age;
-      if (fire) {
-        ns = s_succ[s];
-        nage = 0.0f;
-        reinterpret_cast<ST*>(p.states)[n] = (ST)ns;
-        atomicAdd(&s_cnt[ns], 1);
-        atomicAdd(&s_cnt[s], -1);
-      } else if (!term) {
-        nage = __fadd_rn(age, tau_f);
-      }
-      if (fire || !term) reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
-      if (!(GATHER == G_COUNT_SMEM || GATHER == G_COUNT_GLOBAL) && !p.count_mode) {
-        // ---- (5a) next-step infectivity, cast on store (renewal.py:556-575)
-        float v = 0.0f;
-        if (ns == infectious) {
-          if (shed == FS_SHED_CONSTANT) v = beta_f;
-          else v = __double2float_rn(__dmul_rn(p.model.beta,
-                       shedding_f64(shed, p.model.shed_mu, p.model.shed_sigma, p.model.shed_peak, (double)nage)));
-        }
-        inf_nxt[n] = from_f32<IT>(v);
-      }
-      if (MAT) { p.pressure[n] = pressure; p.rates[n] = rate; }
-    }
-    if (GATHER == G_COUNT_SMEM || GATHER == G_COUNT_GLOBAL || p.count_mode) {
-      // ---- (5b) next-step infectious bit-mask, one word per warp tile
-      const unsigned word = __ballot_sync(kFull, valid && ns == infectious);
+    if (!write_inf) {
+      // next-step mask word; deferred nodes are fixed up in phase B
+      const unsigned word = __ballot_sync(kFull, valid && s == infectious);
       if (lane == 0) mask_nxt[tile] = word;
     }
+    const unsigned dm = __ballot_sync(kFull, defer);
+    if (defer) {
+      const int at = qn + __popc(dm & ((1u << lane) - 1u));
+      q_node[warp][at] = (int)n;
+      q_state[warp][at] = s;
+      q_age[warp][at] = in.age;
+      q_press[warp][at] = pressure;
+    }
+    qn += __popc(dm);
+    if (qn >= 32) {
+      drain(32);
+      if (lane < qn - 32) {
+        q_node[warp][lane] = q_node[warp][32 + lane];
+        q_state[warp][lane] = q_state[warp][32 + lane];
+        q_age[warp][lane] = q_age[warp][32 + lane];
+        q_press[warp][lane] = q_press[warp][32 + lane];
+      }
+      qn -= 32;
+    }
   }
+  if (qn > 0) drain(qn);
+
+  // a warp without tiles still has to see the bulk copy land before exit
+  if (GATHER == G_COUNT_SMEM && !mask_ready) mbar_wait_parity(&s_bar, 0);
 
   // ---- (6) block max-rate / count deltas, last CTA folds the partials ----
 #pragma unroll
@@ -457,12 +658,20 @@ __global__ void k_chunk_first(const int64_t* __restrict__ ro, int64_t n, int64_t
   }
 }
 
-// ptab[k] = k-fold sequential f32 sum of c (count-gather pressure table)
-__global__ void k_ptab(float* ptab, int64_t len, float c) {
+// ptab[k] = k-fold sequential f32 sum of c (count-gather pressure table);
+// *exact_mul = 1 when every entry equals the single product f32(k * c)
+// (e.g. beta = 0.25 with unit weights), letting the kernels skip the lookup
+__global__ void k_ptab(float* ptab, int64_t len, float c, int* exact_mul) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     float acc = 0.0f;
+    int ok = 1;
     ptab[0] = 0.0f;
-    for (int64_t k = 1; k < len; ++k) { acc = __fadd_rn(acc, c); ptab[k] = acc; }
+    for (int64_t k = 1; k < len; ++k) {
+      acc = __fadd_rn(acc, c);
+      ptab[k] = acc;
+      if (acc != __fmul_rn((float)k, c)) ok = 0;
+    }
+    *exact_mul = ok;
   }
 }
 
@@ -620,6 +829,8 @@ struct fs_engine {
   int64_t log_cap = 0;
   float* ptab = nullptr;
   int64_t ptab_len = 0;
+  int ptab_mul = 0;
+  float ptab_c = 0.0f;
   int32_t* active_tiles = nullptr;
   int64_t* num_active = nullptr;
   int64_t* chunk_first = nullptr;
@@ -652,6 +863,7 @@ int dalloc(T** p, size_t count) {
 StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active) {
   StepParams p{};
   p.ro = e->g.row_offsets;
+  p.ro32 = e->g.row_offsets32;
   p.col = e->g.col_indices;
   p.w = e->g.weights;
   p.w_bf16 = e->g.weights_dtype == FS_BF16;
@@ -676,6 +888,8 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active) {
   p.log_counts = e->log_counts;
   p.log_cap = e->log_cap;
   p.ptab = e->ptab;
+  p.ptab_mul = e->ptab_mul;
+  p.ptab_c = e->ptab_c;
   p.active_tiles = (use_active && e->c.compaction) ? e->active_tiles : nullptr;
   p.num_active = e->num_active;
   p.pre = use_pre ? e->pre : nullptr;
@@ -693,6 +907,7 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active) {
 MergeParams make_merge_params(const fs_engine* e) {
   MergeParams q{};
   q.ro = e->g.row_offsets;
+  q.ro32 = e->g.row_offsets32;
   q.col = e->g.col_indices;
   q.w = e->g.weights;
   q.w_bf16 = e->g.weights_dtype == FS_BF16;
@@ -817,7 +1032,7 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
   int rc = 0;
 #define TRY(x) do { rc = (x); if (rc) { fs_engine_destroy(e); return rc; } } while (0)
   for (int mat = 0; mat < 2; ++mat) e->step_fn[mat] = pick_step(e->mixed, e->gather, e->strat, mat != 0, e->step_block);
-  e->step_smem = (e->gather == G_COUNT_SMEM) ? (size_t)e->ntiles * 4 : 0;
+  e->step_smem = (e->gather == G_COUNT_SMEM) ? (size_t)((e->ntiles + 3) & ~3LL) * 4 : 0;
   int occ = 1;
   for (int mat = 0; mat < 2; ++mat) {
     if (e->step_smem > 0)
@@ -862,7 +1077,10 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
     TRY(dalloc(&e->ptab, e->ptab_len));
     volatile float a_ = e->inf_val, w_ = g->uniform_weight;
     const float cval = a_ * w_;  // f32(inf * w): one IEEE single multiply
-    k_ptab<<<1, 1>>>(e->ptab, e->ptab_len, cval);
+    FS_CUDA(cudaMemset(e->bad_flag, 0, sizeof(int)));
+    k_ptab<<<1, 1>>>(e->ptab, e->ptab_len, cval, e->bad_flag);
+    FS_CUDA(cudaMemcpy(&e->ptab_mul, e->bad_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    e->ptab_c = cval;
   }
   if (e->merge) {
     TRY(dalloc(&e->chunk_first, e->nchunks + 1));

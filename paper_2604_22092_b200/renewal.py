@@ -138,6 +138,9 @@ class _DeviceGraph:
         self.num_edges = int(g.num_edges)
         ro = np.ascontiguousarray(g.row_offsets, dtype=np.int64)
         self.row_offsets = torch.from_numpy(ro).to(dev)
+        # int32 copy for the hot kernels when every offset fits (halves the
+        # offset stream; listed in DESIGN.md as an encoding)
+        self.row_offsets32 = self.row_offsets.to(torch.int32) if self.num_edges < 2**31 else None
         self.col_indices = torch.from_numpy(np.ascontiguousarray(g.col_indices, dtype=np.int32)).to(dev)
         w = np.ascontiguousarray(g.weights, dtype=np.float32)
         if mixed:  # weights rounded to bf16 at plan time (renewal.py:330-331)
@@ -155,6 +158,7 @@ class _DeviceGraph:
             num_nodes=self.num_nodes,
             num_edges=self.num_edges,
             row_offsets=_lib.ptr(self.row_offsets),
+            row_offsets32=_lib.ptr(self.row_offsets32),
             col_indices=_lib.ptr(self.col_indices),
             weights=_lib.ptr(self.weights),
             weights_dtype=_lib.BF16 if self.weights_bf16 else _lib.F32,
@@ -233,7 +237,7 @@ class _Engine:
         self.stream = _device.stream_handle(dev)
         _, _, it = _storage(state.mixed_precision)
         if plan.count_mode:
-            w = (n + 31) // 32
+            w = ((n + 31) // 32 + 3) // 4 * 4  # 16-byte multiple: staged by TMA bulk copies
             self.bufs = [torch.zeros(w, dtype=torch.int32, device=dev) for _ in range(2)]
         else:
             self.bufs = [torch.zeros(n, dtype=it, device=dev) for _ in range(2)]
