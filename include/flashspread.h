@@ -81,6 +81,8 @@ typedef struct fs_graph {
   int32_t weights_uniform;      /* 1: every weight == uniform_weight          */
   float uniform_weight;         /* the common weight (already bf16-rounded in mixed mode) */
   int32_t d_max;                /* max in-degree                               */
+  int32_t padded;               /* 1: row_offsets32 readable to N+9 entries and
+                                   col_indices to E+4 (TMA bulk-copy slack)   */
 } fs_graph;
 
 typedef struct fs_compartment {
@@ -142,6 +144,7 @@ typedef struct fs_state_buffers {
                             multiple and 16-byte aligned (TMA bulk staging) */
   float* pressure;       /* f32[N], written on materialising steps            */
   float* rates;          /* f32[N], written on materialising steps            */
+  int32_t padded;        /* 1: states/ages readable to a multiple of 32 nodes */
 } fs_state_buffers;
 
 typedef struct fs_engine fs_engine;

@@ -50,6 +50,7 @@ class FsGraph(ctypes.Structure):
         ("weights_uniform", _c_i32),
         ("uniform_weight", _c_f32),
         ("d_max", _c_i32),
+        ("padded", _c_i32),
     ]
 
 
@@ -120,6 +121,7 @@ class FsStateBuffers(ctypes.Structure):
         ("imask", _vp * 2),
         ("pressure", _vp),
         ("rates", _vp),
+        ("padded", _c_i32),
     ]
 
 

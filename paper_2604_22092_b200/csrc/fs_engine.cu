@@ -214,8 +214,9 @@ __device__ __forceinline__ void load_slice(const int64_t* __restrict__ ro, const
 }
 
 // tile-cooperative count: the warp streams the contiguous edge range of its
-// 32 nodes 32 edges per group (coalesced loads, 8 groups in flight), tests
-// the sources in the mask and ballots.  Lane g keeps group g's ballot word;
+// 32 nodes 32 edges per group, 8 groups per pass with every load of a pass
+// in flight together (columns first, then the mask words they address),
+// tests the source bits and ballots.  Lane g keeps group g's ballot word;
 // afterwards every lane fetches only the words its own slice spans and
 // popcounts them.  Integer counts are order-free: exact for any partition.
 __device__ __forceinline__ uint32_t bmsk(int start, int width) {
@@ -224,12 +225,19 @@ __device__ __forceinline__ uint32_t bmsk(int start, int width) {
   return r;
 }
 
-template <bool SMEM>
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+template <bool SMEM_MASK, bool COL_SMEM = false>
 __device__ __forceinline__ int count_tile(const int32_t* __restrict__ col, const uint32_t* m, int64_t lo, int64_t hi,
                                           bool need, unsigned need_mask, int lane) {
   const int j0 = __ffs(need_mask) - 1, j1 = 31 - __clz(need_mask);
   const int64_t E0 = __shfl_sync(0xffffffffu, lo, j0), E1 = __shfl_sync(0xffffffffu, hi, j1);
   const int32_t* __restrict__ cp = col + E0;
+  const uint32_t cp_s = COL_SMEM ? smem_u32(cp) : 0u;  // columns staged in shared memory
   const int L = (int)(E1 - E0);
   // my slice relative to E0 (empty for lanes that need no count)
   const int a = need ? (int)(lo - E0) : 0, b = need ? (int)(hi - E0) : 0;
@@ -238,18 +246,20 @@ __device__ __forceinline__ int count_tile(const int32_t* __restrict__ col, const
     const int wl = min(L - w0, 1024);
     unsigned mine = 0;
     for (int gb = 0; gb < wl; gb += 256) {
-      int32_t c[8];
+      uint32_t c[8], word[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int e = gb + 32 * u + lane;
-        c[u] = e < wl ? __ldg(cp + w0 + e) : 0;  // out-of-range bits are never counted
+        c[u] = e < wl ? (COL_SMEM ? lds_u32(cp_s + 4u * (uint32_t)(w0 + e)) : (uint32_t)__ldg(cp + w0 + e))
+                      : 0u;  // bits past the range are never counted
       }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) word[u] = SMEM_MASK ? m[c[u] >> 5] : __ldg(m + (c[u] >> 5));
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int g = gb + 32 * u;
         if (g >= wl) break;  // warp-uniform
-        uint32_t word = SMEM ? m[(uint32_t)c[u] >> 5] : __ldg(m + ((uint32_t)c[u] >> 5));
-        const unsigned W = __ballot_sync(0xffffffffu, __funnelshift_r(word, word, c[u]) & 1u);
+        const unsigned W = __ballot_sync(0xffffffffu, __funnelshift_r(word[u], word[u], c[u]) & 1u);
         if (lane == (g >> 5)) mine = W;
       }
     }
@@ -316,49 +326,240 @@ struct NodeIn {
 
 constexpr int kQueue = 64;  // per-warp deferral queue capacity (entries)
 
-// One launch = one reference renewal_step.  Two phases per warp:
+// per-launch constants every phase needs
+struct StepConst {
+  double tau;
+  float tau_f;
+  uint64_t key, seed;
+  int64_t step;
+  int edge_from, infectious, shed;
+  float beta_f;
+  bool write_inf;
+};
+
+// shared-memory model tables + the per-warp deferral queues
+template <int WARPS>
+struct StepShared {
+  int succ[FS_MAX_COMPARTMENTS], term[FS_MAX_COMPARTMENTS], kind[FS_MAX_COMPARTMENTS];
+  double p0[FS_MAX_COMPARTMENTS], p1[FS_MAX_COMPARTMENTS];
+  int cnt[FS_MAX_COMPARTMENTS];
+  float wmax[WARPS];
+  int q_node[WARPS][kQueue];
+  int q_state[WARPS][kQueue];
+  float q_age[WARPS][kQueue];
+  float q_press[WARPS][kQueue];
+};
+
+template <int WARPS>
+__device__ __forceinline__ void load_tables(const StepParams& p, StepShared<WARPS>& sh, int tid) {
+  if (tid < FS_MAX_COMPARTMENTS) {
+    const fs_compartment& c = p.model.comp[tid];
+    sh.succ[tid] = c.succ;
+    sh.term[tid] = c.terminal;
+    sh.kind[tid] = c.hazard;
+    sh.p0[tid] = c.p0;
+    sh.p1[tid] = c.p1;
+    sh.cnt[tid] = 0;
+  }
+}
+
+__device__ __forceinline__ StepConst step_const(const StepParams& p, bool count_gather) {
+  StepConst k;
+  const fs_scalars* S = p.S;  // written by the previous launch's last CTA
+  k.tau = S->tau_next;
+  k.step = S->step;
+  k.seed = S->seed;
+  k.tau_f = __double2float_rn(k.tau);  // np.float32(tau), renewal.py:541
+  k.key = splitmix_step_key(k.seed, (uint64_t)k.step);
+  k.edge_from = p.model.edge_from;
+  k.infectious = p.model.infectious;
+  k.shed = p.model.shedding;
+  k.beta_f = __double2float_rn(p.model.beta);
+  k.write_inf = !count_gather;
+  return k;
+}
+
+// next-step infectivity of a node in compartment ns at age nage (f32 gather;
+// renewal.py:556-565, cast on store by the caller)
+__device__ __forceinline__ float inf_value(const StepParams& p, const StepConst& k, int ns, float nage) {
+  if (ns != k.infectious) return 0.0f;
+  if (k.shed == FS_SHED_CONSTANT) return k.beta_f;
+  return __double2float_rn(
+      __dmul_rn(p.model.beta, shedding_f64(k.shed, p.model.shed_mu, p.model.shed_sigma, p.model.shed_peak, (double)nage)));
+}
+
+// phase B: settle `cnt` queued nodes of this warp, one per lane — rate
+// (pressure or hazard), uniform, Bernoulli, successor / age / infectivity
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
+__device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
+                                            int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
+  __syncwarp();
+  const bool ok = lane < cnt;
+  const int n = ok ? sh.q_node[warp][lane] : 0;
+  const int s = ok ? sh.q_state[warp][lane] : 0;
+  const float age = ok ? sh.q_age[warp][lane] : 0.0f;
+  float rate = 0.0f;
+  if (ok) {
+    if (s == k.edge_from) rate = sh.q_press[warp][lane];
+    else rate = nodal_rate(sh.kind[s], sh.p0[s], sh.p1[s], age, p.hprec);
+  }
+  lmax = fmaxf(lmax, rate);
+  bool fire = false;
+  if (rate > 0.0f) {
+    const double u = (p.rng == FS_RNG_SPLITMIX) ? splitmix_uniform(k.key, (uint64_t)n)
+                                                : philox_uniform(k.seed, (uint64_t)k.step, (uint64_t)n);
+    fire = bernoulli_fire(u, rate, k.tau);
+  }
+  if (ok) {
+    int ns = s;
+    float nage;
+    if (fire) {
+      ns = sh.succ[s];
+      nage = 0.0f;
+      reinterpret_cast<ST*>(p.states)[n] = (ST)ns;
+      atomicAdd(&sh.cnt[ns], 1);
+      atomicAdd(&sh.cnt[s], -1);
+      if (!k.write_inf && ((ns == k.infectious) != (s == k.infectious)))
+        atomicXor(mask_nxt + (n >> 5), 1u << (n & 31));
+    } else {
+      nage = __fadd_rn(age, k.tau_f);  // queued nodes are never terminal
+    }
+    reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
+    if (k.write_inf) inf_nxt[n] = from_f32<IT>(inf_value(p, k, ns, nage));
+    if (MAT) p.rates[n] = rate;
+  }
+  __syncwarp();
+}
+
+// phase A outcome of one tile (pressure already gathered): cheap outcomes
+// now, possible transitions appended to the warp queue (drained at 32)
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
+__device__ __forceinline__ void tile_outcome(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
+                                             int lane, int64_t tile, int64_t n, bool valid, int s, float age,
+                                             float pressure, int& qn, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
+  const bool isS = s == k.edge_from;
+  const bool term = valid && sh.term[s] != 0;
+  const bool defer = valid && !term && (!isS || pressure > 0.0f);
+  if (valid && !term && !defer) {  // S with zero pressure: rate 0, ages
+    const float nage = __fadd_rn(age, k.tau_f);
+    reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
+    if (k.write_inf) inf_nxt[n] = from_f32<IT>(inf_value(p, k, s, nage));
+  } else if (term && k.write_inf) {
+    inf_nxt[n] = from_f32<IT>(inf_value(p, k, s, age));
+  }
+  if (MAT && valid) {
+    p.pressure[n] = pressure;
+    if (!defer) p.rates[n] = 0.0f;
+  }
+  if (!k.write_inf) {
+    // next-step mask word; deferred nodes are fixed up in phase B
+    const unsigned word = __ballot_sync(0xffffffffu, valid && s == k.infectious);
+    if (lane == 0) mask_nxt[tile] = word;
+  }
+  const unsigned dm = __ballot_sync(0xffffffffu, defer);
+  if (defer) {
+    const int at = qn + __popc(dm & ((1u << lane) - 1u));
+    sh.q_node[warp][at] = (int)n;
+    sh.q_state[warp][at] = s;
+    sh.q_age[warp][at] = age;
+    sh.q_press[warp][at] = pressure;
+  }
+  qn += __popc(dm);
+  if (qn >= 32) {
+    drain_queue<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt);
+    if (lane < qn - 32) {
+      sh.q_node[warp][lane] = sh.q_node[warp][32 + lane];
+      sh.q_state[warp][lane] = sh.q_state[warp][32 + lane];
+      sh.q_age[warp][lane] = sh.q_age[warp][32 + lane];
+      sh.q_press[warp][lane] = sh.q_press[warp][32 + lane];
+    }
+    qn -= 32;
+  }
+}
+
+// block max-rate / count deltas; the last CTA to finish folds every CTA's
+// partials into the device scalars and the per-step log
+template <int WARPS>
+__device__ __forceinline__ void finish_step(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
+                                            int lane, float lmax) {
+  constexpr unsigned FULL = 0xffffffffu;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(FULL, lmax, o));
+  if (lane == 0) sh.wmax[warp] = lmax;
+  __syncthreads();
+  if (warp != 0) return;
+  float bmax = lane < WARPS ? sh.wmax[lane] : 0.0f;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(FULL, bmax, o));
+  if (lane == 0) p.part_max[blockIdx.x] = __float_as_uint(bmax);  // rates >= 0: bit order == value order
+  if (lane < FS_MAX_COMPARTMENTS) p.part_cnt[blockIdx.x * kCntStride + lane] = sh.cnt[lane];
+  __threadfence();
+  unsigned ticket = 0;
+  if (lane == 0) ticket = atomicAdd(p.ticket, 1u);
+  ticket = __shfl_sync(FULL, ticket, 0);
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  unsigned mbits = 0;
+  for (unsigned b = lane; b < gridDim.x; b += 32) mbits = max(mbits, __ldcg(p.part_max + b));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mbits = max(mbits, __shfl_xor_sync(FULL, mbits, o));
+  const int64_t slot = k.step % p.log_cap;
+  fs_scalars* W = p.S;
+  const double clock1 = W->clock + k.tau;  // renewal.py:497-498
+  for (int c = 0; c < p.model.num_compartments; ++c) {
+    long long d = 0;
+    for (unsigned b = lane; b < gridDim.x; b += 32) d += __ldcg(p.part_cnt + b * kCntStride + c);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
+    if (lane == 0) {
+      const int64_t v = W->counts[c] + d;
+      W->counts[c] = v;
+      p.log_counts[slot * kCntStride + c] = v;
+    }
+  }
+  if (lane == 0) {
+    const float maxf = __uint_as_float(mbits);
+    // tau' = min(tau_max, eps / (max rate + delta)) in f64 (renewal.py:577-578)
+    const double cand = __ddiv_rn(p.eps, __dadd_rn((double)maxf, p.delta));
+    W->last_max_rate = maxf;
+    W->tau_next = (p.tau_max <= cand) ? p.tau_max : cand;
+    W->clock = clock1;
+    W->step = k.step + 1;
+    W->started = 1;
+    p.log_clock[slot] = clock1;
+    p.log_tau[slot] = k.tau;
+    __threadfence();
+    *p.ticket = 0u;
+  }
+}
+
+// One launch = one reference renewal_step (renewal.py:483-580), two phases
+// per warp:
 //  A (per 32-node tile, dense): node loads (one tile ahead), pressure
 //    gather, and the cheap outcomes: terminal nodes do nothing, S nodes with
 //    zero pressure only age.  Every node that may fire (S with pressure > 0,
 //    any nodal compartment) is appended to the warp's shared-memory queue;
-//    the tile's next-step mask word is written assuming no deferred node
-//    changes infectious status.
+//    the tile's next-step mask word assumes no deferred node changes
+//    infectious status.
 //  B (whenever >= 32 queued, and once at the end): 32 queued nodes at a time,
 //    all lanes busy: rate (pressure or f64 hazard), counter-based uniform,
 //    Bernoulli, successor / age writes, infectivity / mask fix-up.
+// This general kernel serves every gather mode and strategy (and the
+// compaction tile list); the streaming k_step_tma below is the fast path
+// of the count gather.
 template <typename ST, typename AT, typename IT, int GATHER, int STRAT, bool MAT, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const StepParams p) {
   extern __shared__ __align__(16) uint32_t s_mask[];
-  __shared__ int s_succ[FS_MAX_COMPARTMENTS], s_term[FS_MAX_COMPARTMENTS], s_kind[FS_MAX_COMPARTMENTS];
-  __shared__ double s_p0[FS_MAX_COMPARTMENTS], s_p1[FS_MAX_COMPARTMENTS];
-  __shared__ int s_cnt[FS_MAX_COMPARTMENTS];
-  __shared__ float s_wmax[BLOCK / 32];
-  __shared__ __align__(8) uint64_t s_bar;
   constexpr int WARPS = BLOCK / 32;
-  __shared__ int q_node[WARPS][kQueue];
-  __shared__ int q_state[WARPS][kQueue];
-  __shared__ float q_age[WARPS][kQueue];
-  __shared__ float q_press[WARPS][kQueue];
+  __shared__ StepShared<WARPS> sh;
+  __shared__ __align__(8) uint64_t s_bar;
   constexpr bool COUNT = (GATHER == G_COUNT_SMEM || GATHER == G_COUNT_GLOBAL);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int M = p.model.num_compartments;
 
   if (GATHER == G_COUNT_SMEM && tid == 0) mbar_init(&s_bar, 1);
-  if (tid < FS_MAX_COMPARTMENTS) {
-    const fs_compartment& c = p.model.comp[tid];
-    s_succ[tid] = c.succ;
-    s_term[tid] = c.terminal;
-    s_kind[tid] = c.hazard;
-    s_p0[tid] = c.p0;
-    s_p1[tid] = c.p1;
-    s_cnt[tid] = 0;
-  }
-  // step scalars (written by the previous launch's last CTA)
-  const fs_scalars* S = p.S;
-  const double tau = S->tau_next;
-  const int64_t step = S->step;
-  const uint64_t seed = S->seed;
-  const int cur = (int)(step & 1);
+  load_tables<WARPS>(p, sh, tid);
+  const StepConst k = step_const(p, COUNT || p.count_mode);
+  const int cur = (int)(k.step & 1);
   const uint32_t* mask_cur = p.mask[cur];
   uint32_t* mask_nxt = p.mask[cur ^ 1];
   const void* inf_cur = p.inf[cur];
@@ -368,70 +569,12 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   // bulk copies; the first tile's node loads below overlap the transfer
   if (GATHER == G_COUNT_SMEM) stage_mask_async(s_mask, mask_cur, (uint32_t)(((p.ntiles + 3) & ~3LL) * 4), &s_bar);
   bool mask_ready = GATHER != G_COUNT_SMEM;
-
-  const float tau_f = __double2float_rn(tau);  // np.float32(tau), renewal.py:541
-  const uint64_t key = splitmix_step_key(seed, (uint64_t)step);
-  const int edge_from = p.model.edge_from;
-  const int infectious = p.model.infectious;
-  const int shed = p.model.shedding;
-  const float beta_f = __double2float_rn(p.model.beta);
   const uint32_t* gmask = (GATHER == G_COUNT_SMEM) ? s_mask : mask_cur;
-  const bool write_inf = !COUNT && !p.count_mode;
   float lmax = 0.0f;
   int qn = 0;  // queued entries of this warp (warp-uniform)
 
-  // next-step infectivity of a node in compartment ns at age nage (f32 gather)
-  auto inf_value = [&](int ns, float nage) -> float {
-    if (ns != infectious) return 0.0f;
-    if (shed == FS_SHED_CONSTANT) return beta_f;
-    return __double2float_rn(__dmul_rn(p.model.beta, shedding_f64(shed, p.model.shed_mu, p.model.shed_sigma,
-                                                                    p.model.shed_peak, (double)nage)));
-  };
-
-  // ---- phase B: settle `cnt` queued nodes, one per lane ------------------
-  auto drain = [&](int cnt) {
-    __syncwarp();
-    const bool ok = lane < cnt;
-    const int n = ok ? q_node[warp][lane] : 0;
-    const int s = ok ? q_state[warp][lane] : 0;
-    const float age = ok ? q_age[warp][lane] : 0.0f;
-    float rate = 0.0f;
-    if (ok) {
-      if (s == edge_from) rate = q_press[warp][lane];
-      else rate = nodal_rate(s_kind[s], s_p0[s], s_p1[s], age, p.hprec);
-    }
-    lmax = fmaxf(lmax, rate);
-    bool fire = false;
-    if (rate > 0.0f) {
-      const double u = (p.rng == FS_RNG_SPLITMIX) ? splitmix_uniform(key, (uint64_t)n)
-                                                  : philox_uniform(seed, (uint64_t)step, (uint64_t)n);
-      fire = bernoulli_fire(u, rate, tau);
-    }
-    if (ok) {
-      int ns = s;
-      float nage;
-      if (fire) {
-        ns = s_succ[s];
-        nage = 0.0f;
-        reinterpret_cast<ST*>(p.states)[n] = (ST)ns;
-        atomicAdd(&s_cnt[ns], 1);
-        atomicAdd(&s_cnt[s], -1);
-        if (!write_inf && ((ns == infectious) != (s == infectious)))
-          atomicXor(mask_nxt + (n >> 5), 1u << (n & 31));
-      } else {
-        nage = __fadd_rn(age, tau_f);  // queued nodes are never terminal
-      }
-      reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
-      if (write_inf) inf_nxt[n] = from_f32<IT>(inf_value(ns, nage));
-      if (MAT) p.rates[n] = rate;
-    }
-    __syncwarp();
-  };
-
   const int64_t ntiles = p.active_tiles ? *p.num_active : p.ntiles;
   const int64_t stride = (int64_t)gridDim.x * WARPS;
-  // per-node inputs of one 32-node tile, loaded one tile ahead so the next
-  // tile's state/age/offset loads overlap this tile's gather
   auto load_in = [&](int64_t tile, NodeIn<ST, AT>& in) {
     const int64_t n = tile * 32 + lane;
     const bool valid = n < p.n;
@@ -452,17 +595,14 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   for (; t < ntiles; t += stride) {
     const NodeIn<ST, AT> in = nxt;
     const int64_t tile = tile_n;
-    if (t + stride < ntiles) {
+    if (t + stride < ntiles) {  // next tile's node loads overlap this tile
       tile_n = tile_of(t + stride);
       load_in(tile_n, nxt);
     }
     const int64_t n = tile * 32 + lane;
     const bool valid = n < p.n;
-    const int s = in.s;
-    const bool isS = (s == edge_from);
-    const bool need = valid && (isS || MAT);
+    const bool need = valid && (in.s == k.edge_from || MAT);
 
-    // ---- (1) pressure gather -------------------------------------------
     float pressure = 0.0f;
     if (GATHER == G_PRE) {
       if (need) pressure = __ldg(p.pre + n);
@@ -476,10 +616,10 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
         if (GATHER == G_F32) {
           if (need) pressure = fold_thread<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo, in.hi);
         } else if (todo) {
-          const int k = count_tile<GATHER == G_COUNT_SMEM>(p.col, gmask, in.lo, in.hi, need, todo, lane);
-          if (need) pressure = p.ptab_mul ? __fmul_rn((float)k, p.ptab_c) : __ldg(p.ptab + k);
+          const int kk = count_tile<GATHER == G_COUNT_SMEM>(p.col, gmask, in.lo, in.hi, need, todo, lane);
+          if (need) pressure = p.ptab_mul ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
         }
-      } else {
+      } else {  // warp per node (LANE strategy)
         unsigned rest = todo;
         while (rest) {
           const int j = __ffs(rest) - 1;
@@ -489,107 +629,154 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
           if (GATHER == G_F32) {
             pj = fold_warp<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lj, hj, lane);
           } else {
-            const int k = count_warp<GATHER == G_COUNT_SMEM>(p.col, gmask, lj, hj, lane);
-            pj = p.ptab_mul ? __fmul_rn((float)k, p.ptab_c) : __ldg(p.ptab + k);
+            const int kk = count_warp<GATHER == G_COUNT_SMEM>(p.col, gmask, lj, hj, lane);
+            pj = p.ptab_mul ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
           }
           if (lane == j) pressure = pj;
         }
       }
     }
-
-    // ---- (2) cheap outcomes now, possible transitions to the queue -------
-    const bool term = valid && s_term[s] != 0;
-    const bool defer = valid && !term && (!isS || pressure > 0.0f);
-    if (valid && !term && !defer) {  // S with zero pressure: rate 0, ages
-      const float nage = __fadd_rn(in.age, tau_f);
-      reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
-      if (write_inf) inf_nxt[n] = from_f32<IT>(inf_value(s, nage));
-    } else if (term && write_inf) {
-      inf_nxt[n] = from_f32<IT>(inf_value(s, in.age));
-    }
-    if (MAT && valid) {
-      p.pressure[n] = pressure;
-      if (!defer) p.rates[n] = 0.0f;
-    }
-    if (!write_inf) {
-      // next-step mask word; deferred nodes are fixed up in phase B
-      const unsigned word = __ballot_sync(kFull, valid && s == infectious);
-      if (lane == 0) mask_nxt[tile] = word;
-    }
-    const unsigned dm = __ballot_sync(kFull, defer);
-    if (defer) {
-      const int at = qn + __popc(dm & ((1u << lane) - 1u));
-      q_node[warp][at] = (int)n;
-      q_state[warp][at] = s;
-      q_age[warp][at] = in.age;
-      q_press[warp][at] = pressure;
-    }
-    qn += __popc(dm);
-    if (qn >= 32) {
-      drain(32);
-      if (lane < qn - 32) {
-        q_node[warp][lane] = q_node[warp][32 + lane];
-        q_state[warp][lane] = q_state[warp][32 + lane];
-        q_age[warp][lane] = q_age[warp][32 + lane];
-        q_press[warp][lane] = q_press[warp][32 + lane];
-      }
-      qn -= 32;
-    }
+    tile_outcome<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, tile, n, valid, in.s, in.age, pressure, qn, lmax,
+                                         mask_nxt, inf_nxt);
   }
-  if (qn > 0) drain(qn);
-
+  if (qn > 0) drain_queue<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, inf_nxt);
   // a warp without tiles still has to see the bulk copy land before exit
   if (GATHER == G_COUNT_SMEM && !mask_ready) mbar_wait_parity(&s_bar, 0);
+  finish_step<WARPS>(p, k, sh, warp, lane, lmax);
+}
 
-  // ---- (6) block max-rate / count deltas, last CTA folds the partials ----
-#pragma unroll
-  for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(kFull, lmax, o));
-  if (lane == 0) s_wmax[warp] = lmax;
+// ---------------------------------------------------------------------------
+// Streaming fast path of the count gather (PER_NODE strategy).
+// Each warp owns a contiguous run of 32-node tiles and keeps TMA_SLOTS of
+// them in flight: lane 0 issues cp.async.bulk copies of the tile's offsets,
+// states, ages and contiguous column slice into a shared-memory slot whose
+// mbarrier completes on the byte count, so ~TMA_SLOTS x 1.7 KB per warp
+// stream from HBM with no registers held.  The gather then reads columns
+// and the staged infectious mask from shared memory only.
+// ---------------------------------------------------------------------------
+struct TmaLayout {
+  int slots;        // buffers per warp
+  int slot_bytes;   // bytes per buffer
+  int ro_off, st_off, ag_off, col_off;  // byte offsets inside a buffer
+  int col_cap;      // column entries a buffer holds
+};
+
+template <typename ST, typename AT, bool SMEM_MASK, bool MAT, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const TmaLayout L) {
+  extern __shared__ __align__(128) unsigned char dyn[];
+  constexpr int WARPS = BLOCK / 32;
+  __shared__ StepShared<WARPS> sh;
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ __align__(8) uint64_t t_bar[WARPS][4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t mask_words = (p.ntiles + 3) & ~3LL;
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(dyn);
+  unsigned char* wbuf = dyn + (SMEM_MASK ? mask_words * 4 : 0) + (size_t)warp * L.slots * L.slot_bytes;
+
+  if (tid == 0 && SMEM_MASK) mbar_init(&s_bar, 1);
+  if (lane == 0)
+    for (int sl = 0; sl < L.slots; ++sl) mbar_init(&t_bar[warp][sl], 1);
+  load_tables<WARPS>(p, sh, tid);
+  const StepConst k = step_const(p, true);
+  const int cur = (int)(k.step & 1);
+  const uint32_t* mask_cur = p.mask[cur];
+  uint32_t* mask_nxt = p.mask[cur ^ 1];
   __syncthreads();
-  if (warp != 0) return;
-  float bmax = lane < WARPS ? s_wmax[lane] : 0.0f;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(kFull, bmax, o));
-  if (lane == 0) p.part_max[blockIdx.x] = __float_as_uint(bmax);  // rates >= 0: bit order == value order
-  if (lane < FS_MAX_COMPARTMENTS) p.part_cnt[blockIdx.x * kCntStride + lane] = s_cnt[lane];
-  __threadfence();
-  unsigned ticket = 0;
-  if (lane == 0) ticket = atomicAdd(p.ticket, 1u);
-  ticket = __shfl_sync(kFull, ticket, 0);
-  if (ticket != gridDim.x - 1) return;
-  __threadfence();
-  unsigned mbits = 0;
-  for (unsigned b = lane; b < gridDim.x; b += 32) mbits = max(mbits, __ldcg(p.part_max + b));
-#pragma unroll
-  for (int o = 16; o; o >>= 1) mbits = max(mbits, __shfl_xor_sync(kFull, mbits, o));
-  const int64_t slot = step % p.log_cap;
-  const double clock1 = S->clock + tau;  // renewal.py:497-498
-  for (int c = 0; c < M; ++c) {
-    long long d = 0;
-    for (unsigned b = lane; b < gridDim.x; b += 32) d += __ldcg(p.part_cnt + b * kCntStride + c);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(kFull, d, o);
+  if (SMEM_MASK) stage_mask_async(s_mask, mask_cur, (uint32_t)(mask_words * 4), &s_bar);
+  const uint32_t* gmask = SMEM_MASK ? s_mask : mask_cur;
+
+  // contiguous tile run of this warp; lane j holds the run's (j)th tile
+  // boundary offset, so every tile's edge range is a shuffle away
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp, nw = (int64_t)gridDim.x * WARPS;
+  const int64_t per = (p.ntiles + nw - 1) / nw;
+  const int64_t t0 = min(gw * per, p.ntiles), t1 = min(t0 + per, p.ntiles);
+  const int ST_BYTES = (int)((32 * sizeof(ST) + 15) & ~15), AG_BYTES = (int)((32 * sizeof(AT) + 15) & ~15);
+  auto boundary = [&](int64_t base, int j) -> int64_t {  // ro32[32 * (base + j)], clamped at N
+    const int64_t node = min((base + j) * 32, p.n);
+    return (int64_t)__ldg(p.ro32 + node);
+  };
+  int64_t bnd_base = t0;
+  int64_t bnd = (t0 + lane <= t1) ? boundary(t0, lane) : 0;  // lane j: start of tile t0+j
+  auto tile_edges = [&](int64_t t, int64_t& e0, int64_t& e1) {
+    if (t - bnd_base >= 31) {  // refill the boundary window (warp-uniform)
+      bnd_base = t;
+      bnd = (t + lane <= t1) ? boundary(t, lane) : 0;
+    }
+    e0 = __shfl_sync(kFull, bnd, (int)(t - bnd_base));
+    e1 = __shfl_sync(kFull, bnd, (int)(t - bnd_base) + 1);
+  };
+  // issue the bulk copies of tile t into slot sl (lane 0)
+  auto issue = [&](int64_t t, int sl, int64_t e0, int64_t e1) {
     if (lane == 0) {
-      const int64_t v = p.S->counts[c] + d;
-      p.S->counts[c] = v;
-      p.log_counts[slot * kCntStride + c] = v;
+      unsigned char* b = wbuf + (size_t)sl * L.slot_bytes;
+      const int64_t c0 = e0 & ~3LL, c1 = (e1 + 3) & ~3LL;
+      const uint32_t col_bytes = (uint32_t)((c1 - c0) * 4);
+      const uint32_t bytes = 144u + (uint32_t)ST_BYTES + (uint32_t)AG_BYTES + col_bytes;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
+      mbar_arrive_expect_tx(&t_bar[warp][sl], bytes);
+      tma_bulk_g2s(b + L.ro_off, p.ro32 + t * 32, 144u, &t_bar[warp][sl]);
+      tma_bulk_g2s(b + L.st_off, reinterpret_cast<const ST*>(p.states) + t * 32, (uint32_t)ST_BYTES, &t_bar[warp][sl]);
+      tma_bulk_g2s(b + L.ag_off, reinterpret_cast<const AT*>(p.ages) + t * 32, (uint32_t)AG_BYTES, &t_bar[warp][sl]);
+      if (col_bytes) tma_bulk_g2s(b + L.col_off, p.col + c0, col_bytes, &t_bar[warp][sl]);
+    }
+  };
+
+  float lmax = 0.0f;
+  int qn = 0;
+  // prologue: fill the slots
+  int64_t pe0[4], pe1[4];
+#pragma unroll
+  for (int sl = 0; sl < 4; ++sl) {
+    if (sl < L.slots && t0 + sl < t1) {
+      tile_edges(t0 + sl, pe0[sl], pe1[sl]);
+      issue(t0 + sl, sl, pe0[sl], pe1[sl]);
     }
   }
-  if (lane == 0) {
-    const float maxf = __uint_as_float(mbits);
-    // tau' = min(tau_max, eps / (max rate + delta)) in f64 (renewal.py:577-578)
-    const double cand = __ddiv_rn(p.eps, __dadd_rn((double)maxf, p.delta));
-    fs_scalars* W = p.S;
-    W->last_max_rate = maxf;
-    W->tau_next = (p.tau_max <= cand) ? p.tau_max : cand;
-    W->clock = clock1;
-    W->step = step + 1;
-    W->started = 1;
-    p.log_clock[slot] = clock1;
-    p.log_tau[slot] = tau;
-    __threadfence();
-    *p.ticket = 0u;
+  if (SMEM_MASK) mbar_wait_parity(&s_bar, 0);
+  uint32_t phase_bits = 0;  // bit sl: parity of slot sl's next completion
+  int sl = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    mbar_wait_parity(&t_bar[warp][sl], (phase_bits >> sl) & 1u);
+    phase_bits ^= 1u << sl;
+    const unsigned char* b = wbuf + (size_t)sl * L.slot_bytes;
+    const uint32_t bs = smem_u32(b);
+    const int64_t tile = t;
+    const int64_t n = tile * 32 + lane;
+    const bool valid = n < p.n;
+    int s = -1;
+    float age = 0.0f;
+    if (valid) {
+      if (sizeof(ST) == 4) s = (int)lds_u32(bs + L.st_off + 4 * lane);
+      else s = (int)(int8_t)(lds_u32(bs + L.st_off + (lane & ~3)) >> (8 * (lane & 3)));
+      if (sizeof(AT) == 4) age = __uint_as_float(lds_u32(bs + L.ag_off + 4 * lane));
+      else age = __half2float(__ushort_as_half((unsigned short)(lds_u32(bs + L.ag_off + 2 * (lane & ~1)) >> (16 * (lane & 1)))));
+    }
+    const bool need = valid && (s == k.edge_from || MAT);
+    const unsigned todo = __ballot_sync(kFull, need);
+    float pressure = 0.0f;
+    if (todo) {
+      const int64_t e_first = (int32_t)lds_u32(bs + L.ro_off);
+      const int64_t c0 = e_first & ~3LL;
+      const int32_t* col_s = reinterpret_cast<const int32_t*>(b + L.col_off) - c0;  // indexed by global edge id
+      const int64_t lo = valid ? (int32_t)lds_u32(bs + L.ro_off + 4 * lane) : 0;
+      const int64_t hi = valid ? (int32_t)lds_u32(bs + L.ro_off + 4 * lane + 4) : 0;
+      const int kk = count_tile<SMEM_MASK, true>(col_s, gmask, lo, hi, need, todo, lane);
+      if (need) pressure = p.ptab_mul ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
+    }
+    __syncwarp();
+    // the slot is consumed: refill it with tile t + slots
+    const int64_t tn = t + L.slots;
+    if (tn < t1) {
+      int64_t e0, e1;
+      tile_edges(tn, e0, e1);
+      issue(tn, sl, e0, e1);
+    }
+    tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, tile, n, valid, s, age, pressure, qn, lmax, mask_nxt,
+                                            nullptr);
+    sl = (sl + 1 == L.slots) ? 0 : sl + 1;
   }
+  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
+  finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
 
 // ---------------------------------------------------------------------------
@@ -781,6 +968,33 @@ StepFn pick_step(bool mixed, int gather, int strat, bool mat, int& block) {
              : pick_step2<int32_t, float, float, false>(gather, strat, block);
 }
 
+using TmaFn = void (*)(const StepParams, const TmaLayout);
+constexpr int kTmaBlock = 512;
+
+TmaFn pick_tma(bool mixed, bool smem_mask, bool mat) {
+  if (mixed) {
+    if (smem_mask) return mat ? k_step_tma<int8_t, __half, true, true, kTmaBlock> : k_step_tma<int8_t, __half, true, false, kTmaBlock>;
+    return mat ? k_step_tma<int8_t, __half, false, true, kTmaBlock> : k_step_tma<int8_t, __half, false, false, kTmaBlock>;
+  }
+  if (smem_mask) return mat ? k_step_tma<int32_t, float, true, true, kTmaBlock> : k_step_tma<int32_t, float, true, false, kTmaBlock>;
+  return mat ? k_step_tma<int32_t, float, false, true, kTmaBlock> : k_step_tma<int32_t, float, false, false, kTmaBlock>;
+}
+
+// widest 16-byte-aligned column span of any 32-node tile (TMA slot size)
+__global__ void k_max_tile_span(const int32_t* __restrict__ ro32, int64_t n, int64_t ntiles, unsigned long long* out) {
+  unsigned long long best = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = ro32[t * 32], e1 = ro32[min((t + 1) * 32, n)];
+    const unsigned long long span = (unsigned long long)(((e1 + 3) & ~3LL) - (e0 & ~3LL));
+    best = span > best ? span : best;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, best, o);
+    best = v > best ? v : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
 MergeFn pick_merge(bool inf_bf16, int mode, int& block) {
   if (mode == 1) { block = 1024; return inf_bf16 ? k_gather_merge<__nv_bfloat16, 1, 1024> : k_gather_merge<float, 1, 1024>; }
   block = 512;
@@ -812,8 +1026,11 @@ struct fs_engine {
   float inf_val = 0.0f;  // promoted stored value of an I node (count mode)
   // launch shapes
   StepFn step_fn[2] = {nullptr, nullptr};
-  int step_block = 512, step_grid = 0;
-  size_t step_smem = 0;
+  bool tma = false;       // streaming count-gather kernel (k_step_tma)
+  TmaFn tma_fn[2] = {nullptr, nullptr};
+  TmaLayout tl{};
+  int step_block = 512, step_grid = 0, step_grid_general = 0;
+  size_t step_smem = 0, step_smem_general = 0;
   MergeFn merge_fn = nullptr;
   int merge_block = 512, merge_grid = 0;
   size_t merge_smem = 0;
@@ -938,7 +1155,10 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
       e->merge_fn<<<e->merge_grid, e->merge_block, e->merge_smem, st>>>(q);
     }
     StepParams p = make_step_params(e, e->merge, use_active);
-    e->step_fn[mat]<<<e->step_grid, e->step_block, e->step_smem, st>>>(p);
+    if (e->tma && !p.active_tiles)
+      e->tma_fn[mat]<<<e->step_grid, kTmaBlock, e->step_smem, st>>>(p, e->tl);
+    else
+      e->step_fn[mat]<<<e->step_grid_general, e->step_block, e->step_smem_general, st>>>(p);
   }
   FS_CUDA(cudaGetLastError());
   return 0;
@@ -1045,6 +1265,52 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
     const int64_t ctas_needed = (warps_needed + e->step_block / 32 - 1) / (e->step_block / 32);
     e->step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sms * occ, ctas_needed));
   }
+  e->step_grid_general = e->step_grid;
+  e->step_smem_general = e->step_smem;
+  // streaming fast path: count gather, PER_NODE, padded buffers, int32 offsets
+  if (e->count_mode && c->strategy == FS_PER_NODE && !e->merge && g->row_offsets32 && g->padded && buf->padded &&
+      g->num_edges > 0) {
+    unsigned long long* d_span = nullptr;
+    TRY(dalloc(&d_span, 1));
+    FS_CUDA(cudaMemset(d_span, 0, sizeof(unsigned long long)));
+    k_max_tile_span<<<(int)std::min<int64_t>((e->ntiles + 255) / 256, 4096), 256>>>(g->row_offsets32, n, e->ntiles, d_span);
+    unsigned long long span = 0;
+    FS_CUDA(cudaMemcpy(&span, d_span, sizeof(span), cudaMemcpyDeviceToHost));
+    cudaFree(d_span);
+    TmaLayout L{};
+    L.ro_off = 0;
+    L.st_off = 144;
+    L.ag_off = L.st_off + (int)((32 * (e->mixed ? 1 : 4) + 15) & ~15);
+    L.col_off = L.ag_off + (int)((32 * (e->mixed ? 2 : 4) + 15) & ~15);
+    L.col_cap = (int)std::min<unsigned long long>(span, 1ull << 20);
+    L.slot_bytes = (int)((L.col_off + 4 * (int64_t)L.col_cap + 127) & ~127LL);
+    const size_t mask_bytes = (size_t)((e->ntiles + 3) & ~3LL) * 4;
+    cudaFuncAttributes fa{};
+    const int warps = kTmaBlock / 32;
+    int dev_smem = 0;
+    cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    for (int smem_mask = 1; smem_mask >= 0 && !e->tma; --smem_mask) {
+      TmaFn f0 = pick_tma(e->mixed, smem_mask != 0, false);
+      if (cudaFuncGetAttributes(&fa, (const void*)f0) != cudaSuccess) break;
+      for (int slots = 4; slots >= 2; --slots) {
+        const size_t dyn = (smem_mask ? mask_bytes : 0) + (size_t)warps * slots * L.slot_bytes;
+        if (dyn + fa.sharedSizeBytes + 1024 > (size_t)dev_smem) continue;
+        L.slots = slots;
+        e->tl = L;
+        e->tma = true;
+        e->step_smem = dyn;
+        for (int mat = 0; mat < 2; ++mat) {
+          e->tma_fn[mat] = pick_tma(e->mixed, smem_mask != 0, mat != 0);
+          TRY(cudaFuncSetAttribute((const void*)e->tma_fn[mat], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) == cudaSuccess ? 0 : set_error(FS_ECUDA, "tma smem attribute"));
+        }
+        int tocc = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, (const void*)e->tma_fn[0], kTmaBlock, dyn) != cudaSuccess || tocc < 1) tocc = 1;
+        const int64_t ctas_needed = (e->ntiles + warps - 1) / warps;
+        e->step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sms * tocc, ctas_needed));
+        break;
+      }
+    }
+  }
   if (e->merge) {
     const int mode = e->count_mode ? (e->mask_smem ? 1 : 2) : 0;
     e->merge_fn = pick_merge(e->mixed, mode, e->merge_block);
@@ -1059,8 +1325,8 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
   }
 
   TRY(dalloc(&e->S, 1));
-  TRY(dalloc(&e->part_max, e->step_grid));
-  TRY(dalloc(&e->part_cnt, (size_t)e->step_grid * kCntStride));
+  TRY(dalloc(&e->part_max, std::max(e->step_grid, e->step_grid_general)));
+  TRY(dalloc(&e->part_cnt, (size_t)std::max(e->step_grid, e->step_grid_general) * kCntStride));
   TRY(dalloc(&e->ticket, 1));
   e->log_cap = std::max<int64_t>(256, 4 * (int64_t)c->steps_per_batch);
   TRY(dalloc(&e->log_clock, e->log_cap));

@@ -116,6 +116,14 @@ def default_seed_count(num_nodes: int) -> int:
     return max(10, int(round(0.01 * num_nodes)))
 
 
+def _node_buffer(n: int, dtype: torch.dtype, dev: torch.device, fill=0) -> torch.Tensor:
+    """Per-node device array, allocated to a whole number of 32-node tiles
+    (the streaming kernel bulk-copies whole tiles, fs_state_buffers.padded)
+    and returned as the [:n] view."""
+    cap = (n + 31) // 32 * 32
+    return torch.full((cap,), fill, dtype=dtype, device=dev)[:n]
+
+
 def _storage(mixed: bool):
     """(states, ages, infectivity) torch dtypes (renewal.py:358-367)."""
     if mixed:
@@ -139,9 +147,17 @@ class _DeviceGraph:
         ro = np.ascontiguousarray(g.row_offsets, dtype=np.int64)
         self.row_offsets = torch.from_numpy(ro).to(dev)
         # int32 copy for the hot kernels when every offset fits (halves the
-        # offset stream; listed in DESIGN.md as an encoding)
-        self.row_offsets32 = self.row_offsets.to(torch.int32) if self.num_edges < 2**31 else None
-        self.col_indices = torch.from_numpy(np.ascontiguousarray(g.col_indices, dtype=np.int32)).to(dev)
+        # offset stream; listed in DESIGN.md as an encoding).  Both the int32
+        # offsets and the columns carry slack past the end for 16-byte TMA
+        # bulk copies (fs_graph.padded).
+        self.row_offsets32 = None
+        if self.num_edges < 2**31:
+            r32 = torch.full((self.num_nodes + 1 + 8,), self.num_edges, dtype=torch.int32, device=dev)
+            r32[: self.num_nodes + 1] = self.row_offsets
+            self.row_offsets32 = r32[: self.num_nodes + 1]
+        col = torch.zeros(self.num_edges + 4, dtype=torch.int32, device=dev)
+        col[: self.num_edges] = torch.from_numpy(np.ascontiguousarray(g.col_indices, dtype=np.int32)).to(dev)
+        self.col_indices = col[: self.num_edges]
         w = np.ascontiguousarray(g.weights, dtype=np.float32)
         if mixed:  # weights rounded to bf16 at plan time (renewal.py:330-331)
             import ml_dtypes
@@ -165,6 +181,7 @@ class _DeviceGraph:
             weights_uniform=int(self.uniform),
             uniform_weight=self.uniform_weight,
             d_max=self.d_max,
+            padded=1,
         )
 
 
@@ -253,6 +270,7 @@ class _Engine:
             b.infectivity[0], b.infectivity[1] = _lib.ptr(self.bufs[0]), _lib.ptr(self.bufs[1])
         b.pressure = _lib.ptr(state._t.get("pressure"))
         b.rates = _lib.ptr(state._t.get("rates"))
+        b.padded = 1  # states / ages come from _node_buffer
         self._buffers = b
         h = ctypes.c_void_p()
         _lib.check(self.lib.fs_engine_create(plan.graph.view(), plan.model, plan.config, b, scal,
@@ -592,10 +610,10 @@ def init_renewal_state(g, m, cfg: RenewalConfig, seed: int, seed_count: int | No
     dev = _device.device()
     mixed = bool(cfg.mixed_precision)
     st, at, it = _storage(mixed)
-    states = torch.full((n,), int(m.edge_from), dtype=st, device=dev)
+    states = _node_buffer(n, st, dev, int(m.edge_from))
     if seed_count:
         states[_pick_seed_nodes(n, seed, seed_count, dev)] = comp
-    ages = torch.zeros(n, dtype=at, device=dev)
+    ages = _node_buffer(n, at, dev)
     # infectivity beta * s(0): s(0) = 1 for constant transmission and 0 for
     # the hazard / density profiles (h(0) = 0, f(0) = 0)
     inf = torch.zeros(n, dtype=it, device=dev)
@@ -617,8 +635,10 @@ def set_mixed_precision(state: RenewalState, on: bool) -> RenewalState:
     state._push_host()
     state._unbind()
     st, at, it = _storage(bool(on))
-    state._t["states"] = state._t["states"].to(st)
-    state._t["ages"] = state._t["ages"].to(at)
+    for name, dt in (("states", st), ("ages", at)):
+        buf = _node_buffer(state._n, dt, state._dev)
+        buf.copy_(state._t[name].to(dt))
+        state._t[name] = buf
     state._t["inf"] = state._t["inf"].to(torch.float32).to(it)
     state._mixed = bool(on)
     state._plans.clear()
