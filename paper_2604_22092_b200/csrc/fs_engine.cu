@@ -645,6 +645,22 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
 
+// thread-per-node count over a slice staged in shared memory: lane-private
+// loop, two edges per iteration; an odd tail reads the sentinel column
+// `zero_col`, whose mask word is guaranteed zero
+template <bool SMEM_MASK>
+__device__ __forceinline__ int count_slice_smem(uint32_t col_addr, int len, const uint32_t* m, uint32_t zero_col) {
+  int cnt = 0;
+  for (int i = 0; i < len; i += 2) {
+    const uint32_t c0 = lds_u32(col_addr + 4u * (uint32_t)i);
+    const uint32_t c1 = (i + 1 < len) ? lds_u32(col_addr + 4u * (uint32_t)i + 4u) : zero_col;
+    const uint32_t w0 = SMEM_MASK ? m[c0 >> 5] : __ldg(m + (c0 >> 5));
+    const uint32_t w1 = SMEM_MASK ? m[c1 >> 5] : __ldg(m + (c1 >> 5));
+    cnt += (int)(__funnelshift_r(w0, w0, c0) & 1u) + (int)(__funnelshift_r(w1, w1, c1) & 1u);
+  }
+  return cnt;
+}
+
 // ---------------------------------------------------------------------------
 // Streaming fast path of the count gather (PER_NODE strategy).
 // Each warp owns a contiguous run of 32-node tiles and keeps TMA_SLOTS of
@@ -661,7 +677,7 @@ struct TmaLayout {
   int col_cap;      // column entries a buffer holds
 };
 
-template <typename ST, typename AT, bool SMEM_MASK, bool MAT, int BLOCK>
+template <typename ST, typename AT, bool SMEM_MASK, bool MAT, bool PTAB_MUL, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const TmaLayout L) {
   extern __shared__ __align__(128) unsigned char dyn[];
   constexpr int WARPS = BLOCK / 32;
@@ -669,9 +685,13 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ __align__(8) uint64_t t_bar[WARPS][4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t mask_words = (p.ntiles + 3) & ~3LL;
+  // 32-bit indices: N < 2^31 nodes (graph.py:51) and E < 2^31 on this path
+  const int N = (int)p.n, ntiles = (int)p.ntiles;
+  const int mask_words = (ntiles + 1 + 3) & ~3;  // >= one zero word past the last tile
   uint32_t* s_mask = reinterpret_cast<uint32_t*>(dyn);
   unsigned char* wbuf = dyn + (SMEM_MASK ? mask_words * 4 : 0) + (size_t)warp * L.slots * L.slot_bytes;
+  const uint32_t wbuf_s = smem_u32(wbuf);
+  const uint32_t zero_col = (uint32_t)ntiles * 32u;  // sentinel: its mask word is zero
 
   if (tid == 0 && SMEM_MASK) mbar_init(&s_bar, 1);
   if (lane == 0)
@@ -682,97 +702,78 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
   const uint32_t* mask_cur = p.mask[cur];
   uint32_t* mask_nxt = p.mask[cur ^ 1];
   __syncthreads();
-  if (SMEM_MASK) stage_mask_async(s_mask, mask_cur, (uint32_t)(mask_words * 4), &s_bar);
+  if (SMEM_MASK) stage_mask_async(s_mask, mask_cur, (uint32_t)mask_words * 4u, &s_bar);
   const uint32_t* gmask = SMEM_MASK ? s_mask : mask_cur;
+  const ST* __restrict__ states = reinterpret_cast<const ST*>(p.states);
+  const AT* __restrict__ ages = reinterpret_cast<const AT*>(p.ages);
+  const int32_t* __restrict__ ro = p.ro32;
 
   // contiguous tile run of this warp; lane j holds the run's (j)th tile
   // boundary offset, so every tile's edge range is a shuffle away
-  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp, nw = (int64_t)gridDim.x * WARPS;
-  const int64_t per = (p.ntiles + nw - 1) / nw;
-  const int64_t t0 = min(gw * per, p.ntiles), t1 = min(t0 + per, p.ntiles);
-  const int ST_BYTES = (int)((32 * sizeof(ST) + 15) & ~15), AG_BYTES = (int)((32 * sizeof(AT) + 15) & ~15);
-  auto boundary = [&](int64_t base, int j) -> int64_t {  // ro32[32 * (base + j)], clamped at N
-    const int64_t node = min((base + j) * 32, p.n);
-    return (int64_t)__ldg(p.ro32 + node);
-  };
-  int64_t bnd_base = t0;
-  int64_t bnd = (t0 + lane <= t1) ? boundary(t0, lane) : 0;  // lane j: start of tile t0+j
-  auto tile_edges = [&](int64_t t, int64_t& e0, int64_t& e1) {
+  const int gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
+  const int per = (ntiles + nw - 1) / nw;
+  const int t0 = min(gw * per, ntiles), t1 = min(t0 + per, ntiles);
+  int bnd_base = t0;
+  int32_t bnd = (t0 + lane <= t1) ? __ldg(ro + min((t0 + lane) * 32, N)) : 0;  // first edge of tile t0+lane
+  // lane 0 streams tile t's columns [ro[32t] & ~3, (ro[32t+32] + 3) & ~3)
+  // into slot sl with one bulk copy completing on the slot's mbarrier
+  auto issue_cols = [&](int t, int sl) {
     if (t - bnd_base >= 31) {  // refill the boundary window (warp-uniform)
       bnd_base = t;
-      bnd = (t + lane <= t1) ? boundary(t, lane) : 0;
+      bnd = (t + lane <= t1) ? __ldg(ro + min((t + lane) * 32, N)) : 0;
     }
-    e0 = __shfl_sync(kFull, bnd, (int)(t - bnd_base));
-    e1 = __shfl_sync(kFull, bnd, (int)(t - bnd_base) + 1);
-  };
-  // issue the bulk copies of tile t into slot sl (lane 0)
-  auto issue = [&](int64_t t, int sl, int64_t e0, int64_t e1) {
+    const int j = t - bnd_base;
+    const int32_t c0 = __shfl_sync(kFull, bnd, j) & ~3, c1 = (__shfl_sync(kFull, bnd, j + 1) + 3) & ~3;
     if (lane == 0) {
-      unsigned char* b = wbuf + (size_t)sl * L.slot_bytes;
-      const int64_t c0 = e0 & ~3LL, c1 = (e1 + 3) & ~3LL;
-      const uint32_t col_bytes = (uint32_t)((c1 - c0) * 4);
-      const uint32_t bytes = 144u + (uint32_t)ST_BYTES + (uint32_t)AG_BYTES + col_bytes;
+      const uint32_t bytes = 4u * (uint32_t)(c1 - c0);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
       mbar_arrive_expect_tx(&t_bar[warp][sl], bytes);
-      tma_bulk_g2s(b + L.ro_off, p.ro32 + t * 32, 144u, &t_bar[warp][sl]);
-      tma_bulk_g2s(b + L.st_off, reinterpret_cast<const ST*>(p.states) + t * 32, (uint32_t)ST_BYTES, &t_bar[warp][sl]);
-      tma_bulk_g2s(b + L.ag_off, reinterpret_cast<const AT*>(p.ages) + t * 32, (uint32_t)AG_BYTES, &t_bar[warp][sl]);
-      if (col_bytes) tma_bulk_g2s(b + L.col_off, p.col + c0, col_bytes, &t_bar[warp][sl]);
+      if (bytes) tma_bulk_g2s(wbuf + (size_t)sl * L.slot_bytes, p.col + c0, bytes, &t_bar[warp][sl]);
     }
+  };
+  // per-node inputs, coalesced loads two tiles ahead (arrays are padded to
+  // whole tiles, so every lane loads unconditionally)
+  struct In { int s; float age; int32_t lo, hi; };
+  auto load_in = [&](int t, In& in) {
+    const int n = t * 32 + lane;
+    in.s = (int)states[n];
+    in.age = to_f32<AT>(ages[n]);
+    in.lo = __ldg(ro + min(n, N));
+    in.hi = __ldg(ro + min(n + 1, N));
   };
 
   float lmax = 0.0f;
   int qn = 0;
-  // prologue: fill the slots
-  int64_t pe0[4], pe1[4];
-#pragma unroll
-  for (int sl = 0; sl < 4; ++sl) {
-    if (sl < L.slots && t0 + sl < t1) {
-      tile_edges(t0 + sl, pe0[sl], pe1[sl]);
-      issue(t0 + sl, sl, pe0[sl], pe1[sl]);
-    }
-  }
+  for (int sl = 0; sl < L.slots; ++sl)
+    if (t0 + sl < t1) issue_cols(t0 + sl, sl);
+  In in0{}, in1{};
+  if (t0 < t1) load_in(t0, in0);
+  if (t0 + 1 < t1) load_in(t0 + 1, in1);
   if (SMEM_MASK) mbar_wait_parity(&s_bar, 0);
   uint32_t phase_bits = 0;  // bit sl: parity of slot sl's next completion
   int sl = 0;
-  for (int64_t t = t0; t < t1; ++t) {
+  for (int t = t0; t < t1; ++t) {
+    const In in = in0;
+    in0 = in1;
+    if (t + 2 < t1) load_in(t + 2, in1);
+    const int n = t * 32 + lane;
+    const bool valid = n < N;
+    const int s = valid ? in.s : -1;
+    const bool need = valid && (s == k.edge_from || MAT);
     mbar_wait_parity(&t_bar[warp][sl], (phase_bits >> sl) & 1u);
     phase_bits ^= 1u << sl;
-    const unsigned char* b = wbuf + (size_t)sl * L.slot_bytes;
-    const uint32_t bs = smem_u32(b);
-    const int64_t tile = t;
-    const int64_t n = tile * 32 + lane;
-    const bool valid = n < p.n;
-    int s = -1;
-    float age = 0.0f;
-    if (valid) {
-      if (sizeof(ST) == 4) s = (int)lds_u32(bs + L.st_off + 4 * lane);
-      else s = (int)(int8_t)(lds_u32(bs + L.st_off + (lane & ~3)) >> (8 * (lane & 3)));
-      if (sizeof(AT) == 4) age = __uint_as_float(lds_u32(bs + L.ag_off + 4 * lane));
-      else age = __half2float(__ushort_as_half((unsigned short)(lds_u32(bs + L.ag_off + 2 * (lane & ~1)) >> (16 * (lane & 1)))));
-    }
-    const bool need = valid && (s == k.edge_from || MAT);
-    const unsigned todo = __ballot_sync(kFull, need);
     float pressure = 0.0f;
-    if (todo) {
-      const int64_t e_first = (int32_t)lds_u32(bs + L.ro_off);
-      const int64_t c0 = e_first & ~3LL;
-      const int32_t* col_s = reinterpret_cast<const int32_t*>(b + L.col_off) - c0;  // indexed by global edge id
-      const int64_t lo = valid ? (int32_t)lds_u32(bs + L.ro_off + 4 * lane) : 0;
-      const int64_t hi = valid ? (int32_t)lds_u32(bs + L.ro_off + 4 * lane + 4) : 0;
-      const int kk = count_tile<SMEM_MASK, true>(col_s, gmask, lo, hi, need, todo, lane);
-      if (need) pressure = p.ptab_mul ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
+    const int32_t cbase = __shfl_sync(kFull, in.lo, 0) & ~3;  // the slot holds columns from cbase
+    if (need) {
+      const int kk = count_slice_smem<SMEM_MASK>(wbuf_s + (uint32_t)(sl * L.slot_bytes) + 4u * (uint32_t)(in.lo - cbase),
+                                                 in.hi - in.lo, gmask, zero_col);
+      pressure = PTAB_MUL ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
     }
     __syncwarp();
     // the slot is consumed: refill it with tile t + slots
-    const int64_t tn = t + L.slots;
-    if (tn < t1) {
-      int64_t e0, e1;
-      tile_edges(tn, e0, e1);
-      issue(tn, sl, e0, e1);
-    }
-    tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, tile, n, valid, s, age, pressure, qn, lmax, mask_nxt,
-                                            nullptr);
+    if (t + L.slots < t1) issue_cols(t + L.slots, sl);
+    tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure, qn, lmax,
+                                            mask_nxt, nullptr);
     sl = (sl + 1 == L.slots) ? 0 : sl + 1;
   }
   if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
@@ -971,13 +972,17 @@ StepFn pick_step(bool mixed, int gather, int strat, bool mat, int& block) {
 using TmaFn = void (*)(const StepParams, const TmaLayout);
 constexpr int kTmaBlock = 512;
 
-TmaFn pick_tma(bool mixed, bool smem_mask, bool mat) {
-  if (mixed) {
-    if (smem_mask) return mat ? k_step_tma<int8_t, __half, true, true, kTmaBlock> : k_step_tma<int8_t, __half, true, false, kTmaBlock>;
-    return mat ? k_step_tma<int8_t, __half, false, true, kTmaBlock> : k_step_tma<int8_t, __half, false, false, kTmaBlock>;
-  }
-  if (smem_mask) return mat ? k_step_tma<int32_t, float, true, true, kTmaBlock> : k_step_tma<int32_t, float, true, false, kTmaBlock>;
-  return mat ? k_step_tma<int32_t, float, false, true, kTmaBlock> : k_step_tma<int32_t, float, false, false, kTmaBlock>;
+template <typename ST, typename AT, bool SM, bool MAT>
+TmaFn pick_tma3(bool ptab_mul) {
+  return ptab_mul ? k_step_tma<ST, AT, SM, MAT, true, kTmaBlock> : k_step_tma<ST, AT, SM, MAT, false, kTmaBlock>;
+}
+template <typename ST, typename AT>
+TmaFn pick_tma2(bool smem_mask, bool mat, bool ptab_mul) {
+  if (smem_mask) return mat ? pick_tma3<ST, AT, true, true>(ptab_mul) : pick_tma3<ST, AT, true, false>(ptab_mul);
+  return mat ? pick_tma3<ST, AT, false, true>(ptab_mul) : pick_tma3<ST, AT, false, false>(ptab_mul);
+}
+TmaFn pick_tma(bool mixed, bool smem_mask, bool mat, bool ptab_mul) {
+  return mixed ? pick_tma2<int8_t, __half>(smem_mask, mat, ptab_mul) : pick_tma2<int32_t, float>(smem_mask, mat, ptab_mul);
 }
 
 // widest 16-byte-aligned column span of any 32-node tile (TMA slot size)
@@ -1265,6 +1270,17 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
     const int64_t ctas_needed = (warps_needed + e->step_block / 32 - 1) / (e->step_block / 32);
     e->step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sms * occ, ctas_needed));
   }
+  TRY(dalloc(&e->bad_flag, 1));
+  if (e->count_mode) {
+    e->ptab_len = (int64_t)g->d_max + 1;
+    TRY(dalloc(&e->ptab, e->ptab_len));
+    volatile float a_ = e->inf_val, w_ = g->uniform_weight;
+    const float cval = a_ * w_;  // f32(inf * w): one IEEE single multiply
+    FS_CUDA(cudaMemset(e->bad_flag, 0, sizeof(int)));
+    k_ptab<<<1, 1>>>(e->ptab, e->ptab_len, cval, e->bad_flag);
+    FS_CUDA(cudaMemcpy(&e->ptab_mul, e->bad_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    e->ptab_c = cval;
+  }
   e->step_grid_general = e->step_grid;
   e->step_smem_general = e->step_smem;
   // streaming fast path: count gather, PER_NODE, padded buffers, int32 offsets
@@ -1278,19 +1294,16 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
     FS_CUDA(cudaMemcpy(&span, d_span, sizeof(span), cudaMemcpyDeviceToHost));
     cudaFree(d_span);
     TmaLayout L{};
-    L.ro_off = 0;
-    L.st_off = 144;
-    L.ag_off = L.st_off + (int)((32 * (e->mixed ? 1 : 4) + 15) & ~15);
-    L.col_off = L.ag_off + (int)((32 * (e->mixed ? 2 : 4) + 15) & ~15);
+    L.ro_off = L.st_off = L.ag_off = L.col_off = 0;  // slots hold the column slice only
     L.col_cap = (int)std::min<unsigned long long>(span, 1ull << 20);
-    L.slot_bytes = (int)((L.col_off + 4 * (int64_t)L.col_cap + 127) & ~127LL);
-    const size_t mask_bytes = (size_t)((e->ntiles + 3) & ~3LL) * 4;
+    L.slot_bytes = (int)((4 * (int64_t)L.col_cap + 127) & ~127LL);
+    const size_t mask_bytes = (size_t)((e->ntiles + 1 + 3) & ~3LL) * 4;  // + zero sentinel word
     cudaFuncAttributes fa{};
     const int warps = kTmaBlock / 32;
     int dev_smem = 0;
     cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     for (int smem_mask = 1; smem_mask >= 0 && !e->tma; --smem_mask) {
-      TmaFn f0 = pick_tma(e->mixed, smem_mask != 0, false);
+      TmaFn f0 = pick_tma(e->mixed, smem_mask != 0, false, e->ptab_mul != 0);
       if (cudaFuncGetAttributes(&fa, (const void*)f0) != cudaSuccess) break;
       for (int slots = 4; slots >= 2; --slots) {
         const size_t dyn = (smem_mask ? mask_bytes : 0) + (size_t)warps * slots * L.slot_bytes;
@@ -1300,7 +1313,7 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
         e->tma = true;
         e->step_smem = dyn;
         for (int mat = 0; mat < 2; ++mat) {
-          e->tma_fn[mat] = pick_tma(e->mixed, smem_mask != 0, mat != 0);
+          e->tma_fn[mat] = pick_tma(e->mixed, smem_mask != 0, mat != 0, e->ptab_mul != 0);
           TRY(cudaFuncSetAttribute((const void*)e->tma_fn[mat], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) == cudaSuccess ? 0 : set_error(FS_ECUDA, "tma smem attribute"));
         }
         int tocc = 1;
@@ -1333,21 +1346,10 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
   TRY(dalloc(&e->log_tau, e->log_cap));
   TRY(dalloc(&e->log_counts, (size_t)e->log_cap * kCntStride));
   TRY(dalloc(&e->num_active, 1));
-  TRY(dalloc(&e->bad_flag, 1));
   if (c->compaction) TRY(dalloc(&e->active_tiles, e->ntiles));
   FS_CUDA(cudaMemset(e->ticket, 0, sizeof(unsigned)));
   FS_CUDA(cudaMemset(e->num_active, 0, sizeof(int64_t)));
   FS_CUDA(cudaMemcpy(e->S, scal, sizeof(fs_scalars), cudaMemcpyHostToDevice));
-  if (e->count_mode) {
-    e->ptab_len = (int64_t)g->d_max + 1;
-    TRY(dalloc(&e->ptab, e->ptab_len));
-    volatile float a_ = e->inf_val, w_ = g->uniform_weight;
-    const float cval = a_ * w_;  // f32(inf * w): one IEEE single multiply
-    FS_CUDA(cudaMemset(e->bad_flag, 0, sizeof(int)));
-    k_ptab<<<1, 1>>>(e->ptab, e->ptab_len, cval, e->bad_flag);
-    FS_CUDA(cudaMemcpy(&e->ptab_mul, e->bad_flag, sizeof(int), cudaMemcpyDeviceToHost));
-    e->ptab_c = cval;
-  }
   if (e->merge) {
     TRY(dalloc(&e->chunk_first, e->nchunks + 1));
     TRY(dalloc(&e->pre, n));

@@ -254,7 +254,7 @@ class _Engine:
         self.stream = _device.stream_handle(dev)
         _, _, it = _storage(state.mixed_precision)
         if plan.count_mode:
-            w = ((n + 31) // 32 + 3) // 4 * 4  # 16-byte multiple: staged by TMA bulk copies
+            w = ((n + 31) // 32 + 1 + 3) // 4 * 4  # + a zero sentinel word, 16-byte multiple (TMA)
             self.bufs = [torch.zeros(w, dtype=torch.int32, device=dev) for _ in range(2)]
         else:
             self.bufs = [torch.zeros(n, dtype=it, device=dev) for _ in range(2)]
