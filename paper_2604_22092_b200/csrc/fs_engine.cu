@@ -200,6 +200,41 @@ __device__ __forceinline__ void stage_mask_async(uint32_t* dst, const uint32_t* 
   }
 }
 
+// Cluster variant: the CTA of rank r in a cluster of `csize` copies chunks
+// r, r + csize, ... of the mask and multicasts each into every CTA of the
+// cluster (same smem offset, same mbarrier offset), so the cluster reads the
+// mask from L2 once instead of csize times.  Every CTA's barrier expects the
+// full byte count.  Callers must cluster-sync between barrier init and this.
+__device__ __forceinline__ void stage_mask_multicast(uint32_t* dst, const uint32_t* src, uint32_t bytes, uint64_t* bar,
+                                                     uint32_t rank, uint32_t csize) {
+  if (threadIdx.x == 0) {
+    constexpr uint32_t kChunk = 16384u;
+    const uint16_t cta_mask = (uint16_t)((1u << csize) - 1u);
+    const uint32_t nchunks = (bytes + kChunk - 1) / kChunk;
+    for (uint32_t c = rank; c < nchunks; c += csize) {
+      const uint32_t off = c * kChunk, len = min(kChunk, bytes - off);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+              smem_u32(reinterpret_cast<char*>(dst) + off)),
+          "l"(reinterpret_cast<const char*>(src) + off), "r"(len), "r"(smem_u32(bar)), "h"(cta_mask)
+          : "memory");
+    }
+  }
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // [lo, hi) of node n: int32 copy when present; neighbouring lanes share
 // boundaries, so each lane loads one offset and takes hi from lane+1
 __device__ __forceinline__ void load_slice(const int64_t* __restrict__ ro, const int32_t* __restrict__ ro32,
@@ -693,7 +728,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
   const uint32_t wbuf_s = smem_u32(wbuf);
   const uint32_t zero_col = (uint32_t)ntiles * 32u;  // sentinel: its mask word is zero
 
-  if (tid == 0 && SMEM_MASK) mbar_init(&s_bar, 1);
+  const uint32_t csize = SMEM_MASK ? cluster_size() : 1u;
+  if (tid == 0 && SMEM_MASK) {
+    mbar_init(&s_bar, 1);
+    mbar_arrive_expect_tx(&s_bar, (uint32_t)mask_words * 4u);
+  }
   if (lane == 0)
     for (int sl = 0; sl < L.slots; ++sl) mbar_init(&t_bar[warp][sl], 1);
   load_tables<WARPS>(p, sh, tid);
@@ -701,8 +740,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
   const int cur = (int)(k.step & 1);
   const uint32_t* mask_cur = p.mask[cur];
   uint32_t* mask_nxt = p.mask[cur ^ 1];
-  __syncthreads();
-  if (SMEM_MASK) stage_mask_async(s_mask, mask_cur, (uint32_t)mask_words * 4u, &s_bar);
+  if (SMEM_MASK && csize > 1) cluster_sync_all();  // peers' barriers are armed before any multicast lands
+  else __syncthreads();
+  if (SMEM_MASK) stage_mask_multicast(s_mask, mask_cur, (uint32_t)mask_words * 4u, &s_bar, cluster_rank(), csize);
   const uint32_t* gmask = SMEM_MASK ? s_mask : mask_cur;
   const ST* __restrict__ states = reinterpret_cast<const ST*>(p.states);
   const AT* __restrict__ ages = reinterpret_cast<const AT*>(p.ages);
@@ -711,8 +751,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
   // contiguous tile run of this warp; lane j holds the run's (j)th tile
   // boundary offset, so every tile's edge range is a shuffle away
   const int gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
-  const int per = (ntiles + nw - 1) / nw;
-  const int t0 = min(gw * per, ntiles), t1 = min(t0 + per, ntiles);
+  const int per = ntiles / nw, rem = ntiles % nw;  // balanced split
+  const int t0 = gw * per + min(gw, rem), t1 = t0 + per + (gw < rem ? 1 : 0);
   int bnd_base = t0;
   int32_t bnd = (t0 + lane <= t1) ? __ldg(ro + min((t0 + lane) * 32, N)) : 0;  // first edge of tile t0+lane
   // lane 0 streams tile t's columns [ro[32t] & ~3, (ro[32t+32] + 3) & ~3)
@@ -777,6 +817,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
     sl = (sl + 1 == L.slots) ? 0 : sl + 1;
   }
   if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
+  if (SMEM_MASK && csize > 1) cluster_sync_all();  // no CTA exits while its multicasts may be in flight
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
 
@@ -1034,6 +1075,7 @@ struct fs_engine {
   bool tma = false;       // streaming count-gather kernel (k_step_tma)
   TmaFn tma_fn[2] = {nullptr, nullptr};
   TmaLayout tl{};
+  int tma_cluster = 1;    // CTAs sharing one multicast mask fetch
   int step_block = 512, step_grid = 0, step_grid_general = 0;
   size_t step_smem = 0, step_smem_general = 0;
   MergeFn merge_fn = nullptr;
@@ -1160,8 +1202,21 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
       e->merge_fn<<<e->merge_grid, e->merge_block, e->merge_smem, st>>>(q);
     }
     StepParams p = make_step_params(e, e->merge, use_active);
-    if (e->tma && !p.active_tiles)
-      e->tma_fn[mat]<<<e->step_grid, kTmaBlock, e->step_smem, st>>>(p, e->tl);
+    if (e->tma && !p.active_tiles) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(e->step_grid);
+      cfg.blockDim = dim3(kTmaBlock);
+      cfg.dynamicSmemBytes = e->step_smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = e->tma_cluster;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      FS_CUDA(cudaLaunchKernelEx(&cfg, e->tma_fn[mat], p, e->tl));
+    }
     else
       e->step_fn[mat]<<<e->step_grid_general, e->step_block, e->step_smem_general, st>>>(p);
   }
@@ -1320,6 +1375,9 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, (const void*)e->tma_fn[0], kTmaBlock, dyn) != cudaSuccess || tocc < 1) tocc = 1;
         const int64_t ctas_needed = (e->ntiles + warps - 1) / warps;
         e->step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sms * tocc, ctas_needed));
+        // pairs of CTAs share the mask fetch (cluster of 2 packs all 148 SMs)
+        e->tma_cluster = (smem_mask && e->step_grid >= 2) ? 2 : 1;
+        if (e->tma_cluster > 1) e->step_grid -= e->step_grid % e->tma_cluster;
         break;
       }
     }

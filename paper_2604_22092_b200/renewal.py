@@ -315,6 +315,21 @@ class _Engine:
     def run_batch(self, materialize: bool) -> None:
         _lib.check(self.lib.fs_engine_run_batch(self.handle, int(materialize), self.stream))
 
+    def snapshot(self) -> tuple:
+        """Device copies of everything a step mutates (states, ages, the
+        infectivity / mask double buffer, scalars) — for benchmarking the
+        same step window twice."""
+        t = self.state._t
+        return (t["states"].clone(), t["ages"].clone(), [b.clone() for b in self.bufs], self.scalars())
+
+    def restore(self, snap: tuple) -> None:
+        st, ag, bufs, sc = snap
+        self.state._t["states"].copy_(st)
+        self.state._t["ages"].copy_(ag)
+        for dst, src in zip(self.bufs, bufs):
+            dst.copy_(src)
+        self.set_scalars(sc)
+
     def read_log(self, first_step: int, n: int):
         M = self.plan.num_compartments
         clocks = np.empty(n, dtype=np.float64)
