@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdarg>
+#include <cstdlib>
 #include <string>
 #include <vector>
 #include <algorithm>
@@ -86,6 +87,7 @@ struct StepParams {
   const int64_t* num_active;
   const float* pre;              // G_PRE: gathered pressure
   int count_mode;
+  unsigned long long* dbg;       // optional per-CTA %globaltimer stamps [grid][4]
   // model / config
   fs_model model;
   double eps, tau_max, delta;
@@ -221,6 +223,11 @@ __device__ __forceinline__ void stage_mask_multicast(uint32_t* dst, const uint32
     }
   }
 }
+// programmatic dependent launch: let the next step's CTAs launch now, and
+// block until the previous grid's memory is visible
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -534,23 +541,26 @@ __device__ __forceinline__ void finish_step(const StepParams& p, const StepConst
   ticket = __shfl_sync(FULL, ticket, 0);
   if (ticket != gridDim.x - 1) return;
   __threadfence();
+  // one L2 round trip: every partial is loaded independently.  Lane
+  // (half, c) sums compartment c over CTAs b = half, half + 2, ...
   unsigned mbits = 0;
   for (unsigned b = lane; b < gridDim.x; b += 32) mbits = max(mbits, __ldcg(p.part_max + b));
+  const int c = lane & 15, half = lane >> 4;
+  long long d = 0;
+  if (c < p.model.num_compartments) {
+#pragma unroll 8
+    for (unsigned b = half; b < gridDim.x; b += 2) d += __ldcg(p.part_cnt + b * kCntStride + c);
+  }
+  d += __shfl_xor_sync(FULL, d, 16);
 #pragma unroll
   for (int o = 16; o; o >>= 1) mbits = max(mbits, __shfl_xor_sync(FULL, mbits, o));
   const int64_t slot = k.step % p.log_cap;
   fs_scalars* W = p.S;
   const double clock1 = W->clock + k.tau;  // renewal.py:497-498
-  for (int c = 0; c < p.model.num_compartments; ++c) {
-    long long d = 0;
-    for (unsigned b = lane; b < gridDim.x; b += 32) d += __ldcg(p.part_cnt + b * kCntStride + c);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
-    if (lane == 0) {
-      const int64_t v = W->counts[c] + d;
-      W->counts[c] = v;
-      p.log_counts[slot * kCntStride + c] = v;
-    }
+  if (half == 0 && c < p.model.num_compartments) {
+    const int64_t v = W->counts[c] + d;
+    W->counts[c] = v;
+    p.log_counts[slot * kCntStride + c] = v;
   }
   if (lane == 0) {
     const float maxf = __uint_as_float(mbits);
@@ -591,6 +601,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   constexpr bool COUNT = (GATHER == G_COUNT_SMEM || GATHER == G_COUNT_GLOBAL);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+  pdl_wait();
   if (GATHER == G_COUNT_SMEM && tid == 0) mbar_init(&s_bar, 1);
   load_tables<WARPS>(p, sh, tid);
   const StepConst k = step_const(p, COUNT || p.count_mode);
@@ -729,21 +740,21 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
   const uint32_t zero_col = (uint32_t)ntiles * 32u;  // sentinel: its mask word is zero
 
   const uint32_t csize = SMEM_MASK ? cluster_size() : 1u;
+  if (p.dbg && tid == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    p.dbg[blockIdx.x * 4 + 0] = now;
+  }
   if (tid == 0 && SMEM_MASK) {
     mbar_init(&s_bar, 1);
     mbar_arrive_expect_tx(&s_bar, (uint32_t)mask_words * 4u);
   }
   if (lane == 0)
     for (int sl = 0; sl < L.slots; ++sl) mbar_init(&t_bar[warp][sl], 1);
+  pdl_launch_dependents();
   load_tables<WARPS>(p, sh, tid);
-  const StepConst k = step_const(p, true);
-  const int cur = (int)(k.step & 1);
-  const uint32_t* mask_cur = p.mask[cur];
-  uint32_t* mask_nxt = p.mask[cur ^ 1];
   if (SMEM_MASK && csize > 1) cluster_sync_all();  // peers' barriers are armed before any multicast lands
   else __syncthreads();
-  if (SMEM_MASK) stage_mask_multicast(s_mask, mask_cur, (uint32_t)mask_words * 4u, &s_bar, cluster_rank(), csize);
-  const uint32_t* gmask = SMEM_MASK ? s_mask : mask_cur;
   const ST* __restrict__ states = reinterpret_cast<const ST*>(p.states);
   const AT* __restrict__ ages = reinterpret_cast<const AT*>(p.ages);
   const int32_t* __restrict__ ro = p.ro32;
@@ -784,8 +795,17 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
 
   float lmax = 0.0f;
   int qn = 0;
+  // the CSR is static: stream the first column slices before waiting on the
+  // previous step (they overlap its tail under programmatic launch)
   for (int sl = 0; sl < L.slots; ++sl)
     if (t0 + sl < t1) issue_cols(t0 + sl, sl);
+  pdl_wait();  // previous step complete: scalars, states, ages, mask are final
+  const StepConst k = step_const(p, true);
+  const int cur = (int)(k.step & 1);
+  const uint32_t* mask_cur = p.mask[cur];
+  uint32_t* mask_nxt = p.mask[cur ^ 1];
+  if (SMEM_MASK) stage_mask_multicast(s_mask, mask_cur, (uint32_t)mask_words * 4u, &s_bar, cluster_rank(), csize);
+  const uint32_t* gmask = SMEM_MASK ? s_mask : mask_cur;
   In in0{}, in1{};
   if (t0 < t1) load_in(t0, in0);
   if (t0 + 1 < t1) load_in(t0 + 1, in1);
@@ -817,6 +837,16 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
     sl = (sl + 1 == L.slots) ? 0 : sl + 1;
   }
   if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
+  if (p.dbg && lane == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    atomicMax(p.dbg + blockIdx.x * 4 + 1, now);
+    if (warp == 0) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      p.dbg[blockIdx.x * 4 + 2] = sm;
+    }
+  }
   if (SMEM_MASK && csize > 1) cluster_sync_all();  // no CTA exits while its multicasts may be in flight
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
@@ -1076,6 +1106,8 @@ struct fs_engine {
   TmaFn tma_fn[2] = {nullptr, nullptr};
   TmaLayout tl{};
   int tma_cluster = 1;    // CTAs sharing one multicast mask fetch
+  bool pdl = true;        // programmatic dependent launch between steps
+  unsigned long long* dbg = nullptr;  // FS_DEBUG_TIMES: per-CTA timestamps
   int step_block = 512, step_grid = 0, step_grid_general = 0;
   size_t step_smem = 0, step_smem_general = 0;
   MergeFn merge_fn = nullptr;
@@ -1158,6 +1190,7 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active) {
   p.num_active = e->num_active;
   p.pre = use_pre ? e->pre : nullptr;
   p.count_mode = e->count_mode;
+  p.dbg = e->dbg;
   p.model = e->m;
   p.eps = e->c.epsilon;
   p.tau_max = e->c.tau_max;
@@ -1208,13 +1241,15 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
       cfg.blockDim = dim3(kTmaBlock);
       cfg.dynamicSmemBytes = e->step_smem;
       cfg.stream = st;
-      cudaLaunchAttribute attr[1];
+      cudaLaunchAttribute attr[2];
       attr[0].id = cudaLaunchAttributeClusterDimension;
       attr[0].val.clusterDim.x = e->tma_cluster;
       attr[0].val.clusterDim.y = 1;
       attr[0].val.clusterDim.z = 1;
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = e->pdl ? 1 : 0;
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = 2;
       FS_CUDA(cudaLaunchKernelEx(&cfg, e->tma_fn[mat], p, e->tl));
     }
     else
@@ -1414,6 +1449,11 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
     FS_CUDA(cudaMemset(e->pre, 0, n * sizeof(float)));
     k_chunk_first<<<(int)std::min<int64_t>((e->nchunks + 256) / 256, 4096), 256>>>(g->row_offsets, n, g->num_edges,
                                                                                   c->edges_per_block, e->nchunks, e->chunk_first);
+  }
+  if (getenv("FS_NO_PDL")) e->pdl = false;
+  if (getenv("FS_DEBUG_TIMES")) {
+    TRY(dalloc(&e->dbg, (size_t)std::max(e->step_grid, e->step_grid_general) * 4));
+    FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * std::max(e->step_grid, e->step_grid_general) * 4));
   }
   FS_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
   FS_CUDA(cudaGetLastError());
@@ -1659,4 +1699,13 @@ extern "C" int fs_pressure_gather(const fs_graph* g, const void* inf, int32_t in
   }
   FS_CUDA(cudaGetLastError());
   return 0;
+}
+
+extern "C" int fs_engine_debug_times(fs_engine* e, unsigned long long* out, int32_t max_ctas) {
+  if (!e || !e->dbg) return set_error(FS_EINVAL, "engine built without FS_DEBUG_TIMES");
+  const int n = std::min(max_ctas, std::max(e->step_grid, e->step_grid_general));
+  FS_CUDA(cudaDeviceSynchronize());
+  FS_CUDA(cudaMemcpy(out, e->dbg, sizeof(unsigned long long) * 4 * n, cudaMemcpyDeviceToHost));
+  FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * 4 * n));
+  return n;
 }
