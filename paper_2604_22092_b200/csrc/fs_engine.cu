@@ -53,6 +53,24 @@ constexpr size_t kMaxSmemMaskBytes = 188u * 1024u;  // + ~34 KB static (queues) 
 enum Gather { G_COUNT_SMEM = 0, G_COUNT_GLOBAL = 1, G_F32 = 2, G_PRE = 3 };
 enum Strat { S_THREAD = 0, S_WARP = 1 };
 
+// Device-side run scalars.  Two slots ping-pong (the host tracks which one
+// is current): step k reads slot `in` and its CTA 0 writes slot `out`, so no
+// CTA ever reads a slot being written.  `pending` = the count deltas and max
+// rate of step s.step-1 still sit in an accumulator and are folded in by the
+// next step (or by begin_batch / the host).
+struct DevState {
+  fs_scalars s;
+  int pending;
+  int pad_;
+};
+// per-step accumulator (ring of 3): every CTA adds its count deltas and maxes
+// its max rate with non-returning atomics — no fence, no ticket, no tail CTA
+struct StepAcc {
+  unsigned max_bits;
+  int pad_;
+  unsigned long long d[FS_MAX_COMPARTMENTS];
+};
+
 struct StepParams {
   // graph (renewal.py:264-313 inputs)
   const int64_t* ro;
@@ -71,11 +89,10 @@ struct StepParams {
   uint32_t* mask[2];
   float* pressure;
   float* rates;
-  fs_scalars* S;
+  const DevState* Sin;           // scalars as of this step's start
+  DevState* Sout;                // written by CTA 0 for the next step
+  StepAcc* acc;                  // ring of 3 accumulators
   // engine scratch
-  unsigned* part_max;
-  int* part_cnt;
-  unsigned* ticket;
   double* log_clock;
   double* log_tau;
   int64_t* log_counts;
@@ -113,7 +130,7 @@ struct MergeParams {
   int inf_bf16;
   const uint32_t* mask[2];       // count gather input
   const float* ptab;
-  const fs_scalars* S;           // parity source; nullptr -> buffer 0
+  const DevState* S;             // parity source; nullptr -> buffer 0
   float* out;
   int64_t nwords;
 };
@@ -405,12 +422,23 @@ __device__ __forceinline__ void load_tables(const StepParams& p, StepShared<WARP
   }
 }
 
+__device__ __forceinline__ double next_tau(const StepParams& p, float max_rate) {
+  // tau' = min(tau_max, eps / (max rate + delta)) in f64 (renewal.py:577-578)
+  const double cand = __ddiv_rn(p.eps, __dadd_rn((double)max_rate, p.delta));
+  return (p.tau_max <= cand) ? p.tau_max : cand;
+}
+
 __device__ __forceinline__ StepConst step_const(const StepParams& p, bool count_gather) {
   StepConst k;
-  const fs_scalars* S = p.S;  // written by the previous launch's last CTA
-  k.tau = S->tau_next;
-  k.step = S->step;
-  k.seed = S->seed;
+  const DevState* I = p.Sin;  // final: the previous grid completed
+  k.step = I->s.step;
+  k.seed = I->s.seed;
+  if (I->pending) {
+    const StepAcc* A = p.acc + (k.step - 1) % 3;
+    k.tau = next_tau(p, __uint_as_float(__ldcg(&A->max_bits)));
+  } else {
+    k.tau = I->s.tau_next;
+  }
   k.tau_f = __double2float_rn(k.tau);  // np.float32(tau), renewal.py:541
   k.key = splitmix_step_key(k.seed, (uint64_t)k.step);
   k.edge_from = p.model.edge_from;
@@ -419,6 +447,39 @@ __device__ __forceinline__ StepConst step_const(const StepParams& p, bool count_
   k.beta_f = __double2float_rn(p.model.beta);
   k.write_inf = !count_gather;
   return k;
+}
+
+// CTA 0 / thread 0, right after the dependency wait: publish the next
+// step's scalars.  Folds the previous step's pending deltas into the counts
+// (and the per-step log), advances the clock by this step's tau, and clears
+// the accumulator the next step will use.
+__device__ __forceinline__ void commit_step_start(const StepParams& p, const StepConst& k) {
+  const DevState* I = p.Sin;
+  DevState* O = p.Sout;
+  O->s = I->s;
+  const int M = p.model.num_compartments;
+  if (I->pending) {
+    const StepAcc* A = p.acc + (k.step - 1) % 3;
+    const int64_t prev = (k.step - 1) % p.log_cap;
+    for (int c = 0; c < M; ++c) {
+      const int64_t v = I->s.counts[c] + (int64_t)__ldcg(&A->d[c]);
+      O->s.counts[c] = v;
+      p.log_counts[prev * kCntStride + c] = v;
+    }
+    O->s.last_max_rate = __uint_as_float(__ldcg(&A->max_bits));
+  }
+  const double clock1 = I->s.clock + k.tau;  // renewal.py:497-498
+  O->s.clock = clock1;
+  O->s.tau_next = k.tau;
+  O->s.step = k.step + 1;
+  O->s.started = 1;
+  O->pending = 1;
+  const int64_t slot = k.step % p.log_cap;
+  p.log_clock[slot] = clock1;
+  p.log_tau[slot] = k.tau;
+  StepAcc* Z = p.acc + (k.step + 1) % 3;  // last read by the previous step
+  Z->max_bits = 0u;
+  for (int c = 0; c < FS_MAX_COMPARTMENTS; ++c) Z->d[c] = 0ull;
 }
 
 // next-step infectivity of a node in compartment ns at age nage (f32 gather;
@@ -519,8 +580,7 @@ __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepCons
   }
 }
 
-// block max-rate / count deltas; the last CTA to finish folds every CTA's
-// partials into the device scalars and the per-step log
+// block max-rate / count deltas into this step's accumulator
 template <int WARPS>
 __device__ __forceinline__ void finish_step(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
                                             int lane, float lmax) {
@@ -533,48 +593,11 @@ __device__ __forceinline__ void finish_step(const StepParams& p, const StepConst
   float bmax = lane < WARPS ? sh.wmax[lane] : 0.0f;
 #pragma unroll
   for (int o = 16; o; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(FULL, bmax, o));
-  if (lane == 0) p.part_max[blockIdx.x] = __float_as_uint(bmax);  // rates >= 0: bit order == value order
-  if (lane < FS_MAX_COMPARTMENTS) p.part_cnt[blockIdx.x * kCntStride + lane] = sh.cnt[lane];
-  __threadfence();
-  unsigned ticket = 0;
-  if (lane == 0) ticket = atomicAdd(p.ticket, 1u);
-  ticket = __shfl_sync(FULL, ticket, 0);
-  if (ticket != gridDim.x - 1) return;
-  __threadfence();
-  // one L2 round trip: every partial is loaded independently.  Lane
-  // (half, c) sums compartment c over CTAs b = half, half + 2, ...
-  unsigned mbits = 0;
-  for (unsigned b = lane; b < gridDim.x; b += 32) mbits = max(mbits, __ldcg(p.part_max + b));
-  const int c = lane & 15, half = lane >> 4;
-  long long d = 0;
-  if (c < p.model.num_compartments) {
-#pragma unroll 8
-    for (unsigned b = half; b < gridDim.x; b += 2) d += __ldcg(p.part_cnt + b * kCntStride + c);
-  }
-  d += __shfl_xor_sync(FULL, d, 16);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) mbits = max(mbits, __shfl_xor_sync(FULL, mbits, o));
-  const int64_t slot = k.step % p.log_cap;
-  fs_scalars* W = p.S;
-  const double clock1 = W->clock + k.tau;  // renewal.py:497-498
-  if (half == 0 && c < p.model.num_compartments) {
-    const int64_t v = W->counts[c] + d;
-    W->counts[c] = v;
-    p.log_counts[slot * kCntStride + c] = v;
-  }
-  if (lane == 0) {
-    const float maxf = __uint_as_float(mbits);
-    // tau' = min(tau_max, eps / (max rate + delta)) in f64 (renewal.py:577-578)
-    const double cand = __ddiv_rn(p.eps, __dadd_rn((double)maxf, p.delta));
-    W->last_max_rate = maxf;
-    W->tau_next = (p.tau_max <= cand) ? p.tau_max : cand;
-    W->clock = clock1;
-    W->step = k.step + 1;
-    W->started = 1;
-    p.log_clock[slot] = clock1;
-    p.log_tau[slot] = k.tau;
-    __threadfence();
-    *p.ticket = 0u;
+  StepAcc* A = p.acc + k.step % 3;
+  if (lane == 0 && bmax > 0.0f) atomicMax(&A->max_bits, __float_as_uint(bmax));  // rates >= 0: bit order == value order
+  if (lane < p.model.num_compartments) {
+    const int d = sh.cnt[lane];
+    if (d) atomicAdd(&A->d[lane], (unsigned long long)(long long)d);
   }
 }
 
@@ -605,6 +628,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   if (GATHER == G_COUNT_SMEM && tid == 0) mbar_init(&s_bar, 1);
   load_tables<WARPS>(p, sh, tid);
   const StepConst k = step_const(p, COUNT || p.count_mode);
+  if (blockIdx.x == 0 && tid == 0) commit_step_start(p, k);
   const int cur = (int)(k.step & 1);
   const uint32_t* mask_cur = p.mask[cur];
   uint32_t* mask_nxt = p.mask[cur ^ 1];
@@ -740,11 +764,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
   const uint32_t zero_col = (uint32_t)ntiles * 32u;  // sentinel: its mask word is zero
 
   const uint32_t csize = SMEM_MASK ? cluster_size() : 1u;
-  if (p.dbg && tid == 0) {
-    unsigned long long now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    p.dbg[blockIdx.x * 4 + 0] = now;
-  }
+  unsigned long long* dbg = nullptr;
+  unsigned long long* const dbg_base = p.dbg;
   if (tid == 0 && SMEM_MASK) {
     mbar_init(&s_bar, 1);
     mbar_arrive_expect_tx(&s_bar, (uint32_t)mask_words * 4u);
@@ -801,6 +822,15 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
     if (t0 + sl < t1) issue_cols(t0 + sl, sl);
   pdl_wait();  // previous step complete: scalars, states, ages, mask are final
   const StepConst k = step_const(p, true);
+  if (blockIdx.x == 0 && tid == 0) commit_step_start(p, k);
+  if (dbg_base) {
+    dbg = dbg_base + ((size_t)(k.step & 15) * gridDim.x + blockIdx.x) * 4;
+    if (tid == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      dbg[0] = now;
+    }
+  }
   const int cur = (int)(k.step & 1);
   const uint32_t* mask_cur = p.mask[cur];
   uint32_t* mask_nxt = p.mask[cur ^ 1];
@@ -837,18 +867,23 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
     sl = (sl + 1 == L.slots) ? 0 : sl + 1;
   }
   if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
-  if (p.dbg && lane == 0) {
+  if (dbg && lane == 0) {
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    atomicMax(p.dbg + blockIdx.x * 4 + 1, now);
+    atomicMax(dbg + 1, now);
     if (warp == 0) {
       unsigned sm;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-      p.dbg[blockIdx.x * 4 + 2] = sm;
+      dbg[2] = sm;
     }
   }
   if (SMEM_MASK && csize > 1) cluster_sync_all();  // no CTA exits while its multicasts may be in flight
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
+  if (dbg && tid == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    dbg[3] = now;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -863,7 +898,8 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_gather_merge
   extern __shared__ __align__(16) uint32_t s_mask[];
   constexpr int WARPS = BLOCK / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int cur = q.S ? (int)(q.S->step & 1) : 0;
+  pdl_wait();
+  const int cur = q.S ? (int)(q.S->s.step & 1) : 0;
   const uint32_t* mask_cur = q.mask[cur];
   const void* inf_cur = q.inf[cur];
   if (MODE == 1) {
@@ -934,9 +970,29 @@ __global__ void k_ptab(float* ptab, int64_t len, float c, int* exact_mul) {
   }
 }
 
-// batch prologue (renewal.py:583-597)
-__global__ void k_begin_batch(fs_scalars* S, double tau_max, int carry_tau) {
-  if (threadIdx.x == 0 && blockIdx.x == 0 && !carry_tau) S->tau_next = tau_max;
+// batch prologue (renewal.py:583-597): fold a pending step into the
+// scalars, then reset tau unless carry_tau
+__global__ void k_begin_batch(DevState* D, StepAcc* acc, int64_t* log_counts, int64_t log_cap,
+                              int M, double eps, double tau_max, double delta, int carry_tau) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (D->pending) {
+    const int64_t last = D->s.step - 1;
+    const StepAcc* A = acc + last % 3;
+    for (int c = 0; c < M; ++c) {
+      D->s.counts[c] += (int64_t)A->d[c];
+      log_counts[(last % log_cap) * kCntStride + c] = D->s.counts[c];
+    }
+    const float mx = __uint_as_float(A->max_bits);
+    D->s.last_max_rate = mx;
+    const double cand = __ddiv_rn(eps, __dadd_rn((double)mx, delta));
+    D->s.tau_next = (tau_max <= cand) ? tau_max : cand;
+    D->pending = 0;
+  }
+  if (!carry_tau) D->s.tau_next = tau_max;
+  for (int j = 0; j < 3; ++j) {
+    acc[j].max_bits = 0u;
+    for (int c = 0; c < FS_MAX_COMPARTMENTS; ++c) acc[j].d[c] = 0ull;
+  }
 }
 
 // compaction refresh at tile granularity: a 32-node tile is active if any of
@@ -971,8 +1027,8 @@ __global__ void k_zero_i64(int64_t* p) { *p = 0; }
 
 // copy the current double-buffer half (parity of S->step) onto the other
 template <typename T>
-__global__ void k_sync_buffers(const fs_scalars* S, T* b0, T* b1, int64_t n) {
-  const int cur = (int)(S->step & 1);
+__global__ void k_sync_buffers(const DevState* S, T* b0, T* b1, int64_t n) {
+  const int cur = (int)(S->s.step & 1);
   const T* src = cur ? b1 : b0;
   T* dst = cur ? b0 : b1;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -1115,10 +1171,9 @@ struct fs_engine {
   size_t merge_smem = 0;
   int64_t nchunks = 0;
   // engine-owned device scratch
-  fs_scalars* S = nullptr;
-  unsigned* part_max = nullptr;
-  int* part_cnt = nullptr;
-  unsigned* ticket = nullptr;
+  DevState* dstate = nullptr;  // [2] ping-pong run scalars
+  int s_cur = 0;               // which slot is current (host-tracked parity)
+  StepAcc* acc = nullptr;      // [3] per-step accumulators
   double* log_clock = nullptr;
   double* log_tau = nullptr;
   int64_t* log_counts = nullptr;
@@ -1134,7 +1189,7 @@ struct fs_engine {
   int* bad_flag = nullptr;
   // CUDA graphs of one batch (index: materialise last step)
   cudaStream_t cap_stream = nullptr;
-  cudaGraphExec_t batch_exec[2] = {nullptr, nullptr};
+  cudaGraphExec_t batch_exec[4] = {nullptr, nullptr, nullptr, nullptr};
   bool compaction_ready = false;
 };
 
@@ -1156,7 +1211,7 @@ int dalloc(T** p, size_t count) {
   return 0;
 }
 
-StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active) {
+StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, int in_slot) {
   StepParams p{};
   p.ro = e->g.row_offsets;
   p.ro32 = e->g.row_offsets32;
@@ -1175,10 +1230,9 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active) {
   p.mask[1] = e->b.imask[1];
   p.pressure = e->b.pressure;
   p.rates = e->b.rates;
-  p.S = e->S;
-  p.part_max = e->part_max;
-  p.part_cnt = e->part_cnt;
-  p.ticket = e->ticket;
+  p.Sin = e->dstate + in_slot;
+  p.Sout = e->dstate + (in_slot ^ 1);
+  p.acc = e->acc;
   p.log_clock = e->log_clock;
   p.log_tau = e->log_tau;
   p.log_counts = e->log_counts;
@@ -1221,7 +1275,7 @@ MergeParams make_merge_params(const fs_engine* e) {
   q.mask[0] = e->b.imask[0];
   q.mask[1] = e->b.imask[1];
   q.ptab = e->ptab;
-  q.S = e->S;
+  q.S = e->dstate + e->s_cur;
   q.out = e->pre;
   q.nwords = e->ntiles;
   return q;
@@ -1234,7 +1288,7 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
       MergeParams q = make_merge_params(e);
       e->merge_fn<<<e->merge_grid, e->merge_block, e->merge_smem, st>>>(q);
     }
-    StepParams p = make_step_params(e, e->merge, use_active);
+    StepParams p = make_step_params(e, e->merge, use_active, e->s_cur);
     if (e->tma && !p.active_tiles) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(e->step_grid);
@@ -1254,13 +1308,15 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
     }
     else
       e->step_fn[mat]<<<e->step_grid_general, e->step_block, e->step_smem_general, st>>>(p);
+    e->s_cur ^= 1;
   }
   FS_CUDA(cudaGetLastError());
   return 0;
 }
 
 int launch_begin_batch(fs_engine* e, cudaStream_t st) {
-  k_begin_batch<<<1, 32, 0, st>>>(e->S, e->c.tau_max, e->c.carry_tau);
+  k_begin_batch<<<1, 32, 0, st>>>(e->dstate + e->s_cur, e->acc, e->log_counts, e->log_cap, e->m.num_compartments,
+                                  e->c.epsilon, e->c.tau_max, e->c.delta, e->c.carry_tau);
   if (e->c.compaction) {
     uint32_t term_bits = 0;
     for (int i = 0; i < e->m.num_compartments; ++i)
@@ -1280,12 +1336,12 @@ int launch_begin_batch(fs_engine* e, cudaStream_t st) {
     // inactive tiles are never rewritten: make both buffers agree on them
     const int blocks2 = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
     if (e->count_mode)
-      k_sync_buffers<uint32_t><<<blocks2, 256, 0, st>>>(e->S, e->b.imask[0], e->b.imask[1], e->ntiles);
+      k_sync_buffers<uint32_t><<<blocks2, 256, 0, st>>>(e->dstate + e->s_cur, e->b.imask[0], e->b.imask[1], e->ntiles);
     else if (e->mixed)
-      k_sync_buffers<__nv_bfloat16><<<blocks2, 256, 0, st>>>(e->S, (__nv_bfloat16*)e->b.infectivity[0],
+      k_sync_buffers<__nv_bfloat16><<<blocks2, 256, 0, st>>>(e->dstate + e->s_cur, (__nv_bfloat16*)e->b.infectivity[0],
                                                              (__nv_bfloat16*)e->b.infectivity[1], n);
     else
-      k_sync_buffers<float><<<blocks2, 256, 0, st>>>(e->S, (float*)e->b.infectivity[0], (float*)e->b.infectivity[1], n);
+      k_sync_buffers<float><<<blocks2, 256, 0, st>>>(e->dstate + e->s_cur, (float*)e->b.infectivity[0], (float*)e->b.infectivity[1], n);
   }
   FS_CUDA(cudaGetLastError());
   return 0;
@@ -1430,19 +1486,23 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
     e->merge_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sms * mocc, ctas_needed));
   }
 
-  TRY(dalloc(&e->S, 1));
-  TRY(dalloc(&e->part_max, std::max(e->step_grid, e->step_grid_general)));
-  TRY(dalloc(&e->part_cnt, (size_t)std::max(e->step_grid, e->step_grid_general) * kCntStride));
-  TRY(dalloc(&e->ticket, 1));
+  TRY(dalloc(&e->dstate, 2));
+  TRY(dalloc(&e->acc, 3));
   e->log_cap = std::max<int64_t>(256, 4 * (int64_t)c->steps_per_batch);
   TRY(dalloc(&e->log_clock, e->log_cap));
   TRY(dalloc(&e->log_tau, e->log_cap));
   TRY(dalloc(&e->log_counts, (size_t)e->log_cap * kCntStride));
   TRY(dalloc(&e->num_active, 1));
   if (c->compaction) TRY(dalloc(&e->active_tiles, e->ntiles));
-  FS_CUDA(cudaMemset(e->ticket, 0, sizeof(unsigned)));
+  FS_CUDA(cudaMemset(e->acc, 0, 3 * sizeof(StepAcc)));
   FS_CUDA(cudaMemset(e->num_active, 0, sizeof(int64_t)));
-  FS_CUDA(cudaMemcpy(e->S, scal, sizeof(fs_scalars), cudaMemcpyHostToDevice));
+  {
+    DevState d0{};
+    d0.s = *scal;
+    d0.pending = 0;
+    FS_CUDA(cudaMemcpy(e->dstate, &d0, sizeof(DevState), cudaMemcpyHostToDevice));
+    e->s_cur = 0;
+  }
   if (e->merge) {
     TRY(dalloc(&e->chunk_first, e->nchunks + 1));
     TRY(dalloc(&e->pre, n));
@@ -1452,8 +1512,8 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
   }
   if (getenv("FS_NO_PDL")) e->pdl = false;
   if (getenv("FS_DEBUG_TIMES")) {
-    TRY(dalloc(&e->dbg, (size_t)std::max(e->step_grid, e->step_grid_general) * 4));
-    FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * std::max(e->step_grid, e->step_grid_general) * 4));
+    TRY(dalloc(&e->dbg, (size_t)std::max(e->step_grid, e->step_grid_general) * 4 * 16));
+    FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * std::max(e->step_grid, e->step_grid_general) * 4 * 16));
   }
   FS_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
   FS_CUDA(cudaGetLastError());
@@ -1468,7 +1528,7 @@ void fs_engine_destroy(fs_engine* e) {
   cudaSetDevice(e->device);
   for (auto& x : e->batch_exec) if (x) cudaGraphExecDestroy(x);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
-  void* ptrs[] = {e->S, e->part_max, e->part_cnt, e->ticket, e->log_clock, e->log_tau, e->log_counts, e->ptab,
+  void* ptrs[] = {e->dstate, e->acc, e->log_clock, e->log_tau, e->log_counts, e->ptab,
                   e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag};
   for (void* q : ptrs) if (q) cudaFree(q);
   delete e;
@@ -1502,13 +1562,17 @@ int fs_engine_run_batch(fs_engine* e, int32_t materialize, void* stream) {
   if (!e) return set_error(FS_EINVAL, "null engine");
   if (materialize && (!e->b.pressure || !e->b.rates)) return set_error(FS_EINVAL, "materialize needs pressure/rates buffers");
   FS_CUDA(cudaSetDevice(e->device));
-  const int k = materialize ? 1 : 0;
+  // one graph per (materialise, starting scalar slot): the kernels' slot
+  // pointers are baked in at capture
+  const int s0 = e->s_cur;
+  const int k = (materialize ? 2 : 0) + s0;
   if (!e->batch_exec[k]) {
     cudaGraph_t graph = nullptr;
     FS_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = launch_begin_batch(e, e->cap_stream);
     if (!rc) rc = launch_steps(e, e->c.steps_per_batch, materialize != 0, e->c.compaction != 0, e->cap_stream);
     cudaError_t err = cudaStreamEndCapture(e->cap_stream, &graph);
+    e->s_cur = s0;  // capture does not execute
     if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (err != cudaSuccess) return set_error(FS_ECUDA, "graph capture: %s", cudaGetErrorString(err));
     err = cudaGraphInstantiate(&e->batch_exec[k], graph, 0);
@@ -1516,6 +1580,24 @@ int fs_engine_run_batch(fs_engine* e, int32_t materialize, void* stream) {
     if (err != cudaSuccess) return set_error(FS_ECUDA, "graph instantiate: %s", cudaGetErrorString(err));
   }
   FS_CUDA(cudaGraphLaunch(e->batch_exec[k], (cudaStream_t)stream));
+  e->s_cur = s0 ^ (e->c.steps_per_batch & 1);
+  return 0;
+}
+
+// current scalars with a pending step folded in (host side, no writes)
+static int read_state(fs_engine* e, DevState* d, StepAcc* a, cudaStream_t st) {
+  FS_CUDA(cudaMemcpyAsync(d, e->dstate + e->s_cur, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  FS_CUDA(cudaMemcpyAsync(a, e->acc, 3 * sizeof(StepAcc), cudaMemcpyDeviceToHost, st));
+  FS_CUDA(cudaStreamSynchronize(st));
+  if (d->pending) {
+    const StepAcc& A = a[(d->s.step - 1) % 3];
+    for (int c = 0; c < e->m.num_compartments; ++c) d->s.counts[c] += (int64_t)A.d[c];
+    float mx;
+    std::memcpy(&mx, &A.max_bits, sizeof mx);
+    d->s.last_max_rate = mx;
+    const double cand = e->c.epsilon / ((double)mx + e->c.delta);  // same IEEE f64 ops as the device
+    d->s.tau_next = (e->c.tau_max <= cand) ? e->c.tau_max : cand;
+  }
   return 0;
 }
 
@@ -1525,6 +1607,10 @@ int fs_engine_read_log(fs_engine* e, int64_t first_step, int32_t n, double* cloc
   if (n > e->log_cap) return set_error(FS_EINVAL, "log request of %d steps exceeds capacity %lld", n, (long long)e->log_cap);
   FS_CUDA(cudaSetDevice(e->device));
   cudaStream_t st = (cudaStream_t)stream;
+  DevState d;
+  StepAcc a[3];
+  int rc0 = read_state(e, &d, a, st);
+  if (rc0) return rc0;
   std::vector<double> lc(e->log_cap), lt(e->log_cap);
   std::vector<int64_t> lk((size_t)e->log_cap * kCntStride);
   FS_CUDA(cudaMemcpyAsync(lc.data(), e->log_clock, lc.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1536,7 +1622,10 @@ int fs_engine_read_log(fs_engine* e, int64_t first_step, int32_t n, double* cloc
     const int64_t slot = (first_step + i) % e->log_cap;
     if (clocks) clocks[i] = lc[slot];
     if (taus) taus[i] = lt[slot];
-    if (counts) for (int c2 = 0; c2 < M; ++c2) counts[(size_t)i * M + c2] = lk[slot * kCntStride + c2];
+    const bool last_pending = d.pending && first_step + i == d.s.step - 1;  // counts not yet folded on device
+    if (counts)
+      for (int c2 = 0; c2 < M; ++c2)
+        counts[(size_t)i * M + c2] = last_pending ? d.s.counts[c2] : lk[slot * kCntStride + c2];
   }
   return 0;
 }
@@ -1544,16 +1633,24 @@ int fs_engine_read_log(fs_engine* e, int64_t first_step, int32_t n, double* cloc
 int fs_engine_get_scalars(fs_engine* e, fs_scalars* out, void* stream) {
   if (!e || !out) return set_error(FS_EINVAL, "null argument");
   FS_CUDA(cudaSetDevice(e->device));
-  FS_CUDA(cudaMemcpyAsync(out, e->S, sizeof(fs_scalars), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
-  FS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  DevState d;
+  StepAcc a[3];
+  int rc = read_state(e, &d, a, (cudaStream_t)stream);
+  if (rc) return rc;
+  *out = d.s;
   return 0;
 }
 
 int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream) {
   if (!e || !in) return set_error(FS_EINVAL, "null argument");
   FS_CUDA(cudaSetDevice(e->device));
-  FS_CUDA(cudaMemcpyAsync(e->S, in, sizeof(fs_scalars), cudaMemcpyHostToDevice, (cudaStream_t)stream));
-  FS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  cudaStream_t st = (cudaStream_t)stream;
+  DevState d{};
+  d.s = *in;
+  d.pending = 0;
+  FS_CUDA(cudaMemcpyAsync(e->dstate + e->s_cur, &d, sizeof(DevState), cudaMemcpyHostToDevice, st));
+  FS_CUDA(cudaMemsetAsync(e->acc, 0, 3 * sizeof(StepAcc), st));
+  FS_CUDA(cudaStreamSynchronize(st));
   return 0;
 }
 
@@ -1703,9 +1800,9 @@ extern "C" int fs_pressure_gather(const fs_graph* g, const void* inf, int32_t in
 
 extern "C" int fs_engine_debug_times(fs_engine* e, unsigned long long* out, int32_t max_ctas) {
   if (!e || !e->dbg) return set_error(FS_EINVAL, "engine built without FS_DEBUG_TIMES");
-  const int n = std::min(max_ctas, std::max(e->step_grid, e->step_grid_general));
+  const int n = std::min(max_ctas, e->step_grid);  // stamps of the streaming kernel, [16 steps][grid][4]
   FS_CUDA(cudaDeviceSynchronize());
-  FS_CUDA(cudaMemcpy(out, e->dbg, sizeof(unsigned long long) * 4 * n, cudaMemcpyDeviceToHost));
-  FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * 4 * n));
+  FS_CUDA(cudaMemcpy(out, e->dbg, sizeof(unsigned long long) * 4 * 16 * n, cudaMemcpyDeviceToHost));
+  FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * 4 * 16 * n));
   return n;
 }
