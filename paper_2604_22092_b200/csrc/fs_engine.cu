@@ -1097,19 +1097,20 @@ StepFn pick_step(bool mixed, int gather, int strat, bool mat, int& block) {
 }
 
 using TmaFn = void (*)(const StepParams, const TmaLayout);
-constexpr int kTmaBlock = 512;
 
-template <typename ST, typename AT, bool SM, bool MAT>
+template <typename ST, typename AT, bool SM, bool MAT, int B>
 TmaFn pick_tma3(bool ptab_mul) {
-  return ptab_mul ? k_step_tma<ST, AT, SM, MAT, true, kTmaBlock> : k_step_tma<ST, AT, SM, MAT, false, kTmaBlock>;
+  return ptab_mul ? k_step_tma<ST, AT, SM, MAT, true, B> : k_step_tma<ST, AT, SM, MAT, false, B>;
 }
-template <typename ST, typename AT>
+template <typename ST, typename AT, int B>
 TmaFn pick_tma2(bool smem_mask, bool mat, bool ptab_mul) {
-  if (smem_mask) return mat ? pick_tma3<ST, AT, true, true>(ptab_mul) : pick_tma3<ST, AT, true, false>(ptab_mul);
-  return mat ? pick_tma3<ST, AT, false, true>(ptab_mul) : pick_tma3<ST, AT, false, false>(ptab_mul);
+  if (smem_mask) return mat ? pick_tma3<ST, AT, true, true, B>(ptab_mul) : pick_tma3<ST, AT, true, false, B>(ptab_mul);
+  return mat ? pick_tma3<ST, AT, false, true, B>(ptab_mul) : pick_tma3<ST, AT, false, false, B>(ptab_mul);
 }
-TmaFn pick_tma(bool mixed, bool smem_mask, bool mat, bool ptab_mul) {
-  return mixed ? pick_tma2<int8_t, __half>(smem_mask, mat, ptab_mul) : pick_tma2<int32_t, float>(smem_mask, mat, ptab_mul);
+TmaFn pick_tma(bool mixed, bool smem_mask, bool mat, bool ptab_mul, int block) {
+  if (block == 768)
+    return mixed ? pick_tma2<int8_t, __half, 768>(smem_mask, mat, ptab_mul) : pick_tma2<int32_t, float, 768>(smem_mask, mat, ptab_mul);
+  return mixed ? pick_tma2<int8_t, __half, 512>(smem_mask, mat, ptab_mul) : pick_tma2<int32_t, float, 512>(smem_mask, mat, ptab_mul);
 }
 
 // widest 16-byte-aligned column span of any 32-node tile (TMA slot size)
@@ -1163,6 +1164,7 @@ struct fs_engine {
   TmaLayout tl{};
   int tma_cluster = 1;    // CTAs sharing one multicast mask fetch
   bool pdl = true;        // programmatic dependent launch between steps
+  int tma_block = 512;    // threads per CTA of the streaming kernel
   unsigned long long* dbg = nullptr;  // FS_DEBUG_TIMES: per-CTA timestamps
   int step_block = 512, step_grid = 0, step_grid_general = 0;
   size_t step_smem = 0, step_smem_general = 0;
@@ -1292,7 +1294,7 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
     if (e->tma && !p.active_tiles) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(e->step_grid);
-      cfg.blockDim = dim3(kTmaBlock);
+      cfg.blockDim = dim3(e->tma_block);
       cfg.dynamicSmemBytes = e->step_smem;
       cfg.stream = st;
       cudaLaunchAttribute attr[2];
@@ -1445,13 +1447,15 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
     L.slot_bytes = (int)((4 * (int64_t)L.col_cap + 127) & ~127LL);
     const size_t mask_bytes = (size_t)((e->ntiles + 1 + 3) & ~3LL) * 4;  // + zero sentinel word
     cudaFuncAttributes fa{};
-    const int warps = kTmaBlock / 32;
+    if (getenv("FS_TMA_BLOCK")) e->tma_block = atoi(getenv("FS_TMA_BLOCK")) == 768 ? 768 : 512;
+    const int warps = e->tma_block / 32;
     int dev_smem = 0;
     cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     for (int smem_mask = 1; smem_mask >= 0 && !e->tma; --smem_mask) {
-      TmaFn f0 = pick_tma(e->mixed, smem_mask != 0, false, e->ptab_mul != 0);
+      TmaFn f0 = pick_tma(e->mixed, smem_mask != 0, false, e->ptab_mul != 0, e->tma_block);
       if (cudaFuncGetAttributes(&fa, (const void*)f0) != cudaSuccess) break;
-      for (int slots = 4; slots >= 2; --slots) {
+      const int max_slots = getenv("FS_TMA_SLOTS") ? atoi(getenv("FS_TMA_SLOTS")) : 4;
+      for (int slots = std::min(4, std::max(2, max_slots)); slots >= 2; --slots) {
         const size_t dyn = (smem_mask ? mask_bytes : 0) + (size_t)warps * slots * L.slot_bytes;
         if (dyn + fa.sharedSizeBytes + 1024 > (size_t)dev_smem) continue;
         L.slots = slots;
@@ -1459,11 +1463,11 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
         e->tma = true;
         e->step_smem = dyn;
         for (int mat = 0; mat < 2; ++mat) {
-          e->tma_fn[mat] = pick_tma(e->mixed, smem_mask != 0, mat != 0, e->ptab_mul != 0);
+          e->tma_fn[mat] = pick_tma(e->mixed, smem_mask != 0, mat != 0, e->ptab_mul != 0, e->tma_block);
           TRY(cudaFuncSetAttribute((const void*)e->tma_fn[mat], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) == cudaSuccess ? 0 : set_error(FS_ECUDA, "tma smem attribute"));
         }
         int tocc = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, (const void*)e->tma_fn[0], kTmaBlock, dyn) != cudaSuccess || tocc < 1) tocc = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tocc, (const void*)e->tma_fn[0], e->tma_block, dyn) != cudaSuccess || tocc < 1) tocc = 1;
         const int64_t ctas_needed = (e->ntiles + warps - 1) / warps;
         e->step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sms * tocc, ctas_needed));
         // pairs of CTAs share the mask fetch (cluster of 2 packs all 148 SMs)
