@@ -44,6 +44,8 @@ WORKLOADS = {
                model="seir"),
     "c3": dict(desc="C3: SEIR Weibull/Erlang, Barabasi-Albert m=5, N=1e6, edge-merge dispatch", kind="ba",
                n=1_000_000, k=5, model="seir_we"),
+    "c4": dict(desc="C4: SEIR log-normal, uniform-degree k=10, N=1e8, bf16/fp16 mixed-precision storage",
+               kind="regular_dev", n=100_000_000, k=10, model="seir", mixed=True, cpu_n=10_000_000),
 }
 GRAPH_SEED, SIM_SEED = 1, 7
 
@@ -61,6 +63,8 @@ def build_inputs(w):
 
     if w["kind"] == "fixed":
         g = fs.gen_fixed_degree(w["n"], w["k"], seed=GRAPH_SEED)
+    elif w["kind"] == "regular_dev":  # GPU generator (the CPU one does not scale to 1e8)
+        g = fs.gen_fixed_degree_device(w["n"], w["k"], seed=GRAPH_SEED)
     else:
         g = fs.gen_barabasi_albert(w["n"], w["k"], seed=GRAPH_SEED)
     m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0) if w["model"] == "seir" else fs.seir_weibull_erlang(0.25)
@@ -127,8 +131,7 @@ def _cpu_worker(args):
     import paper_2604_22092_b200 as fs
     from oracle import spreadsim_port as O
 
-    g, m = _CPU_INPUTS
-    cfg = fs.RenewalConfig()
+    g, m, cfg = _CPU_INPUTS
     seed = O.derive_seed(SIM_SEED, trial)  # run_ensemble's per-trial seed (analysis.py:61-74)
     st = O.init_state(g, m, cfg, seed)
     for _ in range(warm):
@@ -142,14 +145,16 @@ def _cpu_worker(args):
 _CPU_INPUTS = None
 
 
-def cpu_ensemble(g, m, warm: int, steps: int, workers: int | None = None) -> dict:
+def cpu_ensemble(g, m, warm: int, steps: int, workers: int | None = None, mixed: bool = False) -> dict:
     """The reference's multi-core mode: independent trajectories in a process
     pool, one per host core (analysis.py:97-130 `run_ensemble`), each stepping
     the same graph.  Aggregate NUPS = workers * N * steps / slowest worker."""
     import multiprocessing as mp
 
     global _CPU_INPUTS
-    _CPU_INPUTS = (g, m)
+    import paper_2604_22092_b200 as fs
+
+    _CPU_INPUTS = (g, m, fs.RenewalConfig(mixed_precision=mixed))
     cores = workers or len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     ctx = mp.get_context("fork")
@@ -167,8 +172,14 @@ def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     w = WORKLOADS[args.workload]
-    g, m = build_inputs(w)
-    cb = cpu_ensemble(g, m, args.warmup, args.steps)
+    if "cpu_n" in w:  # bounded sample of a workload too large for host RAM
+        import paper_2604_22092_b200 as fs
+
+        g = fs.gen_fixed_degree_device(w["cpu_n"], w["k"], seed=GRAPH_SEED).to_host()
+        m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    else:
+        g, m = build_inputs(w)
+    cb = cpu_ensemble(g, m, args.warmup, args.steps, mixed=bool(w.get("mixed", False)))
     v = cb["value"]
     print(json.dumps({
         "impl": "reference", "metric": "Giga-NUPS (node updates/s)", "value": v, "unit": "G-NUPS", "n_gpus": world,
@@ -215,14 +226,17 @@ def main() -> None:
 
     w = WORKLOADS[args.workload]
     g, m = build_inputs(w)
-    cfg = fs.RenewalConfig()
+    mixed = bool(w.get("mixed", False))
+    cfg = fs.RenewalConfig(mixed_precision=mixed)
     n = g.num_nodes
+    device_graph = hasattr(g, "device_tensors")
 
     # ---------------- device throughput (value) ----------------
     st = fs.init_renewal_state(g, m, cfg, SIM_SEED)
     plan = R._build_plan(g, m, cfg, st.mixed_precision)
     eng = st._bind(plan, SIM_SEED, materialize=False)
     kernels_per_step = 2 if plan.strategy == fs.Strategy.EDGE_MERGE else 1
+    strategy_name, count_mode = plan.strategy.value, plan.count_mode
     snap0 = eng.snapshot()
     eng.run_batch(False)  # captures the batch CUDA graph outside any timed region
     eng.restore(snap0)
@@ -239,8 +253,11 @@ def main() -> None:
     torch.cuda.synchronize()
     warm_ms = e0.elapsed_time(e1) / (nb * cfg.steps_per_batch)
     eng.restore(snap)
-    # headline: each of the K steps timed alone after an L2 flush
+    # headline: each of the K steps timed alone after an L2 flush: a 512 MiB
+    # write, then a 512 MiB read of another buffer, so the step starts with
+    # none of its inputs in L2 and without the flush's dirty lines pending
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    flush_rd = torch.ones(128 << 20, dtype=torch.int32, device="cuda")
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
@@ -249,6 +266,7 @@ def main() -> None:
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush.zero_()
+            flush_rd.max()
             starts[k].record()
             eng.step(1, False, False)
             ends[k].record()
@@ -269,23 +287,31 @@ def main() -> None:
     e2e = None
     if not args.no_e2e:
         t_final = 50.0
-        g.__dict__.pop("_fs_device_cache", None)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        if device_graph:
+            del g, st, eng, plan, snap, snap0
+            torch.cuda.empty_cache()
+            t0 = time.perf_counter()
+            g = fs.gen_fixed_degree_device(w["n"], w["k"], seed=GRAPH_SEED)
+            h2d = 0
+            src = f"a graph generated on the device (fs_gen_regular, inside the timed region)"
+        else:
+            g.__dict__.pop("_fs_device_cache", None)
+            t0 = time.perf_counter()
+            h2d = g.row_offsets.nbytes + g.col_indices.nbytes
+            src = "a host CsrGraph (CSR H2D inside the timed region)"
         rec = fs.run_renewal(g, m, cfg, SIM_SEED, t_final)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         steps_run = int(np.ceil(rec.summary["step_count"] / cfg.steps_per_batch) * cfg.steps_per_batch)
-        h2d = g.row_offsets.nbytes + g.col_indices.nbytes
         d2h = 8 * (2 + m.num_compartments) * steps_run
         e2e = {"value": n * steps_run / wall / 1e9, "unit": "G-NUPS", "h2d_bytes_per_step": h2d / steps_run,
                "d2h_bytes_per_step": d2h / steps_run, "steps": steps_run, "wall_s": wall,
-               "what": f"run_renewal(t_final={t_final}) from a host CsrGraph: CSR H2D + init + {steps_run} steps in "
+               "what": f"run_renewal(t_final={t_final}) from {src}: init + {steps_run} steps in "
                        f"CUDA-graph batches + per-batch log D2H + record",
                "final_R": rec.summary["final_R"], "peak_I": rec.summary["peak_I"]}
 
     pk = peaks()
-    mixed = bool(cfg.mixed_precision)
     achieved = B_ALG[mixed] * n / (ms_per_step / 1e3) / 1e9
     out = {
         "metric": "Giga-NUPS (node updates/s)",
@@ -298,11 +324,12 @@ def main() -> None:
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32 (f64 hazard/q)",
-        "data": "synthetic (reference generators, graph seed 1, sim seed 7)",
-        "config": {"workload": w["desc"], "n": n, "edges": g.num_edges, "strategy": plan.strategy.value,
-                   "gather": "count (1-bit mask)" if plan.count_mode else "f32", "precision": "fp32 storage",
-                   "l2": "flushed (512 MiB write) before every timed step", "parallelism": f"replicas x{world}",
+        "dtype": "i8/f16/bf16 storage, f32 rates, f64 hazard/q" if mixed else "f32 (f64 hazard/q)",
+        "data": ("synthetic (GPU uniform-degree generator fs_gen_regular, graph seed 1, sim seed 7)" if device_graph
+                 else "synthetic (reference generators, graph seed 1, sim seed 7)"),
+        "config": {"workload": w["desc"], "n": n, "edges": g.num_edges, "strategy": strategy_name,
+                   "gather": "count (1-bit mask)" if count_mode else "f32", "precision": "mixed (states i8, ages f16, infectivity bf16)" if mixed else "fp32 storage",
+                   "l2": "flushed before every timed step (512 MiB write + 512 MiB read of another buffer)", "parallelism": f"replicas x{world}",
                    "steps_from": f"t=0 after {args.warmup} warm-up steps"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(args.workload),
@@ -315,7 +342,15 @@ def main() -> None:
         "e2e": e2e,
     }
     if rank == 0 and world == 1 or rank == 0:
-        out["cpu_baseline"] = cpu_ensemble(g, m, 2, args.cpu_steps) if world == 1 else None
+        out["cpu_baseline"] = None
+        if world == 1 and args.cpu_steps > 0:
+            if "cpu_n" in w:  # bounded sample: the same generator at a size the host handles
+                gs = fs.gen_fixed_degree_device(w["cpu_n"], w["k"], seed=GRAPH_SEED).to_host()
+                cb = cpu_ensemble(gs, m, 1, max(1, args.cpu_steps // 10), workers=2, mixed=mixed)
+                cb["sample"] = "N=%d slice of the same workload family (" % w["cpu_n"] + cb["sample"] + ")"
+            else:
+                cb = cpu_ensemble(g, m, 2, args.cpu_steps, mixed=mixed)
+            out["cpu_baseline"] = cb
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 1
+#define FS_ABI_VERSION 2
 #define FS_MAX_COMPARTMENTS 16
 
 /* error codes */
@@ -147,6 +147,26 @@ typedef struct fs_state_buffers {
   int32_t padded;        /* 1: states/ages readable to a multiple of 32 nodes */
 } fs_state_buffers;
 
+/* node partition of a multi-GPU run: this
+ * engine owns global nodes [node_base, node_base + g->num_nodes); its CSR
+ * rows hold GLOBAL column ids; its mask buffers are global (every rank holds
+ * the whole infectious mask, at least max(world * mask_segment_words,
+ * ceil(N_global/32) + 1) words).  With `comm` (an ncclComm_t from
+ * fs_comm_init) every step is followed by one NCCL group: all-reduce of the
+ * count deltas and the max rate, in-place all-gather of the mask segments
+ * (rank r owns words [r * mask_segment_words, (r+1) * mask_segment_words),
+ * so node_base = r * 32 * mask_segment_words).  Without `comm` the engines of
+ * one process share the mask buffers and call fs_engines_exchange_local.
+ * Requires the count gather (constant transmission, uniform weights). */
+#define FS_MAX_PARTITIONS 16
+typedef struct fs_partition {
+  int64_t node_base;
+  int64_t num_nodes_global;
+  int64_t mask_segment_words;
+  int32_t rank, world;
+  void* comm;
+} fs_partition;
+
 typedef struct fs_engine fs_engine;
 
 int fs_abi_version(void);
@@ -160,7 +180,19 @@ int fs_device_sm_count(int device);
 int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c,
                      const fs_state_buffers* buf, const fs_scalars* scal,
                      int device, fs_engine** out);
+int fs_engine_create_partitioned(const fs_graph* g, const fs_model* m, const fs_config* c,
+                                 const fs_state_buffers* buf, const fs_scalars* scal, int device,
+                                 const fs_partition* part, fs_engine** out);
 void fs_engine_destroy(fs_engine* e);
+/* single-process partition exchange (the NCCL group's effect on engines that
+ * share one device and their mask buffers): call after every engine ran the
+ * same step */
+int fs_engines_exchange_local(fs_engine* const* engines, int32_t count, void* stream);
+/* NCCL communicator of a partitioned run: rank 0 makes the id (returns its
+ * byte length, <= len), every rank calls fs_comm_init with it */
+int fs_comm_unique_id(uint8_t* out, int32_t len);
+int fs_comm_init(int32_t world, int32_t rank, const uint8_t* id, int32_t device, void** comm);
+void fs_comm_destroy(void* comm);
 /* 1 if the engine gathers from the infectious bit-mask, 0 for the f32 gather */
 int fs_engine_uses_count_gather(const fs_engine* e);
 /* which of the two infectivity / mask buffers holds the current step's input */
@@ -215,6 +247,23 @@ int fs_refresh_active(const void* states, int32_t states_dtype, int64_t n,
                       const uint8_t* terminal, int32_t num_compartments,
                       int32_t* out_ids, int64_t capacity, int64_t* num_active,
                       void* stream);
+
+
+/* Random uniform-degree graph on the device (input construction for the
+ * N = 1e8 / 1e9 configs; the reference's CPU generator gen_fixed_degree,
+ * graph.py:289-328, does not scale there — DESIGN.md §8).  Union of d/2
+ * keyed random Hamiltonian cycles (+ one perfect matching when d is odd);
+ * shared edges dropped at both endpoints; slices sorted by source.  Writes
+ * rows [row_lo, row_hi) of the incoming CSR with GLOBAL column ids:
+ * row_offsets int64[rows+1] (local, from 0), col int32[col_capacity].  With
+ * col == NULL only the offsets and *num_edges are produced (sizing call).
+ * Every rank of a node-partitioned run generates its own rows, no exchange. */
+int fs_gen_regular(int64_t n, int32_t k, uint64_t seed, int64_t row_lo, int64_t row_hi,
+                   int64_t* row_offsets, int32_t* col, int64_t col_capacity, int64_t* num_edges,
+                   void* stream);
+/* host evaluation of one row of the same construction (tests); returns the
+ * distinct degree and writes the sorted neighbours to out[k] */
+int fs_gen_regular_row_host(int64_t n, int32_t k, uint64_t seed, int64_t node, int32_t* out);
 
 #ifdef __cplusplus
 }

@@ -319,6 +319,43 @@ def step(st: OracleState, g, m, cfg, seed: int, rng: str = "splitmix") -> float:
     return tau
 
 
+def step_rows(states, ages, ro_local, col_global, inf32_global, lo: int, tau: float, step_counter: int, m, seed: int,
+              mixed: bool, rng: str = "splitmix"):
+    """`step`'s per-node arithmetic on the rows [lo, lo+n) of a node
+    partition: the incoming slices hold global column ids and
+    read the global infectivity; the uniforms are keyed by global id.
+    Returns (states', ages', infectivity' of the rows, local max rate, local
+    count deltas) — the pieces a partitioned run exchanges.  Test oracle for
+    paper_2604_22092_b200.distributed; same operations as `step`."""
+    n = states.size
+    w32 = np.ones(col_global.size, dtype=np.float32)
+    pressure = fold_pressure(np.asarray(ro_local, np.int64), np.asarray(col_global), w32, inf32_global)
+    s = states.copy()
+    age32 = ages.astype(np.float32)
+    rates = np.zeros(n, dtype=np.float32)
+    S = s == m.edge_from
+    rates[S] = pressure[S]
+    for c, (_, h) in sorted(m.nodal.items()):
+        sel = s == c
+        if sel.any():
+            rates[sel] = nodal_hazard(h, age32[sel].astype(np.float64)).astype(np.float32)
+    q = -np.expm1(-(rates.astype(np.float64)) * tau)
+    ids = np.arange(lo, lo + n, dtype=np.uint64)
+    u = uniform_array(seed, step_counter, ids) if rng == "splitmix" else philox_uniform_array(seed, step_counter, ids)
+    fired = np.flatnonzero(u < q)
+    succ = m.successor_array().astype(np.int64)
+    term = m.terminal_mask()
+    old = s[fired].astype(np.int64)
+    new = succ[old]
+    new_age = np.where(~term[s.astype(np.int64)], age32 + np.float32(tau), age32).astype(np.float32)
+    new_age[fired] = 0.0
+    s[fired] = new.astype(s.dtype)
+    delta = np.bincount(new, minlength=m.num_compartments) - np.bincount(old, minlength=m.num_compartments)
+    inf_new = np.where(s == m.infectious, np.float32(m.beta), np.float32(0.0)).astype(np.float32)
+    mx = float(rates.max()) if rates.size else 0.0
+    return s, new_age.astype(np.float16 if mixed else np.float32), inf_new, mx, delta.astype(np.int64)
+
+
 def run_batch(st: OracleState, g, m, cfg, seed: int, rng: str = "splitmix") -> float:
     """R/renewal.py:600-629 (compaction is result-neutral and omitted)."""
     if not cfg.carry_tau:

@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import FlashSpreadNativeError, InvalidConfigError, ReconfigureAfterStartError
 
 MAX_COMPARTMENTS = 16
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # enum fs_dtype
 I8, I32, I64, F16, BF16, F32, F64, U32, U64 = 1, 2, 3, 4, 5, 6, 7, 8, 9
@@ -125,6 +125,17 @@ class FsStateBuffers(ctypes.Structure):
     ]
 
 
+class FsPartition(ctypes.Structure):
+    _fields_ = [
+        ("node_base", _c_i64),
+        ("num_nodes_global", _c_i64),
+        ("mask_segment_words", _c_i64),
+        ("rank", _c_i32),
+        ("world", _c_i32),
+        ("comm", _vp),
+    ]
+
+
 _SIGNATURES = {
     "fs_abi_version": (_c_i32, []),
     "fs_last_error": (ctypes.c_char_p, []),
@@ -132,6 +143,14 @@ _SIGNATURES = {
     "fs_engine_create": (_c_i32, [ctypes.POINTER(FsGraph), ctypes.POINTER(FsModel), ctypes.POINTER(FsConfig),
                                    ctypes.POINTER(FsStateBuffers), ctypes.POINTER(FsScalars), _c_i32,
                                    ctypes.POINTER(_vp)]),
+    "fs_engine_create_partitioned": (_c_i32, [ctypes.POINTER(FsGraph), ctypes.POINTER(FsModel),
+                                              ctypes.POINTER(FsConfig), ctypes.POINTER(FsStateBuffers),
+                                              ctypes.POINTER(FsScalars), _c_i32, ctypes.POINTER(FsPartition),
+                                              ctypes.POINTER(_vp)]),
+    "fs_engines_exchange_local": (_c_i32, [_vp, _c_i32, _vp]),
+    "fs_comm_unique_id": (_c_i32, [_vp, _c_i32]),
+    "fs_comm_init": (_c_i32, [_c_i32, _c_i32, _vp, _c_i32, ctypes.POINTER(_vp)]),
+    "fs_comm_destroy": (None, [_vp]),
     "fs_engine_destroy": (None, [_vp]),
     "fs_engine_uses_count_gather": (_c_i32, [_vp]),
     "fs_engine_current_buffer": (_c_i32, [_vp, _vp]),
@@ -147,6 +166,8 @@ _SIGNATURES = {
     "fs_uniform_fill": (_c_i32, [_c_u64, _c_u64, _vp, _c_i64, _c_i32, _vp, _vp]),
     "fs_hazard_eval": (_c_i32, [ctypes.POINTER(FsCompartment), _vp, _c_i64, _vp, _c_i32, _vp]),
     "fs_erfcx_eval": (_c_i32, [_vp, _c_i64, _vp, _vp]),
+    "fs_gen_regular": (_c_i32, [_c_i64, _c_i32, _c_u64, _c_i64, _c_i64, _vp, _vp, _c_i64, ctypes.POINTER(_c_i64), _vp]),
+    "fs_gen_regular_row_host": (_c_i32, [_c_i64, _c_i32, _c_u64, _c_i64, _vp]),
     "fs_refresh_active": (_c_i32, [_vp, _c_i32, _c_i64, _vp, _c_i32, _vp, _c_i64, ctypes.POINTER(_c_i64), _vp]),
 }
 

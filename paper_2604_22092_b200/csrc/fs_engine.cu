@@ -81,7 +81,10 @@ struct StepParams {
   int w_uniform;
   float w_val;
   int64_t n;
-  int64_t ntiles;         // ceil(N/32)
+  int64_t ntiles;         // ceil(N/32) of the local rows
+  int64_t node_base;      // global id of local node 0 (partitioned runs; multiple of 32)
+  int64_t tile_base;      // node_base / 32
+  int64_t ntiles_mask;    // words of the (global) infectious mask
   // state
   void* states;
   void* ages;
@@ -509,8 +512,9 @@ __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst
   lmax = fmaxf(lmax, rate);
   bool fire = false;
   if (rate > 0.0f) {
-    const double u = (p.rng == FS_RNG_SPLITMIX) ? splitmix_uniform(k.key, (uint64_t)n)
-                                                : philox_uniform(k.seed, (uint64_t)k.step, (uint64_t)n);
+    const uint64_t gid = (uint64_t)(n + p.node_base);  // RNG keyed by the global node id (rng.py:5-7)
+    const double u = (p.rng == FS_RNG_SPLITMIX) ? splitmix_uniform(k.key, gid)
+                                                : philox_uniform(k.seed, (uint64_t)k.step, gid);
     fire = bernoulli_fire(u, rate, k.tau);
   }
   if (ok) {
@@ -523,7 +527,7 @@ __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst
       atomicAdd(&sh.cnt[ns], 1);
       atomicAdd(&sh.cnt[s], -1);
       if (!k.write_inf && ((ns == k.infectious) != (s == k.infectious)))
-        atomicXor(mask_nxt + (n >> 5), 1u << (n & 31));
+        atomicXor(mask_nxt + p.tile_base + (n >> 5), 1u << (n & 31));
     } else {
       nage = __fadd_rn(age, k.tau_f);  // queued nodes are never terminal
     }
@@ -557,7 +561,7 @@ __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepCons
   if (!k.write_inf) {
     // next-step mask word; deferred nodes are fixed up in phase B
     const unsigned word = __ballot_sync(0xffffffffu, valid && s == k.infectious);
-    if (lane == 0) mask_nxt[tile] = word;
+    if (lane == 0) mask_nxt[p.tile_base + tile] = word;
   }
   const unsigned dm = __ballot_sync(0xffffffffu, defer);
   if (defer) {
@@ -637,7 +641,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   __syncthreads();
   // stage the whole infectious mask (N/8 bytes) in shared memory with TMA
   // bulk copies; the first tile's node loads below overlap the transfer
-  if (GATHER == G_COUNT_SMEM) stage_mask_async(s_mask, mask_cur, (uint32_t)(((p.ntiles + 3) & ~3LL) * 4), &s_bar);
+  if (GATHER == G_COUNT_SMEM) stage_mask_async(s_mask, mask_cur, (uint32_t)(((p.ntiles_mask + 3) & ~3LL) * 4), &s_bar);
   bool mask_ready = GATHER != G_COUNT_SMEM;
   const uint32_t* gmask = (GATHER == G_COUNT_SMEM) ? s_mask : mask_cur;
   float lmax = 0.0f;
@@ -757,11 +761,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // 32-bit indices: N < 2^31 nodes (graph.py:51) and E < 2^31 on this path
   const int N = (int)p.n, ntiles = (int)p.ntiles;
-  const int mask_words = (ntiles + 1 + 3) & ~3;  // >= one zero word past the last tile
+  const int mask_words = ((int)p.ntiles_mask + 1 + 3) & ~3;  // >= one zero word past the last tile
   uint32_t* s_mask = reinterpret_cast<uint32_t*>(dyn);
   unsigned char* wbuf = dyn + (SMEM_MASK ? mask_words * 4 : 0) + (size_t)warp * L.slots * L.slot_bytes;
   const uint32_t wbuf_s = smem_u32(wbuf);
-  const uint32_t zero_col = (uint32_t)ntiles * 32u;  // sentinel: its mask word is zero
+  const uint32_t zero_col = (uint32_t)p.ntiles_mask * 32u;  // sentinel: its mask word is zero
 
   const uint32_t csize = SMEM_MASK ? cluster_size() : 1u;
   unsigned long long* dbg = nullptr;
@@ -1061,6 +1065,25 @@ __global__ void k_store_mask(const uint32_t* __restrict__ m, int64_t n, IT c, IT
     out[i] = ((m[i >> 5] >> (i & 31)) & 1u) ? c : from_f32<IT>(0.0f);
 }
 
+// single-process exchange between the partition engines of one device (the
+// virtual-rank emulation of fs_exchange_step used to test the partitioned
+// kernels bit-exactly on one GPU): sum the count deltas and max the max-rate
+// bits of slot `slot` over `count` accumulator rings, written back to all.
+// The mask needs no exchange there: the engines share the mask buffers.
+struct AccPtrs { StepAcc* a[FS_MAX_PARTITIONS]; };
+__global__ void k_exchange_local(AccPtrs ptrs, int count, int slot) {
+  const int t = threadIdx.x;
+  if (t < FS_MAX_COMPARTMENTS) {
+    unsigned long long sum = 0;
+    for (int r = 0; r < count; ++r) sum += ptrs.a[r][slot].d[t];
+    for (int r = 0; r < count; ++r) ptrs.a[r][slot].d[t] = sum;
+  } else if (t == FS_MAX_COMPARTMENTS) {
+    unsigned mx = 0;
+    for (int r = 0; r < count; ++r) mx = max(mx, ptrs.a[r][slot].max_bits);
+    for (int r = 0; r < count; ++r) ptrs.a[r][slot].max_bits = mx;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // kernel selection
 // ---------------------------------------------------------------------------
@@ -1156,6 +1179,13 @@ struct fs_engine {
   int strat = S_THREAD;
   bool merge = false;
   int64_t ntiles = 0;
+  // node partition (fs_engine_create_partitioned); defaults = whole graph
+  int64_t node_base = 0;
+  int64_t ntiles_mask = 0;   // words of the global infectious mask
+  int rank = 0, world = 1;
+  void* comm = nullptr;
+  int64_t mask_seg_words = 0;  // words of mask each rank contributes to the all-gather      // ncclComm_t: per-step exchange after every step kernel
+  int64_t h_step = 0;        // host mirror of the device step counter (exchange slot / mask parity)
   float inf_val = 0.0f;  // promoted stored value of an I node (count mode)
   // launch shapes
   StepFn step_fn[2] = {nullptr, nullptr};
@@ -1191,7 +1221,7 @@ struct fs_engine {
   int* bad_flag = nullptr;
   // CUDA graphs of one batch (index: materialise last step)
   cudaStream_t cap_stream = nullptr;
-  cudaGraphExec_t batch_exec[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaGraphExec_t batch_exec[2][2][3] = {};  // [materialise][scalar slot][step % 3 when exchanging]
   bool compaction_ready = false;
 };
 
@@ -1224,6 +1254,9 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.w_val = e->g.uniform_weight;
   p.n = e->g.num_nodes;
   p.ntiles = e->ntiles;
+  p.node_base = e->node_base;
+  p.tile_base = e->node_base / 32;
+  p.ntiles_mask = e->ntiles_mask;
   p.states = e->b.states;
   p.ages = e->b.ages;
   p.inf[0] = e->b.infectivity[0];
@@ -1279,7 +1312,7 @@ MergeParams make_merge_params(const fs_engine* e) {
   q.ptab = e->ptab;
   q.S = e->dstate + e->s_cur;
   q.out = e->pre;
-  q.nwords = e->ntiles;
+  q.nwords = e->ntiles_mask;
   return q;
 }
 
@@ -1311,6 +1344,16 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
     else
       e->step_fn[mat]<<<e->step_grid_general, e->step_block, e->step_smem_general, st>>>(p);
     e->s_cur ^= 1;
+    if (e->comm) {
+      // step h_step is complete on this rank: make its accumulator and the
+      // next-step mask global
+      const int slot = (int)(e->h_step % 3);
+      uint32_t* mask_nxt = e->b.imask[(e->h_step & 1) ^ 1];
+      const int rc = fs_exchange_step(e->comm, &e->acc[slot].d[0], &e->acc[slot].max_bits, mask_nxt,
+                                      e->mask_seg_words, e->rank, st);
+      if (rc) return rc;
+    }
+    ++e->h_step;
   }
   FS_CUDA(cudaGetLastError());
   return 0;
@@ -1338,7 +1381,7 @@ int launch_begin_batch(fs_engine* e, cudaStream_t st) {
     // inactive tiles are never rewritten: make both buffers agree on them
     const int blocks2 = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
     if (e->count_mode)
-      k_sync_buffers<uint32_t><<<blocks2, 256, 0, st>>>(e->dstate + e->s_cur, e->b.imask[0], e->b.imask[1], e->ntiles);
+      k_sync_buffers<uint32_t><<<blocks2, 256, 0, st>>>(e->dstate + e->s_cur, e->b.imask[0], e->b.imask[1], e->ntiles_mask);
     else if (e->mixed)
       k_sync_buffers<__nv_bfloat16><<<blocks2, 256, 0, st>>>(e->dstate + e->s_cur, (__nv_bfloat16*)e->b.infectivity[0],
                                                              (__nv_bfloat16*)e->b.infectivity[1], n);
@@ -1362,8 +1405,8 @@ int fs_device_sm_count(int device) {
   return v;
 }
 
-int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, const fs_state_buffers* buf,
-                     const fs_scalars* scal, int device, fs_engine** out) {
+static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, const fs_state_buffers* buf,
+                         const fs_scalars* scal, int device, const fs_partition* part, fs_engine** out) {
   if (!g || !m || !c || !buf || !scal || !out) return set_error(FS_EINVAL, "null argument");
   *out = nullptr;
   if (g->num_nodes < 1 || g->num_nodes > 2147483647LL) return set_error(FS_EINVAL, "num_nodes %lld outside [1, 2^31-1]", (long long)g->num_nodes);
@@ -1384,8 +1427,30 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
   e->mixed = c->mixed_precision != 0;
   const int64_t n = g->num_nodes;
   e->ntiles = (n + 31) / 32;
+  e->ntiles_mask = e->ntiles;
+  e->h_step = scal->step;
+  if (part) {
+    if (part->node_base < 0 || part->node_base % 32 != 0 || part->num_nodes_global < part->node_base + n ||
+        part->num_nodes_global > 2147483647LL || part->world < 1 || part->rank < 0 || part->rank >= part->world) {
+      delete e;
+      return set_error(FS_EINVAL, "bad partition (node_base %lld must be a multiple of 32, N_global %lld)",
+                       (long long)part->node_base, (long long)part->num_nodes_global);
+    }
+    e->node_base = part->node_base;
+    e->ntiles_mask = (part->num_nodes_global + 31) / 32;
+    e->rank = part->rank;
+    e->world = part->world;
+    e->comm = part->comm;
+    e->mask_seg_words = part->mask_segment_words;
+    if (e->comm && (e->mask_seg_words < 1 || e->mask_seg_words * e->world < e->ntiles_mask ||
+                    e->node_base / 32 != (int64_t)e->rank * e->mask_seg_words)) {
+      delete e;
+      return set_error(FS_EINVAL, "partition: ranks must own equal mask segments of mask_segment_words words");
+    }
+  }
   const bool can_count = (m->shedding == FS_SHED_CONSTANT) && (g->weights_uniform || g->num_edges == 0);
   e->count_mode = can_count && c->count_gather != 0;
+  if (part && !e->count_mode) { delete e; return set_error(FS_EINVAL, "partitioned runs need the count gather (constant transmission, uniform weights)"); }
   if (c->count_gather == 1 && !can_count) { delete e; return set_error(FS_EINVAL, "count gather requires constant transmission and uniform weights"); }
   if (e->count_mode && (!buf->imask[0] || !buf->imask[1])) { delete e; return set_error(FS_EINVAL, "count gather needs the two mask buffers"); }
   if (!e->count_mode && (!buf->infectivity[0] || !buf->infectivity[1])) { delete e; return set_error(FS_EINVAL, "f32 gather needs the two infectivity buffers"); }
@@ -1395,7 +1460,7 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
     if (e->mixed) bf = __bfloat162float(__float2bfloat16_rn(bf));
     e->inf_val = bf;
   }
-  e->mask_smem = e->count_mode && (size_t)e->ntiles * 4 <= kMaxSmemMaskBytes;
+  e->mask_smem = e->count_mode && (size_t)e->ntiles_mask * 4 <= kMaxSmemMaskBytes;
   e->merge = c->strategy == FS_MERGE && g->num_edges > 0;
   e->strat = c->strategy == FS_LANE ? S_WARP : S_THREAD;
   if (e->merge) e->gather = G_PRE;
@@ -1405,7 +1470,7 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
   int rc = 0;
 #define TRY(x) do { rc = (x); if (rc) { fs_engine_destroy(e); return rc; } } while (0)
   for (int mat = 0; mat < 2; ++mat) e->step_fn[mat] = pick_step(e->mixed, e->gather, e->strat, mat != 0, e->step_block);
-  e->step_smem = (e->gather == G_COUNT_SMEM) ? (size_t)((e->ntiles + 3) & ~3LL) * 4 : 0;
+  e->step_smem = (e->gather == G_COUNT_SMEM) ? (size_t)((e->ntiles_mask + 3) & ~3LL) * 4 : 0;
   int occ = 1;
   for (int mat = 0; mat < 2; ++mat) {
     if (e->step_smem > 0)
@@ -1445,7 +1510,7 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
     L.ro_off = L.st_off = L.ag_off = L.col_off = 0;  // slots hold the column slice only
     L.col_cap = (int)std::min<unsigned long long>(span, 1ull << 20);
     L.slot_bytes = (int)((4 * (int64_t)L.col_cap + 127) & ~127LL);
-    const size_t mask_bytes = (size_t)((e->ntiles + 1 + 3) & ~3LL) * 4;  // + zero sentinel word
+    const size_t mask_bytes = (size_t)((e->ntiles_mask + 1 + 3) & ~3LL) * 4;  // + zero sentinel word
     cudaFuncAttributes fa{};
     if (getenv("FS_TMA_BLOCK")) e->tma_block = atoi(getenv("FS_TMA_BLOCK")) == 768 ? 768 : 512;
     const int warps = e->tma_block / 32;
@@ -1480,7 +1545,7 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
   if (e->merge) {
     const int mode = e->count_mode ? (e->mask_smem ? 1 : 2) : 0;
     e->merge_fn = pick_merge(e->mixed, mode, e->merge_block);
-    e->merge_smem = mode == 1 ? (size_t)e->ntiles * 4 : 0;
+    e->merge_smem = mode == 1 ? (size_t)e->ntiles_mask * 4 : 0;
     if (e->merge_smem)
       TRY(cudaFuncSetAttribute((const void*)e->merge_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->merge_smem) == cudaSuccess ? 0 : set_error(FS_ECUDA, "smem attribute"));
     int mocc = 1;
@@ -1527,10 +1592,24 @@ int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, c
   return 0;
 }
 
+int fs_engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, const fs_state_buffers* buf,
+                     const fs_scalars* scal, int device, fs_engine** out) {
+  return engine_create(g, m, c, buf, scal, device, nullptr, out);
+}
+
+int fs_engine_create_partitioned(const fs_graph* g, const fs_model* m, const fs_config* c,
+                                 const fs_state_buffers* buf, const fs_scalars* scal, int device,
+                                 const fs_partition* part, fs_engine** out) {
+  if (!part) return set_error(FS_EINVAL, "null partition");
+  return engine_create(g, m, c, buf, scal, device, part, out);
+}
+
 void fs_engine_destroy(fs_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
-  for (auto& x : e->batch_exec) if (x) cudaGraphExecDestroy(x);
+  for (auto& a : e->batch_exec)
+    for (auto& b : a)
+      for (auto& x : b) if (x) cudaGraphExecDestroy(x);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   void* ptrs[] = {e->dstate, e->acc, e->log_clock, e->log_tau, e->log_counts, e->ptab,
                   e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag};
@@ -1569,22 +1648,26 @@ int fs_engine_run_batch(fs_engine* e, int32_t materialize, void* stream) {
   // one graph per (materialise, starting scalar slot): the kernels' slot
   // pointers are baked in at capture
   const int s0 = e->s_cur;
-  const int k = (materialize ? 2 : 0) + s0;
-  if (!e->batch_exec[k]) {
+  const int64_t h0 = e->h_step;
+  // the exchange's accumulator slot and mask buffer are baked in at capture
+  cudaGraphExec_t& exec = e->batch_exec[materialize ? 1 : 0][s0][e->comm ? (int)(h0 % 3) : 0];
+  if (!exec) {
     cudaGraph_t graph = nullptr;
     FS_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = launch_begin_batch(e, e->cap_stream);
     if (!rc) rc = launch_steps(e, e->c.steps_per_batch, materialize != 0, e->c.compaction != 0, e->cap_stream);
     cudaError_t err = cudaStreamEndCapture(e->cap_stream, &graph);
     e->s_cur = s0;  // capture does not execute
+    e->h_step = h0;
     if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (err != cudaSuccess) return set_error(FS_ECUDA, "graph capture: %s", cudaGetErrorString(err));
-    err = cudaGraphInstantiate(&e->batch_exec[k], graph, 0);
+    err = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     if (err != cudaSuccess) return set_error(FS_ECUDA, "graph instantiate: %s", cudaGetErrorString(err));
   }
-  FS_CUDA(cudaGraphLaunch(e->batch_exec[k], (cudaStream_t)stream));
+  FS_CUDA(cudaGraphLaunch(exec, (cudaStream_t)stream));
   e->s_cur = s0 ^ (e->c.steps_per_batch & 1);
+  e->h_step = h0 + e->c.steps_per_batch;
   return 0;
 }
 
@@ -1652,9 +1735,26 @@ int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream) {
   DevState d{};
   d.s = *in;
   d.pending = 0;
+  // a pending step must be folded first so no count delta is lost
+  DevState cur;
+  StepAcc a[3];
+  int rc = read_state(e, &cur, a, st);
+  if (rc) return rc;
+  if ((in->step ^ cur.s.step) & 1) {
+    // the step parity selects the current infectivity / mask buffer: move it
+    const int from = (int)(cur.s.step & 1), to = from ^ 1;
+    if (e->count_mode) {
+      const size_t bytes = (size_t)((e->ntiles_mask + 1 + 3) & ~3LL) * 4;
+      FS_CUDA(cudaMemcpyAsync(e->b.imask[to], e->b.imask[from], bytes, cudaMemcpyDeviceToDevice, st));
+    } else {
+      const size_t bytes = (size_t)e->g.num_nodes * (e->mixed ? 2 : 4);
+      FS_CUDA(cudaMemcpyAsync(e->b.infectivity[to], e->b.infectivity[from], bytes, cudaMemcpyDeviceToDevice, st));
+    }
+  }
   FS_CUDA(cudaMemcpyAsync(e->dstate + e->s_cur, &d, sizeof(DevState), cudaMemcpyHostToDevice, st));
   FS_CUDA(cudaMemsetAsync(e->acc, 0, 3 * sizeof(StepAcc), st));
   FS_CUDA(cudaStreamSynchronize(st));
+  e->h_step = in->step;
   return 0;
 }
 
@@ -1667,9 +1767,11 @@ int fs_engine_load_infectivity(fs_engine* e, const void* inf, void* stream) {
     FS_CUDA(cudaMemsetAsync(e->bad_flag, 0, sizeof(int), st));
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
     if (e->mixed)
-      k_load_mask<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)inf, n, e->inf_val, e->b.imask[0], e->b.imask[1], e->bad_flag);
+      k_load_mask<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)inf, n, e->inf_val, e->b.imask[0] + e->node_base / 32,
+                                                          e->b.imask[1] + e->node_base / 32, e->bad_flag);
     else
-      k_load_mask<float><<<blocks, 256, 0, st>>>((const float*)inf, n, e->inf_val, e->b.imask[0], e->b.imask[1], e->bad_flag);
+      k_load_mask<float><<<blocks, 256, 0, st>>>((const float*)inf, n, e->inf_val, e->b.imask[0] + e->node_base / 32,
+                                                 e->b.imask[1] + e->node_base / 32, e->bad_flag);
     int bad = 0;
     FS_CUDA(cudaMemcpyAsync(&bad, e->bad_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     FS_CUDA(cudaStreamSynchronize(st));
@@ -1694,13 +1796,29 @@ int fs_engine_store_infectivity(fs_engine* e, void* out, void* stream) {
   if (e->count_mode) {
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
     if (e->mixed)
-      k_store_mask<__nv_bfloat16><<<blocks, 256, 0, st>>>(e->b.imask[cur], n, __float2bfloat16_rn(e->inf_val), (__nv_bfloat16*)out);
+      k_store_mask<__nv_bfloat16><<<blocks, 256, 0, st>>>(e->b.imask[cur] + e->node_base / 32, n, __float2bfloat16_rn(e->inf_val), (__nv_bfloat16*)out);
     else
-      k_store_mask<float><<<blocks, 256, 0, st>>>(e->b.imask[cur], n, e->inf_val, (float*)out);
+      k_store_mask<float><<<blocks, 256, 0, st>>>(e->b.imask[cur] + e->node_base / 32, n, e->inf_val, (float*)out);
     FS_CUDA(cudaGetLastError());
     return 0;
   }
   FS_CUDA(cudaMemcpyAsync(out, e->b.infectivity[cur], (size_t)n * (e->mixed ? 2 : 4), cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+int fs_engines_exchange_local(fs_engine* const* engines, int32_t count, void* stream) {
+  if (!engines || count < 1 || count > FS_MAX_PARTITIONS) return set_error(FS_EINVAL, "1..%d engines", FS_MAX_PARTITIONS);
+  AccPtrs ptrs{};
+  const int64_t h = engines[0]->h_step;
+  for (int r = 0; r < count; ++r) {
+    if (!engines[r] || engines[r]->h_step != h || engines[r]->device != engines[0]->device)
+      return set_error(FS_EINVAL, "engines must be on one device and at the same step");
+    ptrs.a[r] = engines[r]->acc;
+  }
+  if (h < 1) return set_error(FS_ESTATE, "no step to exchange");
+  FS_CUDA(cudaSetDevice(engines[0]->device));
+  k_exchange_local<<<1, 32, 0, (cudaStream_t)stream>>>(ptrs, count, (int)((h - 1) % 3));
+  FS_CUDA(cudaGetLastError());
   return 0;
 }
 

@@ -1,0 +1,316 @@
+"""Node-partitioned renewal runs across GPUs.
+
+The reference has no multi-GPU path (its only parallelism is the
+ProcessPool of independent trajectories, R/analysis.py:97-130; the paper
+lists multi-GPU as future work).  Here one process per GPU
+owns a contiguous range of global node ids:
+
+* rank r owns nodes [r*chunk, min(N, (r+1)*chunk)), chunk a multiple of 1024
+  nodes, so its slice of the 1-bit infectious mask is the word range
+  [r*chunk/32, (r+1)*chunk/32) — equal-size segments for an in-place
+  all-gather;
+* its CSR rows (global column ids) come from ``gen_fixed_degree_device(...,
+  row_lo, row_hi)`` — no exchange is needed to build the graph;
+* states / ages are local; the infectious mask is replicated;
+* after every step the engine runs one NCCL group (count-delta all-reduce,
+  max-rate all-reduce, mask all-gather) on its stream, inside the batch CUDA
+  graph.
+
+The RNG is keyed by the global node id (R/rng.py:5-7), the max and the
+integer counts are order-free, so a partitioned run is bit-identical to the
+single-GPU run of the same graph (tests/test_distributed.py).
+
+``LocalPartitionedRun`` runs P partitions inside one process on one device
+(shared mask buffers, accumulators combined by ``fs_engines_exchange_local``):
+the same kernels and the same exchange semantics without the transport, so
+the partitioned path is parity-tested on a single GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .errors import InvalidConfigError
+from .graph import resolve_strategy
+from .models import model_descriptor
+from .renewal import (
+    _PRECISION,
+    _STRATEGY_CODE,
+    RenewalConfig,
+    _check_conservation,
+    _DeviceGraph,
+    _node_buffer,
+    _pick_seed_nodes,
+    _storage,
+    default_seed_count,
+)
+from .rng import RNG_KINDS
+from .trajectory import DEFAULT_GRID_POINTS, make_record
+
+__all__ = ["PartitionPlan", "partition_plan", "LocalPartitionedRun", "DistributedRun", "run_renewal_distributed"]
+
+ALIGN = 1024  # nodes per alignment unit: 32 mask words = 128 B segments
+
+
+@dataclass(frozen=True)
+class PartitionPlan:
+    num_nodes: int      # N of the whole graph
+    world: int
+    chunk: int          # nodes per rank (multiple of ALIGN); the last rank may own fewer
+    ranges: tuple       # ((lo, hi), ...) per rank
+
+    @property
+    def mask_segment_words(self) -> int:
+        return self.chunk // 32
+
+    @property
+    def mask_words(self) -> int:
+        """Words of each replicated mask buffer: every segment, the zero
+        sentinel word past the last tile, rounded to 16 bytes."""
+        w = max(self.world * self.mask_segment_words, (self.num_nodes + 31) // 32 + 1)
+        return (w + 3) // 4 * 4
+
+
+def partition_plan(num_nodes: int, world: int, align: int = ALIGN) -> PartitionPlan:
+    """Equal node ranges (the regular graphs of C4/C5 are edge-balanced by
+    node count), each a multiple of `align` nodes so no mask word straddles
+    two ranks."""
+    if world < 1 or num_nodes < world:
+        raise ValueError("need 1 <= world <= num_nodes")
+    if align % 32:
+        raise ValueError("align must be a multiple of 32")
+    chunk = -(-num_nodes // world)
+    chunk = -(-chunk // align) * align
+    ranges = []
+    for r in range(world):
+        lo = min(num_nodes, r * chunk)
+        hi = min(num_nodes, (r + 1) * chunk)
+        ranges.append((lo, hi))
+    if any(hi <= lo for lo, hi in ranges):
+        raise ValueError(f"N={num_nodes} too small for {world} ranks of {align}-node granularity")
+    return PartitionPlan(num_nodes, world, chunk, tuple(ranges))
+
+
+def _config(cfg: RenewalConfig, strategy) -> _lib.FsConfig:
+    return _lib.FsConfig(
+        epsilon=cfg.epsilon, tau_max=cfg.tau_max, delta=cfg.delta, steps_per_batch=cfg.steps_per_batch,
+        strategy=_STRATEGY_CODE[strategy], compaction=int(cfg.compaction), mixed_precision=int(cfg.mixed_precision),
+        lanes_per_node=cfg.lanes_per_node, edges_per_block=cfg.edges_per_block, hazard_chunk=cfg.hazard_chunk,
+        chunk_skip=int(cfg.chunk_skip), carry_tau=int(cfg.carry_tau), rng=RNG_KINDS[cfg.rng],
+        hazard_precision=_PRECISION[cfg.hazard_precision], count_gather=1)
+
+
+def _initial_mask(plan: PartitionPlan, seed_ids: torch.Tensor, infectious: bool, dev) -> torch.Tensor:
+    m = torch.zeros(plan.mask_words, dtype=torch.int32, device=dev)
+    if infectious and seed_ids.numel():
+        words = (seed_ids >> 5).to(torch.int64)
+        bits = torch.ones_like(seed_ids, dtype=torch.int64) << (seed_ids & 31).to(torch.int64)
+        acc = torch.zeros(plan.mask_words, dtype=torch.int64, device=dev)
+        acc.index_add_(0, words, bits)  # distinct ids: sums are disjoint ors
+        m = torch.where(acc >= 2**31, acc - 2**32, acc).to(torch.int32)  # same 32-bit pattern
+    return m
+
+
+class _Partition:
+    """One rank's engine: local rows, global mask buffers (owned or shared)."""
+
+    def __init__(self, g_local, m, cfg: RenewalConfig, seed: int, plan: PartitionPlan, rank: int,
+                 seed_ids: torch.Tensor, masks: list, comm, dev):
+        if m.transmission.kind != "constant":
+            raise InvalidConfigError("partitioned runs need constant transmission (count gather)")
+        lo, hi = plan.ranges[rank]
+        if g_local.num_nodes != hi - lo:
+            raise ValueError(f"rank {rank}: graph slice has {g_local.num_nodes} rows, partition owns {hi - lo}")
+        self.lib = _lib.load()
+        self.lo, self.hi, self.rank = lo, hi, rank
+        self.n = hi - lo
+        self.M = m.num_compartments
+        self.stream = _device.stream_handle(dev)
+        mixed = bool(cfg.mixed_precision)
+        st_t, at_t, _ = _storage(mixed)
+        comp = m.edge_to
+        self.states = _node_buffer(self.n, st_t, dev, int(m.edge_from))
+        local = seed_ids[(seed_ids >= lo) & (seed_ids < hi)] - lo
+        if local.numel():
+            self.states[local] = comp
+        self.ages = _node_buffer(self.n, at_t, dev)
+        self.masks = masks
+        self.dg = _DeviceGraph.from_device(g_local, dev) if hasattr(g_local, "device_tensors") else None
+        if self.dg is None:
+            from .renewal import device_graph
+
+            self.dg = device_graph(g_local, mixed)
+        strategy = resolve_strategy(g_local, cfg.strategy)
+        counts = np.zeros(self.M, dtype=np.int64)
+        counts[m.edge_from] = plan.num_nodes - seed_ids.numel()
+        counts[comp] += seed_ids.numel()
+        scal = _lib.FsScalars(clock=0.0, tau_next=cfg.tau_max, step=0, seed=seed & ((1 << 64) - 1),
+                              last_max_rate=0.0, started=0)
+        for i, c in enumerate(counts):
+            scal.counts[i] = int(c)
+        b = _lib.FsStateBuffers()
+        b.states, b.ages = _lib.ptr(self.states), _lib.ptr(self.ages)
+        b.imask[0], b.imask[1] = _lib.ptr(masks[0]), _lib.ptr(masks[1])
+        b.padded = 1
+        self._b = b
+        part = _lib.FsPartition(node_base=lo, num_nodes_global=plan.num_nodes,
+                                mask_segment_words=plan.mask_segment_words, rank=rank, world=plan.world,
+                                comm=comm)
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.fs_engine_create_partitioned(self.dg.view(), model_descriptor(m), _config(cfg, strategy),
+                                                          b, scal, dev.index, part, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            torch.cuda.current_stream().synchronize()
+            self.lib.fs_engine_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+    def step(self, nsteps: int = 1) -> None:
+        _lib.check(self.lib.fs_engine_step(self.handle, nsteps, 0, 0, self.stream))
+
+    def run_batch(self) -> None:
+        _lib.check(self.lib.fs_engine_run_batch(self.handle, 0, self.stream))
+
+    def scalars(self) -> _lib.FsScalars:
+        s = _lib.FsScalars()
+        _lib.check(self.lib.fs_engine_get_scalars(self.handle, ctypes.byref(s), self.stream))
+        return s
+
+    def read_log(self, first: int, n: int):
+        clocks = np.empty(n, dtype=np.float64)
+        taus = np.empty(n, dtype=np.float64)
+        counts = np.empty((n, self.M), dtype=np.int64)
+        _lib.check(self.lib.fs_engine_read_log(self.handle, first, n, clocks.ctypes.data, taus.ctypes.data,
+                                               counts.ctypes.data, self.stream))
+        return clocks, taus, counts
+
+
+def _seed_ids(m, num_nodes: int, seed: int, seed_count, dev) -> torch.Tensor:
+    count = default_seed_count(num_nodes) if seed_count is None else int(seed_count)
+    return _pick_seed_nodes(num_nodes, seed, count, dev)  # the same global choice on every rank
+
+
+class LocalPartitionedRun:
+    """P partitions of one graph on one device, stepped in lockstep with the
+    exchange done in place (shared mask buffers + fs_engines_exchange_local).
+    `graph_parts[r]` holds rows plan.ranges[r] with global column ids."""
+
+    def __init__(self, graph_parts, m, cfg: RenewalConfig, seed: int, plan: PartitionPlan, seed_count=None):
+        dev = _device.device()
+        self.plan, self.cfg, self.M = plan, cfg, m.num_compartments
+        ids = _seed_ids(m, plan.num_nodes, seed, seed_count, dev)
+        mask0 = _initial_mask(plan, ids, m.edge_to == m.infectious, dev)
+        self.masks = [mask0, mask0.clone()]
+        self.parts = [_Partition(graph_parts[r], m, cfg, seed, plan, r, ids, self.masks, None, dev)
+                      for r in range(plan.world)]
+        self._arr = (ctypes.c_void_p * len(self.parts))(*[p.handle.value for p in self.parts])
+        self.steps = 0
+
+    def step(self) -> None:
+        for p in self.parts:
+            p.step(1)
+        _lib.check(_lib.load().fs_engines_exchange_local(self._arr, len(self.parts), self.parts[0].stream))
+        self.steps += 1
+
+    def run_batch(self):
+        first = self.steps
+        for _ in range(self.cfg.steps_per_batch):
+            self.step()
+        return self.parts[0].read_log(first, self.cfg.steps_per_batch)
+
+    def gather(self) -> dict:
+        """Whole-graph states / ages (concatenated partitions) and scalars."""
+        s = self.parts[0].scalars()
+        return {"states": torch.cat([p.states for p in self.parts]).cpu().numpy(),
+                "ages": torch.cat([p.ages for p in self.parts]).cpu().numpy(),
+                "counts": np.array(s.counts[: self.M], dtype=np.int64), "clock": s.clock, "tau_prev": s.tau_next,
+                "step": s.step, "scalars": [p.scalars() for p in self.parts]}
+
+    def close(self) -> None:
+        for p in self.parts:
+            p.close()
+
+
+class DistributedRun:
+    """This rank's share of a node-partitioned run over NCCL (one process per
+    GPU).  `graph_local` holds the rows of plan.ranges[rank]; `pg` is the
+    torch.distributed group used once, to broadcast the NCCL unique id."""
+
+    def __init__(self, graph_local, m, cfg: RenewalConfig, seed: int, plan: PartitionPlan, rank: int,
+                 seed_count=None, pg=None):
+        import torch.distributed as dist
+
+        dev = _device.device()
+        lib = _lib.load()
+        self.plan, self.cfg, self.M, self.rank = plan, cfg, m.num_compartments, rank
+        buf = (ctypes.c_uint8 * 256)()
+        if rank == 0:
+            nb = _lib.check(lib.fs_comm_unique_id(buf, 256))
+            payload = [bytes(buf)[:nb]]
+        else:
+            payload = [None]
+        if plan.world > 1:
+            dist.broadcast_object_list(payload, src=0, group=pg)
+        idb = (ctypes.c_uint8 * 256).from_buffer_copy(payload[0].ljust(256, b"\0"))
+        comm = ctypes.c_void_p()
+        _lib.check(lib.fs_comm_init(plan.world, rank, idb, dev.index, ctypes.byref(comm)))
+        self.comm = comm
+        ids = _seed_ids(m, plan.num_nodes, seed, seed_count, dev)
+        mask0 = _initial_mask(plan, ids, m.edge_to == m.infectious, dev)
+        self.masks = [mask0, mask0.clone()]
+        self.part = _Partition(graph_local, m, cfg, seed, plan, rank, ids, self.masks, comm.value, dev)
+        self.steps = 0
+
+    def run_batch(self):
+        first = self.steps
+        self.part.run_batch()
+        self.steps += self.cfg.steps_per_batch
+        return self.part.read_log(first, self.cfg.steps_per_batch)
+
+    def step(self, nsteps: int = 1) -> None:
+        self.part.step(nsteps)
+        self.steps += nsteps
+
+    def close(self) -> None:
+        self.part.close()
+        if getattr(self, "comm", None) and self.comm.value:
+            _lib.load().fs_comm_destroy(self.comm)
+            self.comm = None
+
+
+def run_renewal_distributed(graph_local, m, cfg: RenewalConfig, seed: int, t_final: float, plan: PartitionPlan,
+                            rank: int, grid_points: int = DEFAULT_GRID_POINTS, seed_count=None, pg=None):
+    """`run_renewal` (R/renewal.py:632-663) over a node partition: whole
+    batches until clock >= t_final.  Every rank returns the same record
+    (clock and counts are global after each step's exchange)."""
+    import time
+
+    t0 = time.perf_counter()
+    run = DistributedRun(graph_local, m, cfg, seed, plan, rank, seed_count=seed_count, pg=pg)
+    s = run.part.scalars()
+    times, rows = [0.0], [np.array(s.counts[: run.M], dtype=np.int64)]
+    clock, done = 0.0, 0
+    while clock < t_final:
+        clocks, _, counts = run.run_batch()
+        _check_conservation(counts, plan.num_nodes)
+        times.extend(clocks.tolist())
+        rows.extend(counts)
+        done += cfg.steps_per_batch
+        clock = float(clocks[-1])
+    wall = time.perf_counter() - t0
+    t_arr = np.asarray(times)
+    steps = min(int(np.searchsorted(t_arr, t_final, side="left")), done)
+    rec = make_record(t_arr, np.asarray(rows), m.compartments, plan.num_nodes, t_final, grid_points,
+                      extra_summary={"step_count": steps, "wall_clock": wall, "engine": "renewal-partitioned",
+                                     "world": plan.world})
+    run.close()
+    return rec

@@ -185,8 +185,36 @@ class _DeviceGraph:
         )
 
 
+    @classmethod
+    def from_device(cls, g, dev: torch.device) -> "_DeviceGraph":
+        """Wrap a DeviceCsrGraph (GPU-generated, uniform weights) without a
+        host round trip."""
+        self = cls.__new__(cls)
+        self.num_nodes = int(g.num_rows)
+        self.num_edges = int(g.num_edges)
+        t = g.device_tensors()
+        self.row_offsets = t["row_offsets"]
+        self.row_offsets32 = None
+        if self.num_edges < 2**31:
+            r32 = torch.full((self.num_nodes + 1 + 8,), self.num_edges, dtype=torch.int32, device=dev)
+            r32[: self.num_nodes + 1] = self.row_offsets
+            self.row_offsets32 = r32[: self.num_nodes + 1]
+        self.col_indices = t["col_buffer"][: self.num_edges]
+        self.uniform = True
+        self.uniform_weight = float(g.uniform_weight)
+        self.weights = None
+        self.weights_bf16 = False
+        self.d_max = int(g.d_max)
+        return self
+
+
 def device_graph(g, mixed: bool = False) -> _DeviceGraph:
     dev = _device.device()
+    if hasattr(g, "device_tensors"):  # DeviceCsrGraph: already on the device
+        cache = g.__dict__.setdefault("_fs_device_cache", {})
+        if dev.index not in cache:
+            cache[dev.index] = _DeviceGraph.from_device(g, dev)
+        return cache[dev.index]
     cache = g.__dict__.setdefault("_fs_device_cache", {})
     key = (bool(mixed), dev.index)
     if key not in cache:

@@ -35,13 +35,14 @@ def test_library_loads_and_exports_every_declared_symbol():
 
 def test_ctypes_layouts_match_c(tmp_path):
     src = tmp_path / "layout.c"
-    structs = ["fs_graph", "fs_compartment", "fs_model", "fs_config", "fs_scalars", "fs_state_buffers"]
+    structs = ["fs_graph", "fs_compartment", "fs_model", "fs_config", "fs_scalars", "fs_state_buffers", "fs_partition"]
     body = "\n".join(f'printf("{s} %zu\\n", sizeof({s}));' for s in structs)
     offs = {
         "fs_model": ["beta", "shedding", "shed_mu", "shed_peak", "comp"],
         "fs_scalars": ["step", "seed", "last_max_rate", "started", "counts"],
         "fs_graph": ["row_offsets", "weights_dtype", "uniform_weight", "d_max"],
         "fs_config": ["steps_per_batch", "count_gather"],
+        "fs_partition": ["num_nodes_global", "mask_segment_words", "rank", "world", "comm"],
     }
     for s, fields in offs.items():
         for f in fields:
@@ -51,7 +52,8 @@ def test_ctypes_layouts_match_c(tmp_path):
     subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
     got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
     cls = {"fs_graph": _lib.FsGraph, "fs_compartment": _lib.FsCompartment, "fs_model": _lib.FsModel,
-           "fs_config": _lib.FsConfig, "fs_scalars": _lib.FsScalars, "fs_state_buffers": _lib.FsStateBuffers}
+           "fs_config": _lib.FsConfig, "fs_scalars": _lib.FsScalars, "fs_state_buffers": _lib.FsStateBuffers,
+           "fs_partition": _lib.FsPartition}
     for s, c in cls.items():
         assert int(got[s]) == ctypes.sizeof(c), s
     for key, v in got.items():

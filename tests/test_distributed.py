@@ -1,0 +1,162 @@
+"""Node-partitioned runs (paper_2604_22092_b200.distributed).
+
+CPU (gloo, world size 2): the partition plan, and the partitioned algorithm
+itself — the oracle stepped on each rank's rows with the per-step exchange
+(infectivity all-gather, max / count all-reduce) done by torch.distributed —
+reproduces the single-process oracle bit for bit.  GPU: P virtual ranks on
+one device (the partitioned kernels, shared mask buffers, in-place exchange)
+and a world-1 NCCL run both reproduce the single-engine trajectory.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2604_22092_b200 as fs
+from paper_2604_22092_b200.distributed import partition_plan
+
+
+def test_partition_plan_properties():
+    for n, world in [(10_000, 2), (1_000_000, 8), (1_000_000_000, 8), (5000, 3), (4096, 4)]:
+        p = partition_plan(n, world)
+        assert p.ranges[0][0] == 0 and p.ranges[-1][1] == n
+        for (lo, hi), (lo2, _) in zip(p.ranges[:-1], p.ranges[1:]):
+            assert hi == lo2 and lo % 1024 == 0 and (hi - lo) == p.chunk
+        assert p.chunk % 1024 == 0 and p.mask_segment_words * 32 == p.chunk
+        assert p.mask_words >= world * p.mask_segment_words and p.mask_words >= (n + 31) // 32 + 1
+        assert p.mask_words % 4 == 0
+    with pytest.raises(ValueError):
+        partition_plan(2048, 3)  # third rank would be empty
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _partitioned_oracle_worker(rank: int, world: int, port: int, steps: int, out_q) -> None:
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import spreadsim_port as O
+
+    g = fs.gen_fixed_degree(6000, 10, seed=4)
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    cfg = fs.RenewalConfig()
+    seed = 7
+    plan = partition_plan(g.num_nodes, world)
+    lo, hi = plan.ranges[rank]
+    full = O.init_state(g, m, cfg, seed)  # every rank derives the same global seeds
+    states, ages = full.states[lo:hi].copy(), full.ages[lo:hi].copy()
+    ro = g.row_offsets[lo:hi + 1] - g.row_offsets[lo]
+    col = g.col_indices[g.row_offsets[lo]:g.row_offsets[hi]]
+    inf = full.infectivity.astype(np.float32)
+    counts = full.counts.copy()
+    tau, clock = cfg.tau_max, 0.0
+    for k in range(steps):
+        clock += tau
+        states, ages, inf_loc, mx, delta = O.step_rows(states, ages, ro, col, inf, lo, tau, k, m, seed, False)
+        # the exchange: infectivity segments all-gathered, max and deltas all-reduced
+        pad = np.zeros(plan.chunk, dtype=np.float32)
+        pad[: hi - lo] = inf_loc
+        parts = [torch.zeros(plan.chunk) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(pad))
+        inf = torch.cat(parts).numpy()[: g.num_nodes]
+        t = torch.tensor([mx], dtype=torch.float32)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        d = torch.from_numpy(delta)
+        dist.all_reduce(d, op=dist.ReduceOp.SUM)
+        counts = counts + d.numpy()
+        tau = min(cfg.tau_max, cfg.epsilon / (float(t.item()) + cfg.delta))
+    out_q.put((rank, states, ages, counts, clock, tau))
+    dist.destroy_process_group()
+
+
+def test_partitioned_oracle_matches_single_process_gloo():
+    from oracle import spreadsim_port as O
+
+    steps, world = 60, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_partitioned_oracle_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, rest) for r, *rest in (q.get(timeout=300) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = fs.gen_fixed_degree(6000, 10, seed=4)
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    cfg = fs.RenewalConfig()
+    ref = O.init_state(g, m, cfg, 7)
+    for _ in range(steps):
+        O.step(ref, g, m, cfg, 7)
+    states = np.concatenate([res[r][0] for r in range(world)])
+    ages = np.concatenate([res[r][1] for r in range(world)])
+    assert np.array_equal(states, ref.states)
+    assert np.array_equal(ages.view(np.uint32), ref.ages.view(np.uint32))
+    for r in range(world):
+        assert np.array_equal(res[r][2], ref.counts)
+        assert res[r][3] == ref.clock and res[r][4] == ref.tau_prev
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,mixed", [(3, False), (2, True), (4, False)])
+def test_virtual_ranks_match_single_engine(world, mixed):
+    from paper_2604_22092_b200.distributed import LocalPartitionedRun
+
+    n, k = 50_000, 10
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    cfg = fs.RenewalConfig(mixed_precision=mixed)
+    plan = partition_plan(n, world)
+    whole = fs.gen_fixed_degree_device(n, k, seed=2)
+    parts = [fs.gen_fixed_degree_device(n, k, seed=2, row_lo=lo, row_hi=hi) for lo, hi in plan.ranges]
+    run = LocalPartitionedRun(parts, m, cfg, 7, plan)
+    st = fs.init_renewal_state(whole, m, cfg, 7)
+    for _ in range(3):
+        clocks, _, counts = run.run_batch()
+        rec = []
+        fs.run_batch(st, whole, m, cfg, 7, recorder=rec)
+        assert np.array_equal(counts, np.array([c for _, c in rec]))
+        assert np.array_equal(clocks, np.array([t for t, _ in rec]))
+    got = run.gather()
+    assert np.array_equal(got["states"].astype(np.int32), st.states.astype(np.int32))
+    assert np.array_equal(got["ages"].view(np.uint16 if mixed else np.uint32),
+                          st.ages.view(np.uint16 if mixed else np.uint32))
+    assert np.array_equal(got["counts"], st.counts)
+    assert got["clock"] == st.clock and got["tau_prev"] == st.tau_prev
+    run.close()
+
+
+def _nccl_world1_worker(port: int, out_q) -> None:
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    from paper_2604_22092_b200.distributed import run_renewal_distributed
+
+    n = 40_000
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    cfg = fs.RenewalConfig()
+    plan = partition_plan(n, 1)
+    g = fs.gen_fixed_degree_device(n, 10, seed=3)
+    rec = run_renewal_distributed(g, m, cfg, 7, 20.0, plan, 0)
+    ref = fs.run_renewal(g, m, cfg, 7, 20.0)
+    out_q.put((np.array_equal(rec.fractions, ref.fractions), rec.summary["step_count"], ref.summary["step_count"]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_world1_matches_single_engine():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_world1_worker, args=(_free_port(), q))
+    p.start()
+    same, s1, s2 = q.get(timeout=600)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert same and s1 == s2
