@@ -44,6 +44,9 @@ WORKLOADS = {
                model="seir"),
     "c3": dict(desc="C3: SEIR Weibull/Erlang, Barabasi-Albert m=5, N=1e6, edge-merge dispatch", kind="ba",
                n=1_000_000, k=5, model="seir_we"),
+    "c5": dict(desc="C5: SEIR log-normal, uniform-degree k=10, N=1e9, node-partitioned across the GPUs "
+                    "(NCCL mask all-gather + max/count all-reduce per step)",
+               kind="regular_dev", n=1_000_000_000, k=10, model="seir", cpu_n=10_000_000, t_final=10.0),
     "c4": dict(desc="C4: SEIR log-normal, uniform-degree k=10, N=1e8, bf16/fp16 mixed-precision storage",
                kind="regular_dev", n=100_000_000, k=10, model="seir", mixed=True, cpu_n=10_000_000),
 }
@@ -193,13 +196,100 @@ def run_reference(args, rank: int, world: int) -> None:
     }))
 
 
+def run_partitioned(args, w, rank: int, world: int, local: int) -> None:
+    """Node-partitioned run over `world` GPUs: each rank
+    generates its own rows of the graph, owns that node range, and exchanges
+    the infectious mask + max rate + count deltas with NCCL after every step.
+    Strong scaling: the graph (w["n"] nodes) is fixed as the GPU count grows.
+    Inputs are far larger than L2, so the K steps are timed as back-to-back
+    CUDA-graph batches (no flush needed), max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_22092_b200 as fs
+    from paper_2604_22092_b200.distributed import DistributedRun, partition_plan, run_renewal_distributed
+
+    n_total = w["n"]
+    plan = partition_plan(n_total, world)
+    lo, hi = plan.ranges[rank]
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    mixed = bool(w.get("mixed", False))
+    cfg = fs.RenewalConfig(mixed_precision=mixed)
+    g = fs.gen_fixed_degree_device(n_total, w["k"], seed=GRAPH_SEED, row_lo=lo, row_hi=hi)
+    edges = torch.tensor([g.num_edges], dtype=torch.int64, device="cuda")
+    dist.all_reduce(edges)
+    run = DistributedRun(g, m, cfg, SIM_SEED, plan, rank)
+    run.step(args.warmup)
+    run.run_batch()  # capture the batch graph (NCCL inside) outside the timed region
+    nb = max(1, args.steps // cfg.steps_per_batch)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(nb):
+            run.part.run_batch()
+        e1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    steps = nb * cfg.steps_per_batch
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    run.close()
+    del g
+    torch.cuda.empty_cache()
+    e2e = None
+    if not args.no_e2e:
+        t_final = float(w.get("t_final", 50.0))
+        dist.barrier()
+        t0 = time.perf_counter()
+        g = fs.gen_fixed_degree_device(n_total, w["k"], seed=GRAPH_SEED, row_lo=lo, row_hi=hi)
+        rec = run_renewal_distributed(g, m, cfg, SIM_SEED, t_final, plan, rank)
+        torch.cuda.synchronize()
+        wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+        wall = float(wall.item())
+        steps_run = int(np.ceil(rec.summary["step_count"] / cfg.steps_per_batch) * cfg.steps_per_batch)
+        d2h = 8 * (2 + m.num_compartments) * steps_run
+        e2e = {"value": n_total * steps_run / wall / 1e9, "unit": "G-NUPS", "h2d_bytes_per_step": 0.0,
+               "d2h_bytes_per_step": d2h / steps_run, "steps": steps_run, "wall_s": wall,
+               "what": f"run_renewal_distributed(t_final={t_final}) on {world} ranks: per-rank graph generation on the "
+                       f"device + NCCL setup + {steps_run} steps in CUDA-graph batches + per-batch log D2H + record",
+               "final_R": rec.summary["final_R"], "peak_I": rec.summary["peak_I"]}
+    if rank != 0:
+        return
+    pk = peaks()
+    ms_per_step = total_ms / steps
+    achieved = B_ALG[mixed] * n_total / (ms_per_step / 1e3) / 1e9
+    print(json.dumps({
+        "metric": "Giga-NUPS (node updates/s)", "value": n_total * steps / (total_ms / 1e3) / 1e9, "unit": "G-NUPS",
+        "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "i8/f16/bf16 storage, f32 rates, f64 hazard/q" if mixed else "f32 (f64 hazard/q)",
+        "data": "synthetic (GPU uniform-degree generator fs_gen_regular, graph seed 1, sim seed 7)",
+        "config": {"workload": w["desc"], "n": n_total, "edges": int(edges.item()), "strategy": "per-node",
+                   "gather": "count (1-bit mask)", "parallelism": f"node-partitioned x{world} (NCCL)",
+                   "l2": "inputs larger than L2; steps timed back to back as CUDA-graph batches",
+                   "steps_from": f"t=0 after {args.warmup} warm-up steps"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"] * world, "unit": "GB/s",
+                     "frac": achieved / (pk["hbm_gbs"] * world), "traffic": None,
+                     "bytes_per_update": B_ALG[mixed], "peak_source": pk["source"] + f" x {world} GPUs"},
+        "gpu_launches": steps,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": None,
+    }))
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: c2 on one GPU (the headline config), c5 (N=1e9 partitioned) on several")
     ap.add_argument("--cpu-steps", type=int, default=30)
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -223,6 +313,13 @@ def main() -> None:
     torch.cuda.set_device(local)
     import paper_2604_22092_b200 as fs
     from paper_2604_22092_b200 import renewal as R
+
+    if args.workload is None:
+        args.workload = "c2" if world == 1 else "c5"
+    if world > 1:
+        run_partitioned(args, WORKLOADS[args.workload], rank, world, local)
+        dist.destroy_process_group()
+        return
 
     w = WORKLOADS[args.workload]
     g, m = build_inputs(w)
@@ -286,7 +383,7 @@ def main() -> None:
     # ---------------- end to end through the public API ----------------
     e2e = None
     if not args.no_e2e:
-        t_final = 50.0
+        t_final = float(w.get("t_final", 50.0))
         torch.cuda.synchronize()
         if device_graph:
             del g, st, eng, plan, snap, snap0

@@ -635,6 +635,15 @@ def _pick_seed_nodes(n: int, seed: int, count: int, dev: torch.device) -> torch.
     if count == 0:
         return torch.empty(0, dtype=torch.int64, device=dev)
     u = uniform_array(derive_seed(seed, _SEED_PICK_SALT), 0, n=n)
+    if n > (1 << 22) and count < n // 4:
+        # exact prefilter: the `count` smallest of the candidates below a
+        # threshold are the `count` smallest overall whenever at least
+        # `count` values fall below it (expected 1.25 count + 8 sigma)
+        thr = min(1.0, (1.25 * count + 8.0 * (count ** 0.5) + 64.0) / n)
+        cand = torch.nonzero(u < thr).squeeze(1)
+        if cand.numel() >= count:
+            pick = torch.topk(u[cand], count, largest=False, sorted=False).indices
+            return torch.sort(cand[pick]).values
     idx = torch.topk(u, count, largest=False, sorted=False).indices
     return torch.sort(idx).values
 
