@@ -83,6 +83,11 @@ typedef struct fs_graph {
   int32_t d_max;                /* max in-degree                               */
   int32_t padded;               /* 1: row_offsets32 readable to N+9 entries and
                                    col_indices to E+4 (TMA bulk-copy slack)   */
+  /* outgoing CSR (the transpose; the incoming arrays themselves for the
+   * symmetric graphs of every reference generator), int64[N_global+1] /
+   * int32[E]: the push targets of the incremental count mode; NULL = none */
+  const int64_t* out_row_offsets;
+  const int32_t* out_col_indices;
 } fs_graph;
 
 typedef struct fs_compartment {
@@ -120,6 +125,9 @@ typedef struct fs_config {  /* renewal.py:75-99 `RenewalConfig` (+ rng, hazard_p
   int32_t rng;               /* enum fs_rng                                    */
   int32_t hazard_precision;  /* enum fs_hazard_precision                       */
   int32_t count_gather;      /* -1 auto, 0 force general f32 gather, 1 require count gather */
+  int32_t incremental;       /* count gather only: -1 auto, 0 off (gather the mask every step),
+                                1 require — keep per-node infectious-neighbour counts current
+                                by pushes along the outgoing CSR instead of re-gathering */
 } fs_config;
 
 /* device-resident engine scalars; mirrors the scalar fields of

@@ -51,6 +51,8 @@ class FsGraph(ctypes.Structure):
         ("uniform_weight", _c_f32),
         ("d_max", _c_i32),
         ("padded", _c_i32),
+        ("out_row_offsets", _vp),
+        ("out_col_indices", _vp),
     ]
 
 
@@ -98,6 +100,7 @@ class FsConfig(ctypes.Structure):
         ("rng", _c_i32),
         ("hazard_precision", _c_i32),
         ("count_gather", _c_i32),
+        ("incremental", _c_i32),
     ]
 
 

@@ -50,7 +50,8 @@ constexpr int kCntStride = FS_MAX_COMPARTMENTS;
 // tables on a 227 KB CTA
 constexpr size_t kMaxSmemMaskBytes = 188u * 1024u;  // + ~34 KB static (queues) <= 227 KB
 
-enum Gather { G_COUNT_SMEM = 0, G_COUNT_GLOBAL = 1, G_F32 = 2, G_PRE = 3 };
+enum Gather { G_COUNT_SMEM = 0, G_COUNT_GLOBAL = 1, G_F32 = 2, G_PRE = 3, G_INCR = 4 };
+constexpr uint32_t kDeltaBias = 0x8000u;  // pending delta d is stored as d + 0x8000 (|d| <= d_max < 2^15)
 enum Strat { S_THREAD = 0, S_WARP = 1 };
 
 // Device-side run scalars.  Two slots ping-pong (the host tracks which one
@@ -107,6 +108,14 @@ struct StepParams {
   const int64_t* num_active;
   const float* pre;              // G_PRE: gathered pressure
   int count_mode;
+  // incremental count mode (G_INCR): per-node infectious in-neighbour count,
+  // kept current by +-1 pushes along the outgoing edges of every node whose
+  // infectious status changes
+  uint16_t* cnt;                 // [N] counts as of the current step's start, minus pending deltas
+  uint32_t* pend[2];             // [ceil(N/2)] words of biased u16 pending deltas, double-buffered by step parity
+  const int64_t* out_ro;         // outgoing CSR (the incoming one for symmetric graphs)
+  const int32_t* out_col;
+  int stream_evict_first;        // CSR stream larger than L2: evict-first hint on column loads
   unsigned long long* dbg;       // optional per-CTA %globaltimer stamps [grid][4]
   // model / config
   fs_model model;
@@ -139,11 +148,36 @@ struct MergeParams {
 };
 
 // ---------------------------------------------------------------------------
+// L2 residency hints.  The infectious mask is read randomly ~d times per
+// node per step and must stay in L2; the CSR column stream is read once per
+// step and, when the working set exceeds L2, should not evict the mask.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_stream(int evict_first) {
+  uint64_t a, b;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(a));
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(b));
+  return evict_first ? a : b;
+}
+__device__ __forceinline__ uint32_t ldg_hint(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int32_t ldg_hint(const int32_t* p, uint64_t pol) {
+  return (int32_t)ldg_hint(reinterpret_cast<const uint32_t*>(p), pol);
+}
+
+// ---------------------------------------------------------------------------
 // gather primitives
 // ---------------------------------------------------------------------------
 template <bool SMEM>
 __device__ __forceinline__ int mask_bit(const uint32_t* __restrict__ m, int32_t c) {
-  uint32_t w = SMEM ? m[c >> 5] : __ldg(m + (c >> 5));
+  uint32_t w = SMEM ? m[c >> 5] : ldg_hint(m + (c >> 5), l2_policy_last());
   return (int)((w >> (c & 31)) & 1u);
 }
 
@@ -203,6 +237,12 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+               : "memory");
 }
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -295,7 +335,7 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 
 template <bool SMEM_MASK, bool COL_SMEM = false>
 __device__ __forceinline__ int count_tile(const int32_t* __restrict__ col, const uint32_t* m, int64_t lo, int64_t hi,
-                                          bool need, unsigned need_mask, int lane) {
+                                          bool need, unsigned need_mask, int lane, uint64_t col_pol) {
   const int j0 = __ffs(need_mask) - 1, j1 = 31 - __clz(need_mask);
   const int64_t E0 = __shfl_sync(0xffffffffu, lo, j0), E1 = __shfl_sync(0xffffffffu, hi, j1);
   const int32_t* __restrict__ cp = col + E0;
@@ -312,11 +352,11 @@ __device__ __forceinline__ int count_tile(const int32_t* __restrict__ col, const
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int e = gb + 32 * u + lane;
-        c[u] = e < wl ? (COL_SMEM ? lds_u32(cp_s + 4u * (uint32_t)(w0 + e)) : (uint32_t)__ldg(cp + w0 + e))
+        c[u] = e < wl ? (COL_SMEM ? lds_u32(cp_s + 4u * (uint32_t)(w0 + e)) : (uint32_t)ldg_hint(cp + w0 + e, col_pol))
                       : 0u;  // bits past the range are never counted
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) word[u] = SMEM_MASK ? m[c[u] >> 5] : __ldg(m + (c[u] >> 5));
+      for (int u = 0; u < 8; ++u) word[u] = SMEM_MASK ? m[c[u] >> 5] : ldg_hint(m + (c[u] >> 5), l2_policy_last());
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int g = gb + 32 * u;
@@ -526,8 +566,21 @@ __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst
       reinterpret_cast<ST*>(p.states)[n] = (ST)ns;
       atomicAdd(&sh.cnt[ns], 1);
       atomicAdd(&sh.cnt[s], -1);
-      if (!k.write_inf && ((ns == k.infectious) != (s == k.infectious)))
+      if (!k.write_inf && ((ns == k.infectious) != (s == k.infectious))) {
         atomicXor(mask_nxt + p.tile_base + (n >> 5), 1u << (n & 31));
+        if (p.cnt) {  // incremental counts: +-1 on every out-neighbour's pending delta
+          uint32_t* dn = p.pend[(k.step & 1) ^ 1];
+          const int64_t gn = n + p.node_base;
+          const int64_t e0 = __ldg(p.out_ro + gn), e1 = __ldg(p.out_ro + gn + 1);
+          const bool up = ns == k.infectious;
+          for (int64_t e = e0; e < e1; ++e) {
+            const int32_t j = __ldg(p.out_col + e);
+            const uint32_t one = 1u << (16 * (j & 1));
+            if (up) atomicAdd(dn + (j >> 1), one);
+            else atomicSub(dn + (j >> 1), one);
+          }
+        }
+      }
     } else {
       nage = __fadd_rn(age, k.tau_f);  // queued nodes are never terminal
     }
@@ -655,7 +708,14 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
     in.s = valid ? (int)reinterpret_cast<const ST*>(p.states)[n] : -1;
     in.age = valid ? to_f32<AT>(reinterpret_cast<const AT*>(p.ages)[n]) : 0.0f;
     in.lo = in.hi = 0;
-    if (GATHER != G_PRE) load_slice(p.ro, p.ro32, n, valid, lane, in.lo, in.hi);
+    if (GATHER == G_INCR) {  // lo <- count, hi <- pending delta (biased)
+      if (valid) {
+        in.lo = p.cnt[n];
+        in.hi = reinterpret_cast<const uint16_t*>(p.pend[cur])[n];
+      }
+    } else if (GATHER != G_PRE) {
+      load_slice(p.ro, p.ro32, n, valid, lane, in.lo, in.hi);
+    }
   };
   auto tile_of = [&](int64_t t) -> int64_t { return p.active_tiles ? (int64_t)p.active_tiles[t] : t; };
 
@@ -678,7 +738,17 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
     const bool need = valid && (in.s == k.edge_from || MAT);
 
     float pressure = 0.0f;
-    if (GATHER == G_PRE) {
+    if (GATHER == G_INCR) {
+      // fold the pushes of the previous step into the count (and clear them)
+      uint32_t c = (uint32_t)in.lo;
+      const uint32_t dl = (uint32_t)in.hi;
+      if (valid && dl != kDeltaBias) {
+        c = c + dl - kDeltaBias;
+        p.cnt[n] = (uint16_t)c;
+        reinterpret_cast<uint16_t*>(p.pend[cur])[n] = (uint16_t)kDeltaBias;
+      }
+      if (need) pressure = p.ptab_mul ? __fmul_rn((float)c, p.ptab_c) : __ldg(p.ptab + c);
+    } else if (GATHER == G_PRE) {
       if (need) pressure = __ldg(p.pre + n);
     } else {
       if (GATHER == G_COUNT_SMEM && !mask_ready) {
@@ -690,7 +760,8 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
         if (GATHER == G_F32) {
           if (need) pressure = fold_thread<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo, in.hi);
         } else if (todo) {
-          const int kk = count_tile<GATHER == G_COUNT_SMEM>(p.col, gmask, in.lo, in.hi, need, todo, lane);
+          const int kk = count_tile<GATHER == G_COUNT_SMEM>(p.col, gmask, in.lo, in.hi, need, todo, lane,
+                                                            l2_policy_stream(p.stream_evict_first));
           if (need) pressure = p.ptab_mul ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
         }
       } else {  // warp per node (LANE strategy)
@@ -722,15 +793,21 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
 // thread-per-node count over a slice staged in shared memory: lane-private
 // loop, two edges per iteration; an odd tail reads the sentinel column
 // `zero_col`, whose mask word is guaranteed zero
-template <bool SMEM_MASK>
+// U columns per round, all of a round's mask loads in flight together: the
+// mask lookups (shared memory at N <~ 1.5e6, L2 beyond) are the dependent
+// latency of the gather, so a degree-d slice costs ceil(d/U) round trips.
+template <bool SMEM_MASK, int U>
 __device__ __forceinline__ int count_slice_smem(uint32_t col_addr, int len, const uint32_t* m, uint32_t zero_col) {
   int cnt = 0;
-  for (int i = 0; i < len; i += 2) {
-    const uint32_t c0 = lds_u32(col_addr + 4u * (uint32_t)i);
-    const uint32_t c1 = (i + 1 < len) ? lds_u32(col_addr + 4u * (uint32_t)i + 4u) : zero_col;
-    const uint32_t w0 = SMEM_MASK ? m[c0 >> 5] : __ldg(m + (c0 >> 5));
-    const uint32_t w1 = SMEM_MASK ? m[c1 >> 5] : __ldg(m + (c1 >> 5));
-    cnt += (int)(__funnelshift_r(w0, w0, c0) & 1u) + (int)(__funnelshift_r(w1, w1, c1) & 1u);
+  const uint64_t pol = SMEM_MASK ? 0ull : l2_policy_last();
+  for (int i = 0; i < len; i += U) {
+    uint32_t c[U], w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = (i + u < len) ? lds_u32(col_addr + 4u * (uint32_t)(i + u)) : zero_col;
+#pragma unroll
+    for (int u = 0; u < U; ++u) w[u] = SMEM_MASK ? m[c[u] >> 5] : ldg_hint(m + (c[u] >> 5), pol);
+#pragma unroll
+    for (int u = 0; u < U; ++u) cnt += (int)(__funnelshift_r(w[u], w[u], c[u]) & 1u);
   }
   return cnt;
 }
@@ -744,6 +821,15 @@ __device__ __forceinline__ int count_slice_smem(uint32_t col_addr, int len, cons
 // stream from HBM with no registers held.  The gather then reads columns
 // and the staged infectious mask from shared memory only.
 // ---------------------------------------------------------------------------
+#ifndef FS_GATHER_U_SMEM
+#define FS_GATHER_U_SMEM 2
+#endif
+#ifndef FS_GATHER_U_GLOBAL
+#define FS_GATHER_U_GLOBAL 2
+#endif
+constexpr int kGatherU_Smem = FS_GATHER_U_SMEM;
+constexpr int kGatherU_Global = FS_GATHER_U_GLOBAL;
+
 struct TmaLayout {
   int slots;        // buffers per warp
   int slot_bytes;   // bytes per buffer
@@ -789,6 +875,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
   const int gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
   const int per = ntiles / nw, rem = ntiles % nw;  // balanced split
   const int t0 = gw * per + min(gw, rem), t1 = t0 + per + (gw < rem ? 1 : 0);
+  const uint64_t col_pol = l2_policy_stream(p.stream_evict_first);
   int bnd_base = t0;
   int32_t bnd = (t0 + lane <= t1) ? __ldg(ro + min((t0 + lane) * 32, N)) : 0;  // first edge of tile t0+lane
   // lane 0 streams tile t's columns [ro[32t] & ~3, (ro[32t+32] + 3) & ~3)
@@ -804,7 +891,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
       const uint32_t bytes = 4u * (uint32_t)(c1 - c0);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
       mbar_arrive_expect_tx(&t_bar[warp][sl], bytes);
-      if (bytes) tma_bulk_g2s(wbuf + (size_t)sl * L.slot_bytes, p.col + c0, bytes, &t_bar[warp][sl]);
+      if (bytes) tma_bulk_g2s_hint(wbuf + (size_t)sl * L.slot_bytes, p.col + c0, bytes, &t_bar[warp][sl], col_pol);
     }
   };
   // per-node inputs, coalesced loads two tiles ahead (arrays are padded to
@@ -859,7 +946,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
     float pressure = 0.0f;
     const int32_t cbase = __shfl_sync(kFull, in.lo, 0) & ~3;  // the slot holds columns from cbase
     if (need) {
-      const int kk = count_slice_smem<SMEM_MASK>(wbuf_s + (uint32_t)(sl * L.slot_bytes) + 4u * (uint32_t)(in.lo - cbase),
+      const int kk = count_slice_smem<SMEM_MASK, SMEM_MASK ? kGatherU_Smem : kGatherU_Global>(wbuf_s + (uint32_t)(sl * L.slot_bytes) + 4u * (uint32_t)(in.lo - cbase),
                                                  in.hi - in.lo, gmask, zero_col);
       pressure = PTAB_MUL ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
     }
@@ -939,6 +1026,26 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_gather_merge
         else v = __ldg(q.ptab + count_warp<MODE == 1>(q.col, gmask, lj, hj, lane));
         if (lane == j) q.out[n] = v;
       }
+    }
+  }
+}
+
+// incremental count mode: counts from scratch (engine start, host edits):
+// cnt[n] = number of infectious in-neighbours in mask m; both pending-delta
+// buffers cleared to the bias
+__global__ void k_init_counts(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
+                              const uint32_t* __restrict__ m, int64_t n, uint16_t* __restrict__ cnt,
+                              uint32_t* __restrict__ d0, uint32_t* __restrict__ d1) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int c = 0;
+    for (int64_t e = __ldg(ro + i), e1 = __ldg(ro + i + 1); e < e1; ++e) {
+      const int32_t j = __ldg(col + e);
+      c += (int)((__ldg(m + (j >> 5)) >> (j & 31)) & 1u);
+    }
+    cnt[i] = (uint16_t)c;
+    if ((i & 1) == 0) {
+      d0[i >> 1] = kDeltaBias | (kDeltaBias << 16);
+      d1[i >> 1] = kDeltaBias | (kDeltaBias << 16);
     }
   }
 }
@@ -1101,6 +1208,9 @@ StepFn pick_step2(int gather, int strat, int& block) {
       block = 512;
       return strat == S_WARP ? k_step<ST, AT, IT, G_COUNT_GLOBAL, S_WARP, MAT, 512>
                              : k_step<ST, AT, IT, G_COUNT_GLOBAL, S_THREAD, MAT, 512>;
+    case G_INCR:
+      block = 512;
+      return k_step<ST, AT, IT, G_INCR, S_THREAD, MAT, 512>;
     case G_F32:
       block = 512;
       return strat == S_WARP ? k_step<ST, AT, IT, G_F32, S_WARP, MAT, 512>
@@ -1223,6 +1333,11 @@ struct fs_engine {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t batch_exec[2][2][3] = {};  // [materialise][scalar slot][step % 3 when exchanging]
   bool compaction_ready = false;
+  int stream_evict_first = 0;
+  // incremental count mode
+  bool incr = false;
+  uint16_t* cnt = nullptr;
+  uint32_t* delta[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -1279,6 +1394,12 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.num_active = e->num_active;
   p.pre = use_pre ? e->pre : nullptr;
   p.count_mode = e->count_mode;
+  p.stream_evict_first = e->stream_evict_first;
+  p.cnt = e->incr ? e->cnt : nullptr;
+  p.pend[0] = e->delta[0];
+  p.pend[1] = e->delta[1];
+  p.out_ro = e->g.out_row_offsets;
+  p.out_col = e->g.out_col_indices;
   p.dbg = e->dbg;
   p.model = e->m;
   p.eps = e->c.epsilon;
@@ -1392,6 +1513,17 @@ int launch_begin_batch(fs_engine* e, cudaStream_t st) {
   return 0;
 }
 
+// incremental counts from the current mask (buffer of step parity `step`)
+int recount(fs_engine* e, int64_t step, cudaStream_t st) {
+  if (!e->incr) return 0;
+  const int64_t n = e->g.num_nodes;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
+  k_init_counts<<<std::max(1, blocks), 256, 0, st>>>(e->g.row_offsets, e->g.col_indices, e->b.imask[step & 1], n,
+                                                     e->cnt, e->delta[0], e->delta[1]);
+  FS_CUDA(cudaGetLastError());
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1461,9 +1593,16 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     e->inf_val = bf;
   }
   e->mask_smem = e->count_mode && (size_t)e->ntiles_mask * 4 <= kMaxSmemMaskBytes;
-  e->merge = c->strategy == FS_MERGE && g->num_edges > 0;
+  // incremental counts: count gather + an outgoing CSR to push along, single
+  // partition, degrees below the 2^15 delta headroom
+  const bool can_incr = e->count_mode && !part && g->out_row_offsets && g->out_col_indices && g->d_max < 32768 &&
+                        g->num_edges > 0;
+  if (c->incremental == 1 && !can_incr) { delete e; return set_error(FS_EINVAL, "incremental counts need the count gather, an outgoing CSR, d_max < 32768 and one partition"); }
+  e->incr = can_incr && c->incremental != 0;
+  e->merge = c->strategy == FS_MERGE && g->num_edges > 0 && !e->incr;
   e->strat = c->strategy == FS_LANE ? S_WARP : S_THREAD;
-  if (e->merge) e->gather = G_PRE;
+  if (e->incr) e->gather = G_INCR;
+  else if (e->merge) e->gather = G_PRE;
   else if (e->count_mode) e->gather = e->mask_smem ? G_COUNT_SMEM : G_COUNT_GLOBAL;
   else e->gather = G_F32;
 
@@ -1494,10 +1633,19 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     FS_CUDA(cudaMemcpy(&e->ptab_mul, e->bad_flag, sizeof(int), cudaMemcpyDeviceToHost));
     e->ptab_c = cval;
   }
+  {
+    // column stream + per-node arrays larger than half the L2: stream them
+    // with evict-first so the randomly read mask keeps its lines
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+    const double ws = 4.0 * (double)g->num_edges + 16.0 * (double)n;
+    e->stream_evict_first = (l2 > 0 && ws > 0.5 * (double)l2) ? 1 : 0;
+    if (getenv("FS_NO_EVICT_HINT")) e->stream_evict_first = 0;
+  }
   e->step_grid_general = e->step_grid;
   e->step_smem_general = e->step_smem;
   // streaming fast path: count gather, PER_NODE, padded buffers, int32 offsets
-  if (e->count_mode && c->strategy == FS_PER_NODE && !e->merge && g->row_offsets32 && g->padded && buf->padded &&
+  if (e->count_mode && !e->incr && c->strategy == FS_PER_NODE && !e->merge && g->row_offsets32 && g->padded && buf->padded &&
       g->num_edges > 0) {
     unsigned long long* d_span = nullptr;
     TRY(dalloc(&d_span, 1));
@@ -1579,6 +1727,12 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     k_chunk_first<<<(int)std::min<int64_t>((e->nchunks + 256) / 256, 4096), 256>>>(g->row_offsets, n, g->num_edges,
                                                                                   c->edges_per_block, e->nchunks, e->chunk_first);
   }
+  if (e->incr) {
+    TRY(dalloc(&e->cnt, (size_t)e->ntiles * 32));
+    TRY(dalloc(&e->delta[0], (size_t)e->ntiles * 16));
+    TRY(dalloc(&e->delta[1], (size_t)e->ntiles * 16));
+    TRY(recount(e, scal->step, nullptr));
+  }
   if (getenv("FS_NO_PDL")) e->pdl = false;
   if (getenv("FS_DEBUG_TIMES")) {
     TRY(dalloc(&e->dbg, (size_t)std::max(e->step_grid, e->step_grid_general) * 4 * 16));
@@ -1612,7 +1766,8 @@ void fs_engine_destroy(fs_engine* e) {
       for (auto& x : b) if (x) cudaGraphExecDestroy(x);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   void* ptrs[] = {e->dstate, e->acc, e->log_clock, e->log_tau, e->log_counts, e->ptab,
-                  e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag};
+                  e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag,
+                  e->cnt, e->delta[0], e->delta[1]};
   for (void* q : ptrs) if (q) cudaFree(q);
   delete e;
 }
@@ -1753,6 +1908,10 @@ int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream) {
   }
   FS_CUDA(cudaMemcpyAsync(e->dstate + e->s_cur, &d, sizeof(DevState), cudaMemcpyHostToDevice, st));
   FS_CUDA(cudaMemsetAsync(e->acc, 0, 3 * sizeof(StepAcc), st));
+  if ((in->step ^ cur.s.step) & 1) {  // pending deltas are indexed by step parity: rebuild
+    rc = recount(e, in->step, st);
+    if (rc) return rc;
+  }
   FS_CUDA(cudaStreamSynchronize(st));
   e->h_step = in->step;
   return 0;
@@ -1776,6 +1935,13 @@ int fs_engine_load_infectivity(fs_engine* e, const void* inf, void* stream) {
     FS_CUDA(cudaMemcpyAsync(&bad, e->bad_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     FS_CUDA(cudaStreamSynchronize(st));
     if (bad) return set_error(FS_EREPR, "infectivity values are not in {0, beta}: the count gather cannot represent them");
+    {
+      DevState d;
+      StepAcc a[3];
+      int rc = read_state(e, &d, a, st);
+      if (!rc) rc = recount(e, d.s.step, st);
+      if (rc) return rc;
+    }
     return 0;
   }
   const size_t bytes = (size_t)n * (e->mixed ? 2 : 4);

@@ -102,7 +102,7 @@ def _config(cfg: RenewalConfig, strategy) -> _lib.FsConfig:
         strategy=_STRATEGY_CODE[strategy], compaction=int(cfg.compaction), mixed_precision=int(cfg.mixed_precision),
         lanes_per_node=cfg.lanes_per_node, edges_per_block=cfg.edges_per_block, hazard_chunk=cfg.hazard_chunk,
         chunk_skip=int(cfg.chunk_skip), carry_tau=int(cfg.carry_tau), rng=RNG_KINDS[cfg.rng],
-        hazard_precision=_PRECISION[cfg.hazard_precision], count_gather=1)
+        hazard_precision=_PRECISION[cfg.hazard_precision], count_gather=1, incremental=0)
 
 
 def _initial_mask(plan: PartitionPlan, seed_ids: torch.Tensor, infectious: bool, dev) -> torch.Tensor:

@@ -55,7 +55,8 @@ _SEED_PICK_SALT = 0x5EEDC0DE  # renewal.py:55
 _STRATEGY_CODE = {Strategy.PER_NODE: _lib.PER_NODE, Strategy.LANE_CHUNKED: _lib.LANE,
                   Strategy.EDGE_MERGE: _lib.MERGE}
 _PRECISION = {"f64": _lib.HAZ_F64, "f32": _lib.HAZ_F32}
-_GATHER = {"auto": -1, "f32": 0, "count": 1}
+_GATHER = {"auto": -1, "f32": 0, "count": 1, "incremental": 1}
+_INCREMENTAL = {"auto": -1, "f32": 0, "count": 0, "incremental": 1}
 
 
 @dataclass
@@ -65,7 +66,11 @@ class RenewalConfig:
 
     rng               "splitmix" (reference mixer, bit-exact parity) | "philox"
     hazard_precision  "f64" (the reference's float64 hazard) | "f32"
-    gather            "auto" (1-bit count gather when exact) | "f32" | "count"
+    gather            "auto" (exact count encodings when transmission is
+                      constant and weights uniform: incremental counts when an
+                      outgoing CSR is known, else the 1-bit mask gather) |
+                      "f32" (the literal CSR-order fold) | "count" (mask gather
+                      every step) | "incremental" (require incremental counts)
     """
 
     epsilon: float = 0.03
@@ -96,7 +101,7 @@ class RenewalConfig:
         if self.hazard_precision not in _PRECISION:
             raise ValueError("hazard_precision must be 'f64' or 'f32'")
         if self.gather not in _GATHER:
-            raise ValueError("gather must be 'auto', 'f32' or 'count'")
+            raise ValueError("gather must be 'auto', 'f32', 'count' or 'incremental'")
 
 
 @dataclass
@@ -168,6 +173,7 @@ class _DeviceGraph:
         self.weights = None if self.uniform else _device.to_device(w, dev)
         self.weights_bf16 = mixed
         self.d_max = int(np.diff(ro).max()) if self.num_nodes else 0
+        self.symmetric = _is_symmetric(self)
 
     def view(self) -> _lib.FsGraph:
         return _lib.FsGraph(
@@ -182,6 +188,9 @@ class _DeviceGraph:
             uniform_weight=self.uniform_weight,
             d_max=self.d_max,
             padded=1,
+            # the outgoing CSR of a symmetric (undirected) graph is the incoming one
+            out_row_offsets=_lib.ptr(self.row_offsets) if self.symmetric else None,
+            out_col_indices=_lib.ptr(self.col_indices) if self.symmetric else None,
         )
 
 
@@ -205,7 +214,23 @@ class _DeviceGraph:
         self.weights = None
         self.weights_bf16 = False
         self.d_max = int(g.d_max)
+        self.symmetric = not g.partitioned  # fs_gen_regular graphs are undirected by construction
         return self
+
+
+def _is_symmetric(dg) -> bool:
+    """Is the incoming CSR its own transpose (an undirected graph, as every
+    reference generator makes, R/graph.py:221-231)?  Decided on the device:
+    the sorted (dst, src) keys equal the sorted (src, dst) keys."""
+    n, e = dg.num_nodes, dg.num_edges
+    if e == 0:
+        return True
+    deg = dg.row_offsets[1:] - dg.row_offsets[:-1]
+    dst = torch.repeat_interleave(torch.arange(n, device=deg.device, dtype=torch.int64), deg)
+    src = dg.col_indices.to(torch.int64)
+    fwd = dst * n + src  # already sorted: rows by dst, slices by src
+    rev = torch.sort(src * n + dst).values
+    return bool(torch.equal(fwd, rev))
 
 
 def device_graph(g, mixed: bool = False) -> _DeviceGraph:
@@ -248,8 +273,8 @@ def _build_plan(g, m, cfg: RenewalConfig, mixed: bool) -> _EnginePlan:
     strategy = resolve_strategy(g, cfg.strategy)
     dg = device_graph(g, mixed)
     count_mode = m.transmission.kind == "constant" and dg.uniform and cfg.gather != "f32"
-    if cfg.gather == "count" and not count_mode:
-        raise InvalidConfigError("gather='count' needs constant transmission and uniform weights")
+    if cfg.gather in ("count", "incremental") and not count_mode:
+        raise InvalidConfigError(f"gather={cfg.gather!r} needs constant transmission and uniform weights")
     c = _lib.FsConfig(
         epsilon=cfg.epsilon, tau_max=cfg.tau_max, delta=cfg.delta,
         steps_per_batch=cfg.steps_per_batch, strategy=_STRATEGY_CODE[strategy],
@@ -258,6 +283,7 @@ def _build_plan(g, m, cfg: RenewalConfig, mixed: bool) -> _EnginePlan:
         hazard_chunk=cfg.hazard_chunk, chunk_skip=int(cfg.chunk_skip), carry_tau=int(cfg.carry_tau),
         rng=RNG_KINDS[cfg.rng], hazard_precision=_PRECISION[cfg.hazard_precision],
         count_gather=1 if count_mode else 0,
+        incremental=_INCREMENTAL[cfg.gather] if count_mode else 0,
     )
     return _EnginePlan(strategy=strategy, graph=dg, model=model_descriptor(m), config=c,
                        succ=m.successor_array(), terminal=m.terminal_mask(), count_mode=count_mode,

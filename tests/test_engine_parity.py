@@ -146,6 +146,8 @@ def test_trajectory_parity_graph_replay(name):
 @pytest.mark.parametrize("overrides", [
     {"strategy": Strategy.PER_NODE}, {"strategy": Strategy.LANE_CHUNKED}, {"strategy": Strategy.EDGE_MERGE},
     {"strategy": Strategy.EDGE_MERGE, "edges_per_block": 64}, {"compaction": True}, {"gather": "f32"},
+    {"gather": "count"}, {"gather": "count", "strategy": Strategy.EDGE_MERGE}, {"gather": "incremental"},
+    {"gather": "incremental", "compaction": True},
     {"chunk_skip": False, "hazard_chunk": 64},
 ])
 @pytest.mark.parametrize("name", ["c1", "ba_merge"])
@@ -154,9 +156,10 @@ def test_variants_are_result_neutral(name, overrides):
     assert_matches(st, log, cps, ref)
 
 
+@pytest.mark.parametrize("gather", ["incremental", "count"])
 @pytest.mark.parametrize("name", ["c1", "ba_merge"])
-def test_compaction_graph_replay_neutral(name):
-    st, log, _, ref = run_engine_case(name, overrides={"compaction": True}, batches_via_graph=True)
+def test_compaction_graph_replay_neutral(name, gather):
+    st, log, _, ref = run_engine_case(name, overrides={"compaction": True, "gather": gather}, batches_via_graph=True)
     assert np.array_equal(log["counts"], ref["counts"])
     assert np.array_equal(st.states.astype(np.int32), ref["states"])
     assert np.array_equal(st.ages.astype(np.float32), ref["ages"])

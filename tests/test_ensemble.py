@@ -1,0 +1,61 @@
+"""Ensemble statistics (north_star's second correctness form).
+
+Golden values: tests/golden/make_ensemble_golden.py ran the reference's own
+ensembles of its acceptance suite (T/test_acceptance.py:34-79: ER N=1000,
+d=8, seed 20250809, 100 runs, 10 E seeds, t_final=50) — the CPU tau-leap
+engine and the exact next-reaction oracle (R/exact.py:187-310).
+
+* The GPU engine, fed the same per-trial seeds derive_seed(seed, trial)
+  (R/analysis.py:61-74), reproduces every tau-leap trajectory's summary
+  exactly (peak I, its time, final R, step count).
+* Its ensemble means agree with the exact oracle's within Monte Carlo error
+  (3 standard errors of the difference; tau-leap bias at eps=0.03 is far
+  below that, pkg/test_output.txt:11,13).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+import paper_2604_22092_b200 as fs
+from tests._cases import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with np.load(GOLDEN / "ensemble.npz") as z:
+        d = {k: z[k] for k in z.files}
+    return d, json.loads((GOLDEN / "ensemble.json").read_text())
+
+
+@pytest.fixture(scope="module")
+def ours(golden):
+    _, meta = golden
+    _, n, d, seed = meta["graph"]
+    g = fs.gen_erdos_renyi(n, d, seed=seed)
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    cfg = fs.RenewalConfig()
+    recs = [fs.run_renewal(g, m, cfg, fs.derive_seed(meta["seed"], t), meta["t_final"], seed_count=meta["seed_count"])
+            for t in range(meta["runs"])]
+    out = {k: np.array([r.summary[k] for r in recs], dtype=np.float64)
+           for k in ("peak_I", "peak_I_time", "final_R", "step_count")}
+    out["mean"] = np.mean([r.fractions for r in recs], axis=0)
+    return out
+
+
+def test_tau_leap_ensemble_is_the_reference_trajectory_by_trajectory(golden, ours):
+    ref, _ = golden
+    for k in ("peak_I", "peak_I_time", "final_R", "step_count"):
+        assert np.array_equal(ours[k], ref[f"renewal__{k}"]), k
+    assert np.array_equal(ours["mean"], ref["renewal__mean"])
+
+
+@pytest.mark.parametrize("stat", ["peak_I", "final_R", "peak_I_time"])
+def test_ensemble_agrees_with_exact_oracle_within_mc_error(golden, ours, stat):
+    ref, _ = golden
+    a, b = ours[stat], ref[f"exact__{stat}"]
+    se = np.sqrt(a.var(ddof=1) / a.size + b.var(ddof=1) / b.size)
+    assert abs(a.mean() - b.mean()) <= 3.0 * se + 1e-3, (stat, a.mean(), b.mean(), se)
