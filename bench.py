@@ -334,6 +334,7 @@ def main() -> None:
     eng = st._bind(plan, SIM_SEED, materialize=False)
     kernels_per_step = 2 if plan.strategy == fs.Strategy.EDGE_MERGE else 1
     strategy_name, count_mode = plan.strategy.value, plan.count_mode
+    incremental = count_mode and plan.config.incremental != 0 and plan.graph.symmetric
     snap0 = eng.snapshot()
     eng.run_batch(False)  # captures the batch CUDA graph outside any timed region
     eng.restore(snap0)
@@ -425,7 +426,8 @@ def main() -> None:
         "data": ("synthetic (GPU uniform-degree generator fs_gen_regular, graph seed 1, sim seed 7)" if device_graph
                  else "synthetic (reference generators, graph seed 1, sim seed 7)"),
         "config": {"workload": w["desc"], "n": n, "edges": g.num_edges, "strategy": strategy_name,
-                   "gather": "count (1-bit mask)" if count_mode else "f32", "precision": "mixed (states i8, ages f16, infectivity bf16)" if mixed else "fp32 storage",
+                   "gather": ("incremental counts (pushes along the outgoing CSR)" if incremental else
+                              "count (1-bit mask)" if count_mode else "f32"), "precision": "mixed (states i8, ages f16, infectivity bf16)" if mixed else "fp32 storage",
                    "l2": "flushed before every timed step (512 MiB write + 512 MiB read of another buffer)", "parallelism": f"replicas x{world}",
                    "steps_from": f"t=0 after {args.warmup} warm-up steps"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",

@@ -152,7 +152,8 @@ typedef struct fs_state_buffers {
                             multiple and 16-byte aligned (TMA bulk staging) */
   float* pressure;       /* f32[N], written on materialising steps            */
   float* rates;          /* f32[N], written on materialising steps            */
-  int32_t padded;        /* 1: states/ages readable to a multiple of 32 nodes */
+  int32_t padded;        /* 1: states/ages readable to a multiple of 32 nodes,
+                            2: to a multiple of 128 nodes (streaming kernel) */
 } fs_state_buffers;
 
 /* node partition of a multi-GPU run: this

@@ -790,6 +790,76 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
 
+// ---------------------------------------------------------------------------
+// Step kernel of the incremental count mode (G_INCR, no compaction list).
+// No gather: a node's infectious in-neighbour count is read like any other
+// per-node field, so phase A is a coalesced stream over (state, age,
+// count, pending delta) — 32-node tiles, lane per node, two tiles of loads
+// in flight, 32-bit indexing, the step constants computed once per CTA.
+// Phase B (the deferral queue: hazards, uniforms, Bernoulli, pushes) is the
+// same as k_step's.
+// ---------------------------------------------------------------------------
+template <typename ST, typename AT, bool MAT, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
+  constexpr int WARPS = BLOCK / 32;
+  __shared__ StepShared<WARPS> sh;
+  __shared__ StepConst s_k;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_launch_dependents();
+  load_tables<WARPS>(p, sh, tid);  // static model tables: before the dependency wait
+  pdl_wait();
+  if (tid == 0) {
+    s_k = step_const(p, true);
+    if (blockIdx.x == 0) commit_step_start(p, s_k);
+  }
+  __syncthreads();
+  const StepConst k = s_k;
+  const int cur = (int)(k.step & 1);
+  uint32_t* mask_nxt = p.mask[cur ^ 1];
+  const ST* __restrict__ states = reinterpret_cast<const ST*>(p.states);
+  const AT* __restrict__ ages = reinterpret_cast<const AT*>(p.ages);
+  uint16_t* __restrict__ cnt = p.cnt;
+  uint16_t* __restrict__ pend = reinterpret_cast<uint16_t*>(p.pend[cur]);
+  const uint32_t N = (uint32_t)p.n, ntiles = (uint32_t)p.ntiles;
+  const uint32_t stride = gridDim.x * WARPS;
+  struct In { int s; float age; uint32_t c, d; };
+  // arrays are padded to whole 128-node units: every lane loads unconditionally
+  auto load = [&](uint32_t t, In& in) {
+    const uint32_t n = t * 32u + (uint32_t)lane;
+    in.s = (int)states[n];
+    in.age = to_f32<AT>(ages[n]);
+    in.c = cnt[n];
+    in.d = pend[n];
+  };
+  float lmax = 0.0f;
+  int qn = 0;
+  uint32_t t = blockIdx.x * WARPS + warp;
+  In in0{}, in1{};
+  if (t < ntiles) load(t, in0);
+  if (t + stride < ntiles) load(t + stride, in1);
+  for (; t < ntiles; t += stride) {
+    const In in = in0;
+    in0 = in1;
+    if (t + 2 * stride < ntiles) load(t + 2 * stride, in1);
+    const uint32_t n = t * 32u + (uint32_t)lane;
+    const bool valid = n < N;
+    uint32_t c = in.c;
+    if (valid && in.d != kDeltaBias) {  // fold the previous step's pushes, clear them
+      c = c + in.d - kDeltaBias;
+      cnt[n] = (uint16_t)c;
+      pend[n] = (uint16_t)kDeltaBias;
+    }
+    const int s = valid ? in.s : -1;
+    const float pressure = (valid && (s == k.edge_from || MAT))
+                               ? (p.ptab_mul ? __fmul_rn((float)c, p.ptab_c) : __ldg(p.ptab + c))
+                               : 0.0f;
+    tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, (int64_t)t, (int64_t)n, valid, s, in.age, pressure,
+                                            qn, lmax, mask_nxt, nullptr);
+  }
+  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
+  finish_step<WARPS>(p, k, sh, warp, lane, lmax);
+}
+
 // thread-per-node count over a slice staged in shared memory: lane-private
 // loop, two edges per iteration; an odd tail reads the sentinel column
 // `zero_col`, whose mask word is guaranteed zero
@@ -1229,6 +1299,11 @@ StepFn pick_step(bool mixed, int gather, int strat, bool mat, int& block) {
              : pick_step2<int32_t, float, float, false>(gather, strat, block);
 }
 
+StepFn pick_stream(bool mixed, bool mat) {
+  if (mixed) return mat ? k_step_incr<int8_t, __half, true, 512> : k_step_incr<int8_t, __half, false, 512>;
+  return mat ? k_step_incr<int32_t, float, true, 512> : k_step_incr<int32_t, float, false, 512>;
+}
+
 using TmaFn = void (*)(const StepParams, const TmaLayout);
 
 template <typename ST, typename AT, bool SM, bool MAT, int B>
@@ -1336,6 +1411,9 @@ struct fs_engine {
   int stream_evict_first = 0;
   // incremental count mode
   bool incr = false;
+  bool stream = false;         // k_step_stream fast path of the incremental mode
+  StepFn stream_fn[2] = {nullptr, nullptr};
+  int stream_grid = 0;
   uint16_t* cnt = nullptr;
   uint32_t* delta[2] = {nullptr, nullptr};
 };
@@ -1445,7 +1523,19 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
       e->merge_fn<<<e->merge_grid, e->merge_block, e->merge_smem, st>>>(q);
     }
     StepParams p = make_step_params(e, e->merge, use_active, e->s_cur);
-    if (e->tma && !p.active_tiles) {
+    if (e->stream && !p.active_tiles) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(e->stream_grid);
+      cfg.blockDim = dim3(512);
+      cfg.dynamicSmemBytes = 0;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = e->pdl ? 1 : 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      FS_CUDA(cudaLaunchKernelEx(&cfg, e->stream_fn[mat], p));
+    } else if (e->tma && !p.active_tiles) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(e->step_grid);
       cfg.blockDim = dim3(e->tma_block);
@@ -1728,10 +1818,20 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
                                                                                   c->edges_per_block, e->nchunks, e->chunk_first);
   }
   if (e->incr) {
-    TRY(dalloc(&e->cnt, (size_t)e->ntiles * 32));
-    TRY(dalloc(&e->delta[0], (size_t)e->ntiles * 16));
-    TRY(dalloc(&e->delta[1], (size_t)e->ntiles * 16));
+    const size_t cap = (size_t)((n + 127) / 128) * 128;  // whole 128-node stream units
+    TRY(dalloc(&e->cnt, cap));
+    TRY(dalloc(&e->delta[0], cap / 2));
+    TRY(dalloc(&e->delta[1], cap / 2));
     TRY(recount(e, scal->step, nullptr));
+    // streaming kernel: per-node arrays readable to a multiple of 128 nodes
+    if (buf->padded >= 2 && !getenv("FS_NO_STREAM")) {
+      e->stream = true;
+      for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0);
+      int socc = 1;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&socc, (const void*)e->stream_fn[0], 512, 0) != cudaSuccess || socc < 1) socc = 1;
+      if (getenv("FS_INCR_CTAS_PER_SM")) socc = std::max(1, std::min(socc, atoi(getenv("FS_INCR_CTAS_PER_SM"))));
+      e->stream_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sms * socc, (e->ntiles + 15) / 16));
+    }
   }
   if (getenv("FS_NO_PDL")) e->pdl = false;
   if (getenv("FS_DEBUG_TIMES")) {

@@ -122,10 +122,10 @@ def default_seed_count(num_nodes: int) -> int:
 
 
 def _node_buffer(n: int, dtype: torch.dtype, dev: torch.device, fill=0) -> torch.Tensor:
-    """Per-node device array, allocated to a whole number of 32-node tiles
-    (the streaming kernel bulk-copies whole tiles, fs_state_buffers.padded)
+    """Per-node device array, allocated to a whole number of 128-node units
+    (the streaming kernels read whole tiles / vectors, fs_state_buffers.padded)
     and returned as the [:n] view."""
-    cap = (n + 31) // 32 * 32
+    cap = (n + 127) // 128 * 128
     return torch.full((cap,), fill, dtype=dtype, device=dev)[:n]
 
 
@@ -324,7 +324,7 @@ class _Engine:
             b.infectivity[0], b.infectivity[1] = _lib.ptr(self.bufs[0]), _lib.ptr(self.bufs[1])
         b.pressure = _lib.ptr(state._t.get("pressure"))
         b.rates = _lib.ptr(state._t.get("rates"))
-        b.padded = 1  # states / ages come from _node_buffer
+        b.padded = 2  # states / ages come from _node_buffer (whole 128-node units)
         self._buffers = b
         h = ctypes.c_void_p()
         _lib.check(self.lib.fs_engine_create(plan.graph.view(), plan.model, plan.config, b, scal,
