@@ -197,6 +197,19 @@ void fs_engine_destroy(fs_engine* e);
  * share one device and their mask buffers): call after every engine ran the
  * same step */
 int fs_engines_exchange_local(fs_engine* const* engines, int32_t count, void* stream);
+/* Partitioned incremental counts: a rank whose node changes
+ * infectious status pushes +-1 straight into the owner's pending-delta array —
+ * in its own memory or a peer's over NVLink — during the step, so the only
+ * per-step collective left is the tiny count / max-rate all-reduce.  Each
+ * engine exposes its two delta buffers (by step parity); every engine must be
+ * given all ranks' buffers, ptrs[parity * world + rank], before stepping:
+ * the other engines' pointers directly (one device) or peer mappings from
+ * fs_ipc_open_handle (one process per GPU). */
+int fs_engine_delta_buffers(fs_engine* e, void** out2);
+int fs_engine_set_peer_deltas(fs_engine* e, void* const* ptrs);
+int fs_ipc_get_handle(void* dptr, uint8_t* out, int32_t len);
+int fs_ipc_open_handle(const uint8_t* handle, int32_t device, void** out);
+int fs_ipc_close(void* dptr);
 /* NCCL communicator of a partitioned run: rank 0 makes the id (returns its
  * byte length, <= len), every rank calls fs_comm_init with it */
 int fs_comm_unique_id(uint8_t* out, int32_t len);

@@ -151,6 +151,11 @@ _SIGNATURES = {
                                               ctypes.POINTER(FsScalars), _c_i32, ctypes.POINTER(FsPartition),
                                               ctypes.POINTER(_vp)]),
     "fs_engines_exchange_local": (_c_i32, [_vp, _c_i32, _vp]),
+    "fs_engine_delta_buffers": (_c_i32, [_vp, _vp]),
+    "fs_engine_set_peer_deltas": (_c_i32, [_vp, _vp]),
+    "fs_ipc_get_handle": (_c_i32, [_vp, _vp, _c_i32]),
+    "fs_ipc_open_handle": (_c_i32, [_vp, _c_i32, ctypes.POINTER(_vp)]),
+    "fs_ipc_close": (_c_i32, [_vp]),
     "fs_comm_unique_id": (_c_i32, [_vp, _c_i32]),
     "fs_comm_init": (_c_i32, [_c_i32, _c_i32, _vp, _c_i32, ctypes.POINTER(_vp)]),
     "fs_comm_destroy": (None, [_vp]),

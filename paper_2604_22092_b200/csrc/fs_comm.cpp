@@ -23,7 +23,7 @@ int fs_exchange_step(void* comm, unsigned long long* d16, unsigned* max_bits, ui
   FS_NCCL(ncclGroupStart());
   FS_NCCL(ncclAllReduce(d16, d16, FS_MAX_COMPARTMENTS, ncclUint64, ncclSum, c, st));
   FS_NCCL(ncclAllReduce(max_bits, max_bits, 1, ncclUint32, ncclMax, c, st));  // rates >= 0: bits order as values
-  FS_NCCL(ncclAllGather(mask + (int64_t)rank * seg_words, mask, (size_t)seg_words, ncclUint32, c, st));
+  if (mask) FS_NCCL(ncclAllGather(mask + (int64_t)rank * seg_words, mask, (size_t)seg_words, ncclUint32, c, st));
   FS_NCCL(ncclGroupEnd());
   return 0;
 }

@@ -113,8 +113,11 @@ struct StepParams {
   // infectious status changes
   uint16_t* cnt;                 // [N] counts as of the current step's start, minus pending deltas
   uint32_t* pend[2];             // [ceil(N/2)] words of biased u16 pending deltas, double-buffered by step parity
-  const int64_t* out_ro;         // outgoing CSR (the incoming one for symmetric graphs)
-  const int32_t* out_col;
+  const int64_t* out_ro;         // outgoing CSR of the local rows (the incoming one for symmetric graphs)
+  const int32_t* out_col;        // global ids
+  int world;                     // > 1: pushes go to the owner's pending deltas (peer_pend)
+  int64_t part_chunk;            // nodes per rank
+  uint32_t* peer_pend[2][FS_MAX_PARTITIONS];  // every rank's pending-delta arrays, by parity
   int stream_evict_first;        // CSR stream larger than L2: evict-first hint on column loads
   unsigned long long* dbg;       // optional per-CTA %globaltimer stamps [grid][4]
   // model / config
@@ -452,6 +455,16 @@ struct StepShared {
   float q_press[WARPS][kQueue];
 };
 
+// end-of-step pool of the warps' leftover queue entries (drain_pooled)
+template <int WARPS>
+struct StepPool {
+  int node[WARPS * 32];
+  int state[WARPS * 32];
+  float age[WARPS * 32];
+  float press[WARPS * 32];
+  int n;
+};
+
 template <int WARPS>
 __device__ __forceinline__ void load_tables(const StepParams& p, StepShared<WARPS>& sh, int tid) {
   if (tid < FS_MAX_COMPARTMENTS) {
@@ -537,16 +550,18 @@ __device__ __forceinline__ float inf_value(const StepParams& p, const StepConst&
 // phase B: settle `cnt` queued nodes of this warp, one per lane — rate
 // (pressure or hazard), uniform, Bernoulli, successor / age / infectivity
 template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
-__device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
-                                            int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
+__device__ __forceinline__ void drain_entries(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh,
+                                              const int* qn_node, const int* qn_state, const float* qn_age,
+                                              const float* qn_press, int lane, int cnt, float& lmax,
+                                              uint32_t* mask_nxt, IT* inf_nxt) {
   __syncwarp();
   const bool ok = lane < cnt;
-  const int n = ok ? sh.q_node[warp][lane] : 0;
-  const int s = ok ? sh.q_state[warp][lane] : 0;
-  const float age = ok ? sh.q_age[warp][lane] : 0.0f;
+  const int n = ok ? qn_node[lane] : 0;
+  const int s = ok ? qn_state[lane] : 0;
+  const float age = ok ? qn_age[lane] : 0.0f;
   float rate = 0.0f;
   if (ok) {
-    if (s == k.edge_from) rate = sh.q_press[warp][lane];
+    if (s == k.edge_from) rate = qn_press[lane];
     else rate = nodal_rate(sh.kind[s], sh.p0[s], sh.p1[s], age, p.hprec);
   }
   lmax = fmaxf(lmax, rate);
@@ -569,15 +584,23 @@ __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst
       if (!k.write_inf && ((ns == k.infectious) != (s == k.infectious))) {
         atomicXor(mask_nxt + p.tile_base + (n >> 5), 1u << (n & 31));
         if (p.cnt) {  // incremental counts: +-1 on every out-neighbour's pending delta
-          uint32_t* dn = p.pend[(k.step & 1) ^ 1];
-          const int64_t gn = n + p.node_base;
-          const int64_t e0 = __ldg(p.out_ro + gn), e1 = __ldg(p.out_ro + gn + 1);
+          const int nxt = (int)((k.step & 1) ^ 1);
+          const int64_t e0 = __ldg(p.out_ro + n), e1 = __ldg(p.out_ro + n + 1);  // out-row of local node n
           const bool up = ns == k.infectious;
           for (int64_t e = e0; e < e1; ++e) {
-            const int32_t j = __ldg(p.out_col + e);
-            const uint32_t one = 1u << (16 * (j & 1));
-            if (up) atomicAdd(dn + (j >> 1), one);
-            else atomicSub(dn + (j >> 1), one);
+            const int32_t j = __ldg(p.out_col + e);  // global id
+            const uint32_t one = 1u << (16 * (j & 1));  // chunk boundaries are even: parity is global
+            uint32_t* dn;
+            if (p.world > 1) {
+              // node-partitioned: the owner's pending-delta array, in this
+              // device's memory or a peer's over NVLink
+              const int owner = (int)((int64_t)j / p.part_chunk);
+              dn = p.peer_pend[nxt][owner] + (((int64_t)j - (int64_t)owner * p.part_chunk) >> 1);
+            } else {
+              dn = p.pend[nxt] + (j >> 1);
+            }
+            if (up) atomicAdd(dn, one);
+            else atomicSub(dn, one);
           }
         }
       }
@@ -589,6 +612,43 @@ __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst
     if (MAT) p.rates[n] = rate;
   }
   __syncwarp();
+}
+
+// phase B on this warp's own queue
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
+__device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
+                                            int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
+  drain_entries<ST, AT, IT, MAT, WARPS>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp], sh.q_press[warp],
+                                        lane, cnt, lmax, mask_nxt, inf_nxt);
+}
+
+// end of a CTA's tiles: the warps' partial queues (< 32 each) are pooled and
+// drained 32 entries per warp, instead of one partly-filled drain per warp
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
+__device__ __forceinline__ void drain_pooled(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh,
+                                             StepPool<WARPS>& pool, int warp, int lane, int qn, float& lmax,
+                                             uint32_t* mask_nxt, IT* inf_nxt) {
+  int* pn = pool.node;
+  int* ps = pool.state;
+  float* pa = pool.age;
+  float* pp = pool.press;
+  int* pool_n = &pool.n;
+  if (qn > 0) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(pool_n, qn);
+    base = __shfl_sync(kFull, base, 0);
+    if (lane < qn) {
+      pn[base + lane] = sh.q_node[warp][lane];
+      ps[base + lane] = sh.q_state[warp][lane];
+      pa[base + lane] = sh.q_age[warp][lane];
+      pp[base + lane] = sh.q_press[warp][lane];
+    }
+  }
+  __syncthreads();
+  const int total = *pool_n;
+  for (int off = warp * 32; off < total; off += WARPS * 32)
+    drain_entries<ST, AT, IT, MAT, WARPS>(p, k, sh, pn + off, ps + off, pa + off, pp + off, lane, min(32, total - off),
+                                          lmax, mask_nxt, inf_nxt);
 }
 
 // phase A outcome of one tile (pressure already gathered): cheap outcomes
@@ -799,16 +859,23 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
 // Phase B (the deferral queue: hazards, uniforms, Bernoulli, pushes) is the
 // same as k_step's.
 // ---------------------------------------------------------------------------
+#ifndef FS_INCR_PF
+#define FS_INCR_PF 8
+#endif
+constexpr uint32_t kIncrPrefetch = FS_INCR_PF;  // tiles ahead for the L2 prefetch (<= 2: off)
+
 template <typename ST, typename AT, bool MAT, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   constexpr int WARPS = BLOCK / 32;
   __shared__ StepShared<WARPS> sh;
   __shared__ StepConst s_k;
+  __shared__ StepPool<WARPS> s_pool;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_launch_dependents();
   load_tables<WARPS>(p, sh, tid);  // static model tables: before the dependency wait
   pdl_wait();
   if (tid == 0) {
+    s_pool.n = 0;
     s_k = step_const(p, true);
     if (blockIdx.x == 0) commit_step_start(p, s_k);
   }
@@ -831,15 +898,28 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     in.c = cnt[n];
     in.d = pend[n];
   };
+  // L2 prefetch FS_INCR_PF tiles ahead: lanes 0-3 each touch one of the
+  // tile's four lines (states, ages, counts, deltas), so DRAM latency is paid
+  // off the critical path and the register loads two tiles ahead hit L2
+  auto prefetch = [&](uint32_t t) {
+    const uint32_t n = t * 32u;
+    const void* a = lane == 0 ? (const void*)(states + n) : lane == 1 ? (const void*)(ages + n)
+                  : lane == 2 ? (const void*)(cnt + n) : (const void*)(pend + n);
+    if (lane < 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+  };
   float lmax = 0.0f;
   int qn = 0;
   uint32_t t = blockIdx.x * WARPS + warp;
   In in0{}, in1{};
+  if (kIncrPrefetch > 2)
+    for (uint32_t j = 2; j < (uint32_t)kIncrPrefetch; ++j)
+      if (t + j * stride < ntiles) prefetch(t + j * stride);
   if (t < ntiles) load(t, in0);
   if (t + stride < ntiles) load(t + stride, in1);
   for (; t < ntiles; t += stride) {
     const In in = in0;
     in0 = in1;
+    if (kIncrPrefetch > 2 && t + kIncrPrefetch * stride < ntiles) prefetch(t + kIncrPrefetch * stride);
     if (t + 2 * stride < ntiles) load(t + 2 * stride, in1);
     const uint32_t n = t * 32u + (uint32_t)lane;
     const bool valid = n < N;
@@ -856,7 +936,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, (int64_t)t, (int64_t)n, valid, s, in.age, pressure,
                                             qn, lmax, mask_nxt, nullptr);
   }
-  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
+  drain_pooled<ST, AT, float, MAT, WARPS>(p, k, sh, s_pool, warp, lane, qn, lmax, mask_nxt, nullptr);
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
 
@@ -1411,6 +1491,8 @@ struct fs_engine {
   int stream_evict_first = 0;
   // incremental count mode
   bool incr = false;
+  uint32_t* peer_pend[2][FS_MAX_PARTITIONS] = {};  // partitioned incremental: every rank's delta arrays
+  bool peers_linked = false;
   bool stream = false;         // k_step_stream fast path of the incremental mode
   StepFn stream_fn[2] = {nullptr, nullptr};
   int stream_grid = 0;
@@ -1478,6 +1560,10 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.pend[1] = e->delta[1];
   p.out_ro = e->g.out_row_offsets;
   p.out_col = e->g.out_col_indices;
+  p.world = e->incr ? e->world : 1;
+  p.part_chunk = e->mask_seg_words * 32;
+  for (int par = 0; par < 2; ++par)
+    for (int r = 0; r < FS_MAX_PARTITIONS; ++r) p.peer_pend[par][r] = e->peer_pend[par][r];
   p.dbg = e->dbg;
   p.model = e->m;
   p.eps = e->c.epsilon;
@@ -1516,6 +1602,8 @@ MergeParams make_merge_params(const fs_engine* e) {
 }
 
 int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_active, cudaStream_t st) {
+  if (e->incr && e->world > 1 && !e->peers_linked)
+    return set_error(FS_ESTATE, "partitioned incremental engine: link the ranks' delta buffers first");
   for (int k = 0; k < nsteps; ++k) {
     const bool mat = materialize_last && (k == nsteps - 1);
     if (e->merge) {
@@ -1560,7 +1648,9 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
       // next-step mask global
       const int slot = (int)(e->h_step % 3);
       uint32_t* mask_nxt = e->b.imask[(e->h_step & 1) ^ 1];
-      const int rc = fs_exchange_step(e->comm, &e->acc[slot].d[0], &e->acc[slot].max_bits, mask_nxt,
+      // incremental counts travel as peer pushes during the step: only the
+      // accumulator is reduced; otherwise the next-step mask is all-gathered
+      const int rc = fs_exchange_step(e->comm, &e->acc[slot].d[0], &e->acc[slot].max_bits, e->incr ? nullptr : mask_nxt,
                                       e->mask_seg_words, e->rank, st);
       if (rc) return rc;
     }
@@ -1664,7 +1754,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     e->world = part->world;
     e->comm = part->comm;
     e->mask_seg_words = part->mask_segment_words;
-    if (e->comm && (e->mask_seg_words < 1 || e->mask_seg_words * e->world < e->ntiles_mask ||
+    if ((e->comm || e->world > 1) && (e->mask_seg_words < 1 || e->mask_seg_words * e->world < e->ntiles_mask ||
                     e->node_base / 32 != (int64_t)e->rank * e->mask_seg_words)) {
       delete e;
       return set_error(FS_EINVAL, "partition: ranks must own equal mask segments of mask_segment_words words");
@@ -1685,8 +1775,8 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   e->mask_smem = e->count_mode && (size_t)e->ntiles_mask * 4 <= kMaxSmemMaskBytes;
   // incremental counts: count gather + an outgoing CSR to push along, single
   // partition, degrees below the 2^15 delta headroom
-  const bool can_incr = e->count_mode && !part && g->out_row_offsets && g->out_col_indices && g->d_max < 32768 &&
-                        g->num_edges > 0;
+  const bool can_incr = e->count_mode && g->out_row_offsets && g->out_col_indices && g->d_max < 32768 &&
+                        g->num_edges > 0 && (!part || part->mask_segment_words > 0);
   if (c->incremental == 1 && !can_incr) { delete e; return set_error(FS_EINVAL, "incremental counts need the count gather, an outgoing CSR, d_max < 32768 and one partition"); }
   e->incr = can_incr && c->incremental != 0;
   e->merge = c->strategy == FS_MERGE && g->num_edges > 0 && !e->incr;
@@ -2069,6 +2159,50 @@ int fs_engine_store_infectivity(fs_engine* e, void* out, void* stream) {
     return 0;
   }
   FS_CUDA(cudaMemcpyAsync(out, e->b.infectivity[cur], (size_t)n * (e->mixed ? 2 : 4), cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+int fs_engine_delta_buffers(fs_engine* e, void** out2) {
+  if (!e || !out2) return set_error(FS_EINVAL, "null argument");
+  if (!e->incr) return set_error(FS_ESTATE, "engine does not use incremental counts");
+  out2[0] = e->delta[0];
+  out2[1] = e->delta[1];
+  return 0;
+}
+
+int fs_engine_set_peer_deltas(fs_engine* e, void* const* ptrs) {
+  if (!e || !ptrs) return set_error(FS_EINVAL, "null argument");
+  if (!e->incr || e->world < 2) return set_error(FS_ESTATE, "not a partitioned incremental engine");
+  for (int par = 0; par < 2; ++par)
+    for (int r = 0; r < e->world; ++r) {
+      if (!ptrs[par * e->world + r]) return set_error(FS_EINVAL, "null delta buffer for rank %d", r);
+      e->peer_pend[par][r] = static_cast<uint32_t*>(ptrs[par * e->world + r]);
+    }
+  if (e->peer_pend[0][e->rank] != e->delta[0] || e->peer_pend[1][e->rank] != e->delta[1])
+    return set_error(FS_EINVAL, "rank %d's own entries must be its own delta buffers", e->rank);
+  e->peers_linked = true;
+  return 0;
+}
+
+int fs_ipc_get_handle(void* dptr, uint8_t* out, int32_t len) {
+  if (!dptr || !out || len < (int32_t)sizeof(cudaIpcMemHandle_t)) return set_error(FS_EINVAL, "ipc handle buffer too small");
+  cudaIpcMemHandle_t h;
+  FS_CUDA(cudaIpcGetMemHandle(&h, dptr));
+  memcpy(out, &h, sizeof h);
+  return (int)sizeof h;
+}
+
+int fs_ipc_open_handle(const uint8_t* in, int32_t device, void** out) {
+  if (!in || !out) return set_error(FS_EINVAL, "null argument");
+  FS_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, in, sizeof h);
+  FS_CUDA(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+int fs_ipc_close(void* dptr) {
+  if (dptr) FS_CUDA(cudaIpcCloseMemHandle(dptr));
   return 0;
 }
 

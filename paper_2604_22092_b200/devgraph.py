@@ -43,6 +43,7 @@ class DeviceCsrGraph:
         self._ro = row_offsets            # int64[num_rows + 1]
         self._col_buffer = col_buffer     # int32[>= num_edges + 4] (bulk-copy slack)
         self.d_max = int(d_max)
+        self.symmetric_global = True  # fs_gen_regular graphs are undirected: out-rows == in-rows
         self._host: dict[str, np.ndarray] = {}
         self.outgoing = None
 

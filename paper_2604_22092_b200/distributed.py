@@ -96,13 +96,13 @@ def partition_plan(num_nodes: int, world: int, align: int = ALIGN) -> PartitionP
     return PartitionPlan(num_nodes, world, chunk, tuple(ranges))
 
 
-def _config(cfg: RenewalConfig, strategy) -> _lib.FsConfig:
+def _config(cfg: RenewalConfig, strategy, incremental: int) -> _lib.FsConfig:
     return _lib.FsConfig(
         epsilon=cfg.epsilon, tau_max=cfg.tau_max, delta=cfg.delta, steps_per_batch=cfg.steps_per_batch,
         strategy=_STRATEGY_CODE[strategy], compaction=int(cfg.compaction), mixed_precision=int(cfg.mixed_precision),
         lanes_per_node=cfg.lanes_per_node, edges_per_block=cfg.edges_per_block, hazard_chunk=cfg.hazard_chunk,
         chunk_skip=int(cfg.chunk_skip), carry_tau=int(cfg.carry_tau), rng=RNG_KINDS[cfg.rng],
-        hazard_precision=_PRECISION[cfg.hazard_precision], count_gather=1, incremental=0)
+        hazard_precision=_PRECISION[cfg.hazard_precision], count_gather=1, incremental=incremental)
 
 
 def _initial_mask(plan: PartitionPlan, seed_ids: torch.Tensor, infectious: bool, dev) -> torch.Tensor:
@@ -162,9 +162,21 @@ class _Partition:
                                 mask_segment_words=plan.mask_segment_words, rank=rank, world=plan.world,
                                 comm=comm)
         h = ctypes.c_void_p()
-        _lib.check(self.lib.fs_engine_create_partitioned(self.dg.view(), model_descriptor(m), _config(cfg, strategy),
-                                                          b, scal, dev.index, part, ctypes.byref(h)))
+        incr = {"auto": -1, "incremental": 1}.get(cfg.gather, 0) if self.dg.symmetric else 0
+        _lib.check(self.lib.fs_engine_create_partitioned(self.dg.view(), model_descriptor(m),
+                                                          _config(cfg, strategy, incr), b, scal, dev.index, part,
+                                                          ctypes.byref(h)))
         self.handle = h
+        bufs = (ctypes.c_void_p * 2)()
+        self.incremental = self.lib.fs_engine_delta_buffers(self.handle, bufs) == 0
+        self.delta_buffers = (bufs[0], bufs[1]) if self.incremental else None
+
+    def link_peers(self, table) -> None:
+        """table[parity][rank] = device address of that rank's delta buffer
+        (own entries: this engine's buffers)."""
+        world = len(table[0])
+        arr = (ctypes.c_void_p * (2 * world))(*[table[par][r] for par in range(2) for r in range(world)])
+        _lib.check(self.lib.fs_engine_set_peer_deltas(self.handle, arr))
 
     def close(self) -> None:
         if getattr(self, "handle", None):
@@ -212,6 +224,10 @@ class LocalPartitionedRun:
         self.masks = [mask0, mask0.clone()]
         self.parts = [_Partition(graph_parts[r], m, cfg, seed, plan, r, ids, self.masks, None, dev)
                       for r in range(plan.world)]
+        if plan.world > 1 and self.parts[0].incremental:
+            table = [[p.delta_buffers[par] for p in self.parts] for par in range(2)]
+            for p in self.parts:
+                p.link_peers(table)
         self._arr = (ctypes.c_void_p * len(self.parts))(*[p.handle.value for p in self.parts])
         self.steps = 0
 
@@ -269,6 +285,36 @@ class DistributedRun:
         self.masks = [mask0, mask0.clone()]
         self.part = _Partition(graph_local, m, cfg, seed, plan, rank, ids, self.masks, comm.value, dev)
         self.steps = 0
+        self._opened = []
+        if plan.world > 1 and self.part.incremental:
+            self._link_peers_ipc(dev, pg)
+
+    def _link_peers_ipc(self, dev, pg) -> None:
+        """Map every rank's pending-delta buffers into this process (CUDA IPC
+        over NVLink) so the step kernel can push into them directly."""
+        import torch.distributed as dist
+
+        lib = _lib.load()
+        mine = []
+        for ptr in self.part.delta_buffers:
+            h = (ctypes.c_uint8 * 128)()
+            nb = _lib.check(lib.fs_ipc_get_handle(ptr, h, 128))
+            mine.append(bytes(h)[:nb])
+        allh = [None] * self.plan.world
+        dist.all_gather_object(allh, mine, group=pg)
+        table = [[None] * self.plan.world for _ in range(2)]
+        for r in range(self.plan.world):
+            for par in range(2):
+                if r == self.rank:
+                    table[par][r] = self.part.delta_buffers[par]
+                    continue
+                buf = (ctypes.c_uint8 * 128).from_buffer_copy(allh[r][par].ljust(128, b"\0"))
+                out = ctypes.c_void_p()
+                _lib.check(lib.fs_ipc_open_handle(buf, dev.index, ctypes.byref(out)))
+                self._opened.append(out)
+                table[par][r] = out.value
+        self.part.link_peers(table)
+        dist.barrier(group=pg)  # every rank linked before anyone pushes
 
     def run_batch(self):
         first = self.steps
@@ -281,6 +327,10 @@ class DistributedRun:
         self.steps += nsteps
 
     def close(self) -> None:
+        lib = _lib.load()
+        for h in getattr(self, "_opened", []):
+            lib.fs_ipc_close(h)
+        self._opened = []
         self.part.close()
         if getattr(self, "comm", None) and self.comm.value:
             _lib.load().fs_comm_destroy(self.comm)

@@ -1,0 +1,97 @@
+"""GPU ensembles of independent renewal trajectories.
+
+The reference runs ensembles as a process pool of CPU trajectories,
+`run_ensemble(engine, g, m, cfg, seed, t_final, runs, ...)` with per-trial
+seeds `derive_seed(seed, trial)` and results ordered by trial
+(R/analysis.py:97-130).  Here the trials of the "renewal" engine run on one
+GPU at the same time: every trial owns an engine on its own CUDA stream,
+the graph's device copy is shared, and the host loop keeps `concurrency`
+trials in flight, launching one CUDA-graph batch per trial per round and
+reading each trial's per-batch log as it lands.  Each trial is exactly
+`run_renewal(g, m, cfg, derive_seed(seed, trial), ...)` (same kernels, same
+per-trial RNG keys), so the ensemble is bit-identical to the sequential one
+and to the reference's CPU ensemble (tests/test_ensemble.py).
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import torch
+
+from . import _device
+from .renewal import RenewalConfig, _build_plan, _check_conservation, init_renewal_state
+from .rng import derive_seed
+from .trajectory import DEFAULT_GRID_POINTS, TrajectoryRecord, make_record
+
+__all__ = ["run_ensemble"]
+
+
+class _Trial:
+    def __init__(self, trial: int, g, m, cfg, seed: int, seed_count, seed_compartment, stream, plan):
+        self.trial, self.stream = trial, stream
+        self.seed = derive_seed(seed, trial)
+        self.t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            self.state = init_renewal_state(g, m, cfg, self.seed, seed_count, seed_compartment)
+            self.eng = self.state._bind(plan, self.seed, materialize=False)
+        self.times = [0.0]
+        self.rows = [self.state.counts.copy()]
+        self.done, self.clock = 0, 0.0
+
+    def launch(self) -> None:
+        self.eng.run_batch(materialize=False)
+
+    def collect(self, b: int, n: int) -> None:
+        clocks, _, counts = self.eng.read_log(self.done, b)
+        _check_conservation(counts, n)
+        self.times.extend(clocks.tolist())
+        self.rows.extend(counts)
+        self.done += b
+        self.clock = float(clocks[-1])
+
+    def record(self, g, m, t_final: float, grid_points: int) -> TrajectoryRecord:
+        wall = time.perf_counter() - self.t0
+        t_arr = np.asarray(self.times)
+        steps = min(int(np.searchsorted(t_arr, t_final, side="left")), self.done)
+        rec = make_record(t_arr, np.asarray(self.rows), m.compartments, g.num_nodes, t_final, grid_points,
+                          extra_summary={"step_count": steps, "wall_clock": wall, "engine": "renewal"})
+        with torch.cuda.stream(self.stream):
+            self.state._unbind()
+        self.stream.synchronize()
+        return rec
+
+
+def run_ensemble(engine: str, g, m, cfg, seed: int, t_final: float, runs: int,
+                 grid_points: int = DEFAULT_GRID_POINTS, workers: int = 1, seed_count=None, seed_compartment=None,
+                 concurrency: int = 32) -> list[TrajectoryRecord]:
+    """R/analysis.py:97-130 for the renewal engine, trials concurrent on the
+    GPU (`workers` is accepted for signature compatibility; `concurrency`
+    bounds the trials in flight).  Records are ordered by trial index."""
+    if engine != "renewal":
+        raise ValueError(f"the B200 ensemble runs the renewal engine only (got {engine!r})")
+    cfg = cfg or RenewalConfig()
+    _device.device()
+    b = cfg.steps_per_batch
+    free = [torch.cuda.Stream() for _ in range(max(1, min(concurrency, runs)))]
+    plan = _build_plan(g, m, cfg, bool(cfg.mixed_precision))  # one device copy of the graph for every trial
+    out: list[TrajectoryRecord | None] = [None] * runs
+    pending = list(range(runs))
+    live: list[_Trial] = []
+    torch.cuda.current_stream().synchronize()  # the graph upload precedes the trial streams
+    while pending or live:
+        while pending and free:
+            live.append(_Trial(pending.pop(0), g, m, cfg, seed, seed_count, seed_compartment, free.pop(), plan))
+        for tr in live:
+            tr.launch()
+        still = []
+        for tr in live:
+            tr.collect(b, g.num_nodes)
+            if tr.clock < t_final:
+                still.append(tr)
+            else:
+                out[tr.trial] = tr.record(g, m, t_final, grid_points)
+                free.append(tr.stream)
+        live = still
+    return out  # type: ignore[return-value]

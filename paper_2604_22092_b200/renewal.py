@@ -214,7 +214,9 @@ class _DeviceGraph:
         self.weights = None
         self.weights_bf16 = False
         self.d_max = int(g.d_max)
-        self.symmetric = not g.partitioned  # fs_gen_regular graphs are undirected by construction
+        # fs_gen_regular graphs are undirected by construction: a row slice's
+        # out-rows are its in-rows (global ids), which is all the pushes need
+        self.symmetric = bool(getattr(g, "symmetric_global", False))
         return self
 
 

@@ -38,12 +38,32 @@ def ours(golden):
     g = fs.gen_erdos_renyi(n, d, seed=seed)
     m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
     cfg = fs.RenewalConfig()
-    recs = [fs.run_renewal(g, m, cfg, fs.derive_seed(meta["seed"], t), meta["t_final"], seed_count=meta["seed_count"])
-            for t in range(meta["runs"])]
+    # the GPU ensemble runner (concurrent trials on CUDA streams)
+    recs = fs.run_ensemble("renewal", g, m, cfg, meta["seed"], meta["t_final"], meta["runs"],
+                           seed_count=meta["seed_count"])
     out = {k: np.array([r.summary[k] for r in recs], dtype=np.float64)
            for k in ("peak_I", "peak_I_time", "final_R", "step_count")}
     out["mean"] = np.mean([r.fractions for r in recs], axis=0)
+    out["recs"] = recs
+    out["inputs"] = (g, m, cfg, meta)
     return out
+
+
+def test_ensemble_runner_equals_sequential_run_renewal(ours):
+    g, m, cfg, meta = ours["inputs"]
+    for t in (0, 1, 57, meta["runs"] - 1):
+        rec = fs.run_renewal(g, m, cfg, fs.derive_seed(meta["seed"], t), meta["t_final"], seed_count=meta["seed_count"])
+        assert np.array_equal(rec.fractions, ours["recs"][t].fractions)
+        assert rec.summary["step_count"] == ours["recs"][t].summary["step_count"]
+
+
+def test_mixed_precision_final_r_within_half_percent(ours):
+    # reference acceptance criterion 7 (T/test_acceptance.py:215-233)
+    g, m, _, meta = ours["inputs"]
+    recs = fs.run_ensemble("renewal", g, m, fs.RenewalConfig(mixed_precision=True), meta["seed"], meta["t_final"],
+                           meta["runs"], seed_count=meta["seed_count"])
+    fr = np.mean([r.summary["final_R"] for r in recs])
+    assert abs(fr - ours["final_R"].mean()) <= 0.005 * ours["final_R"].mean()
 
 
 def test_tau_leap_ensemble_is_the_reference_trajectory_by_trajectory(golden, ours):
