@@ -119,6 +119,8 @@ struct StepParams {
   int64_t part_chunk;            // nodes per rank
   uint32_t* peer_pend[2][FS_MAX_PARTITIONS];  // every rank's pending-delta arrays, by parity
   int stream_evict_first;        // CSR stream larger than L2: evict-first hint on column loads
+  int incr_pf;                   // k_step_incr: L2 prefetch distance in tiles (<= 2: off)
+  int incr_pool;                 // k_step_incr: pool the warps' leftover queues at the end
   unsigned long long* dbg;       // optional per-CTA %globaltimer stamps [grid][4]
   // model / config
   fs_model model;
@@ -911,15 +913,16 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   int qn = 0;
   uint32_t t = blockIdx.x * WARPS + warp;
   In in0{}, in1{};
-  if (kIncrPrefetch > 2)
-    for (uint32_t j = 2; j < (uint32_t)kIncrPrefetch; ++j)
+  const uint32_t pf = (uint32_t)p.incr_pf;
+  if (pf > 2)
+    for (uint32_t j = 2; j < pf; ++j)
       if (t + j * stride < ntiles) prefetch(t + j * stride);
   if (t < ntiles) load(t, in0);
   if (t + stride < ntiles) load(t + stride, in1);
   for (; t < ntiles; t += stride) {
     const In in = in0;
     in0 = in1;
-    if (kIncrPrefetch > 2 && t + kIncrPrefetch * stride < ntiles) prefetch(t + kIncrPrefetch * stride);
+    if (pf > 2 && t + pf * stride < ntiles) prefetch(t + pf * stride);
     if (t + 2 * stride < ntiles) load(t + 2 * stride, in1);
     const uint32_t n = t * 32u + (uint32_t)lane;
     const bool valid = n < N;
@@ -936,7 +939,8 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, (int64_t)t, (int64_t)n, valid, s, in.age, pressure,
                                             qn, lmax, mask_nxt, nullptr);
   }
-  drain_pooled<ST, AT, float, MAT, WARPS>(p, k, sh, s_pool, warp, lane, qn, lmax, mask_nxt, nullptr);
+  if (p.incr_pool) drain_pooled<ST, AT, float, MAT, WARPS>(p, k, sh, s_pool, warp, lane, qn, lmax, mask_nxt, nullptr);
+  else if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
 
@@ -1555,6 +1559,8 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.pre = use_pre ? e->pre : nullptr;
   p.count_mode = e->count_mode;
   p.stream_evict_first = e->stream_evict_first;
+  p.incr_pf = getenv("FS_INCR_PF") ? atoi(getenv("FS_INCR_PF")) : (int)kIncrPrefetch;
+  p.incr_pool = getenv("FS_NO_POOL") ? 0 : 1;
   p.cnt = e->incr ? e->cnt : nullptr;
   p.pend[0] = e->delta[0];
   p.pend[1] = e->delta[1];
