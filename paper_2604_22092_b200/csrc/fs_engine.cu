@@ -119,8 +119,6 @@ struct StepParams {
   int64_t part_chunk;            // nodes per rank
   uint32_t* peer_pend[2][FS_MAX_PARTITIONS];  // every rank's pending-delta arrays, by parity
   int stream_evict_first;        // CSR stream larger than L2: evict-first hint on column loads
-  int incr_pf;                   // k_step_incr: L2 prefetch distance in tiles (<= 2: off)
-  int incr_pool;                 // k_step_incr: pool the warps' leftover queues at the end
   unsigned long long* dbg;       // optional per-CTA %globaltimer stamps [grid][4]
   // model / config
   fs_model model;
@@ -457,16 +455,6 @@ struct StepShared {
   float q_press[WARPS][kQueue];
 };
 
-// end-of-step pool of the warps' leftover queue entries (drain_pooled)
-template <int WARPS>
-struct StepPool {
-  int node[WARPS * 32];
-  int state[WARPS * 32];
-  float age[WARPS * 32];
-  float press[WARPS * 32];
-  int n;
-};
-
 template <int WARPS>
 __device__ __forceinline__ void load_tables(const StepParams& p, StepShared<WARPS>& sh, int tid) {
   if (tid < FS_MAX_COMPARTMENTS) {
@@ -622,35 +610,6 @@ __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst
                                             int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
   drain_entries<ST, AT, IT, MAT, WARPS>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp], sh.q_press[warp],
                                         lane, cnt, lmax, mask_nxt, inf_nxt);
-}
-
-// end of a CTA's tiles: the warps' partial queues (< 32 each) are pooled and
-// drained 32 entries per warp, instead of one partly-filled drain per warp
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
-__device__ __forceinline__ void drain_pooled(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh,
-                                             StepPool<WARPS>& pool, int warp, int lane, int qn, float& lmax,
-                                             uint32_t* mask_nxt, IT* inf_nxt) {
-  int* pn = pool.node;
-  int* ps = pool.state;
-  float* pa = pool.age;
-  float* pp = pool.press;
-  int* pool_n = &pool.n;
-  if (qn > 0) {
-    int base = 0;
-    if (lane == 0) base = atomicAdd(pool_n, qn);
-    base = __shfl_sync(kFull, base, 0);
-    if (lane < qn) {
-      pn[base + lane] = sh.q_node[warp][lane];
-      ps[base + lane] = sh.q_state[warp][lane];
-      pa[base + lane] = sh.q_age[warp][lane];
-      pp[base + lane] = sh.q_press[warp][lane];
-    }
-  }
-  __syncthreads();
-  const int total = *pool_n;
-  for (int off = warp * 32; off < total; off += WARPS * 32)
-    drain_entries<ST, AT, IT, MAT, WARPS>(p, k, sh, pn + off, ps + off, pa + off, pp + off, lane, min(32, total - off),
-                                          lmax, mask_nxt, inf_nxt);
 }
 
 // phase A outcome of one tile (pressure already gathered): cheap outcomes
@@ -861,23 +820,16 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
 // Phase B (the deferral queue: hazards, uniforms, Bernoulli, pushes) is the
 // same as k_step's.
 // ---------------------------------------------------------------------------
-#ifndef FS_INCR_PF
-#define FS_INCR_PF 8
-#endif
-constexpr uint32_t kIncrPrefetch = FS_INCR_PF;  // tiles ahead for the L2 prefetch (<= 2: off)
-
 template <typename ST, typename AT, bool MAT, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   constexpr int WARPS = BLOCK / 32;
   __shared__ StepShared<WARPS> sh;
   __shared__ StepConst s_k;
-  __shared__ StepPool<WARPS> s_pool;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_launch_dependents();
   load_tables<WARPS>(p, sh, tid);  // static model tables: before the dependency wait
   pdl_wait();
   if (tid == 0) {
-    s_pool.n = 0;
     s_k = step_const(p, true);
     if (blockIdx.x == 0) commit_step_start(p, s_k);
   }
@@ -900,29 +852,15 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     in.c = cnt[n];
     in.d = pend[n];
   };
-  // L2 prefetch FS_INCR_PF tiles ahead: lanes 0-3 each touch one of the
-  // tile's four lines (states, ages, counts, deltas), so DRAM latency is paid
-  // off the critical path and the register loads two tiles ahead hit L2
-  auto prefetch = [&](uint32_t t) {
-    const uint32_t n = t * 32u;
-    const void* a = lane == 0 ? (const void*)(states + n) : lane == 1 ? (const void*)(ages + n)
-                  : lane == 2 ? (const void*)(cnt + n) : (const void*)(pend + n);
-    if (lane < 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-  };
   float lmax = 0.0f;
   int qn = 0;
   uint32_t t = blockIdx.x * WARPS + warp;
   In in0{}, in1{};
-  const uint32_t pf = (uint32_t)p.incr_pf;
-  if (pf > 2)
-    for (uint32_t j = 2; j < pf; ++j)
-      if (t + j * stride < ntiles) prefetch(t + j * stride);
   if (t < ntiles) load(t, in0);
   if (t + stride < ntiles) load(t + stride, in1);
   for (; t < ntiles; t += stride) {
     const In in = in0;
     in0 = in1;
-    if (pf > 2 && t + pf * stride < ntiles) prefetch(t + pf * stride);
     if (t + 2 * stride < ntiles) load(t + 2 * stride, in1);
     const uint32_t n = t * 32u + (uint32_t)lane;
     const bool valid = n < N;
@@ -939,8 +877,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, (int64_t)t, (int64_t)n, valid, s, in.age, pressure,
                                             qn, lmax, mask_nxt, nullptr);
   }
-  if (p.incr_pool) drain_pooled<ST, AT, float, MAT, WARPS>(p, k, sh, s_pool, warp, lane, qn, lmax, mask_nxt, nullptr);
-  else if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
+  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
 
@@ -1559,8 +1496,6 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.pre = use_pre ? e->pre : nullptr;
   p.count_mode = e->count_mode;
   p.stream_evict_first = e->stream_evict_first;
-  p.incr_pf = getenv("FS_INCR_PF") ? atoi(getenv("FS_INCR_PF")) : (int)kIncrPrefetch;
-  p.incr_pool = getenv("FS_NO_POOL") ? 0 : 1;
   p.cnt = e->incr ? e->cnt : nullptr;
   p.pend[0] = e->delta[0];
   p.pend[1] = e->delta[1];
