@@ -317,6 +317,8 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload is None:
+        args.workload = "c2" if world == 1 else "c5"
     if world > 1:
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
     if args.impl == "reference":
@@ -329,8 +331,6 @@ def main() -> None:
     import paper_2604_22092_b200 as fs
     from paper_2604_22092_b200 import renewal as R
 
-    if args.workload is None:
-        args.workload = "c2" if world == 1 else "c5"
     if world > 1:
         run_partitioned(args, WORKLOADS[args.workload], rank, world, local)
         dist.destroy_process_group()
@@ -420,6 +420,7 @@ def main() -> None:
         d2h = 8 * (2 + m.num_compartments) * steps_run
         e2e = {"value": n * steps_run / wall / 1e9, "unit": "G-NUPS", "h2d_bytes_per_step": h2d / steps_run,
                "d2h_bytes_per_step": d2h / steps_run, "steps": steps_run, "wall_s": wall,
+               "setup_s": rec.summary.get("setup_s"),
                "what": f"run_renewal(t_final={t_final}) from {src}: init + {steps_run} steps in "
                        f"CUDA-graph batches + per-batch log D2H + record",
                "final_R": rec.summary["final_R"], "peak_I": rec.summary["peak_I"]}

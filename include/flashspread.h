@@ -238,6 +238,11 @@ int fs_engine_read_log(fs_engine* e, int64_t first_step, int32_t n,
                        double* clocks, double* taus, int64_t* counts, void* stream);
 int fs_engine_get_scalars(fs_engine* e, fs_scalars* out, void* stream);
 int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream);
+/* The engine memoises nodal hazards per age cohort (nodes that entered a
+ * compartment at the same step share their age bit for bit): call this after
+ * writing ages or states from outside the engine (host edits, snapshot
+ * restores) so no node is assumed to follow its cohort. */
+int fs_engine_reset_age_memo(fs_engine* e, void* stream);
 /* re-derive the infectious mask / general buffer from a freshly uploaded
  * infectivity array (host edits between steps); `inf` has the storage dtype */
 int fs_engine_load_infectivity(fs_engine* e, const void* inf, void* stream);

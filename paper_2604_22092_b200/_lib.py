@@ -152,6 +152,7 @@ _SIGNATURES = {
                                               ctypes.POINTER(_vp)]),
     "fs_engines_exchange_local": (_c_i32, [_vp, _c_i32, _vp]),
     "fs_engine_delta_buffers": (_c_i32, [_vp, _vp]),
+    "fs_engine_reset_age_memo": (_c_i32, [_vp, _vp]),
     "fs_engine_set_peer_deltas": (_c_i32, [_vp, _vp]),
     "fs_ipc_get_handle": (_c_i32, [_vp, _vp, _c_i32]),
     "fs_ipc_open_handle": (_c_i32, [_vp, _c_i32, ctypes.POINTER(_vp)]),

@@ -51,6 +51,10 @@ constexpr int kCntStride = FS_MAX_COMPARTMENTS;
 constexpr size_t kMaxSmemMaskBytes = 188u * 1024u;  // + ~34 KB static (queues) <= 227 KB
 
 enum Gather { G_COUNT_SMEM = 0, G_COUNT_GLOBAL = 1, G_F32 = 2, G_PRE = 3, G_INCR = 4 };
+constexpr int32_t kEntryInvalid = INT32_MIN;  // age not known to follow its cohort (init, host edits)
+constexpr int kMemoSlots = 2;                  // age-dependent compartments memoised per CTA
+constexpr int kMemoW = 1 << 10;                // entry steps per compartment (direct-mapped ring)
+
 constexpr uint32_t kDeltaBias = 0x8000u;  // pending delta d is stored as d + 0x8000 (|d| <= d_max < 2^15)
 enum Strat { S_THREAD = 0, S_WARP = 1 };
 
@@ -119,6 +123,10 @@ struct StepParams {
   int64_t part_chunk;            // nodes per rank
   uint32_t* peer_pend[2][FS_MAX_PARTITIONS];  // every rank's pending-delta arrays, by parity
   int stream_evict_first;        // CSR stream larger than L2: evict-first hint on column loads
+  int host_parity;               // the host's mirror of (step & 1) for this launch (early loads), -1: none
+  // age-cohort hazard memo: entry step of each node's
+  // current compartment; the per-CTA memo itself lives in shared memory
+  int32_t* entry;                // [N] or nullptr (memo off)
   unsigned long long* dbg;       // optional per-CTA %globaltimer stamps [grid][4]
   // model / config
   fs_model model;
@@ -127,6 +135,29 @@ struct StepParams {
   int hprec;
   float inf_val;                 // stored infectivity of an I node (count mode), promoted
 };
+
+// Per-CTA, per-step memo of nodal hazard rates by age cohort: every node
+// that entered compartment c at step j carries the same age bits (the same
+// f32 recurrence age += f32(tau) since), hence the same rate, so the f64
+// hazard (R/hazards.py:122-132) runs once per (CTA, c, j) instead of once
+// per node.  Entries are (step tag << 32 | rate bits); racing writers store
+// identical values.  Results are bit-identical with or without it.
+struct HazardMemo {
+  unsigned long long e[kMemoSlots][kMemoW];
+  int slot[FS_MAX_COMPARTMENTS];  // compartment -> memo slot, -1: not memoised
+};
+
+template <int BLOCK>
+__device__ __forceinline__ void memo_init(HazardMemo& hm, const StepParams& p, int tid) {
+  for (int i = tid; i < kMemoSlots * kMemoW; i += BLOCK) (&hm.e[0][0])[i] = ~0ull;  // tag 0xFFFFFFFF: stale
+  if (tid == 0) {
+    int next = 0;
+    for (int c = 0; c < FS_MAX_COMPARTMENTS; ++c) {
+      const bool costly = c < p.model.num_compartments && p.model.comp[c].hazard >= FS_HZ_LOGNORMAL;
+      hm.slot[c] = (costly && next < kMemoSlots) ? next++ : -1;
+    }
+  }
+}
 
 struct MergeParams {
   const int64_t* ro;
@@ -539,20 +570,60 @@ __device__ __forceinline__ float inf_value(const StepParams& p, const StepConst&
 
 // phase B: settle `cnt` queued nodes of this warp, one per lane — rate
 // (pressure or hazard), uniform, Bernoulli, successor / age / infectivity
+// incremental counts: +-1 on node j's pending delta (buffer `nxt`), in this
+// device's memory or, node-partitioned, the owner's — possibly a peer GPU's
+// over NVLink.  Chunk boundaries are even, so the 16-bit lane
+// of j is the same in global and owner-local numbering.
+__device__ __forceinline__ void push_delta(const StepParams& p, int nxt, int32_t j, bool up) {
+  const uint32_t one = 1u << (16 * (j & 1));
+  uint32_t* dn;
+  if (p.world > 1) {
+    const int owner = (int)((int64_t)j / p.part_chunk);
+    dn = p.peer_pend[nxt][owner] + (((int64_t)j - (int64_t)owner * p.part_chunk) >> 1);
+  } else {
+    dn = p.pend[nxt] + (j >> 1);
+  }
+  if (up) atomicAdd(dn, one);
+  else atomicSub(dn, one);
+}
+
 template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
 __device__ __forceinline__ void drain_entries(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh,
                                               const int* qn_node, const int* qn_state, const float* qn_age,
                                               const float* qn_press, int lane, int cnt, float& lmax,
-                                              uint32_t* mask_nxt, IT* inf_nxt) {
+                                              uint32_t* mask_nxt, IT* inf_nxt, HazardMemo* hm = nullptr) {
   __syncwarp();
   const bool ok = lane < cnt;
+  int push = 0;  // +1 / -1: this node's infectious status changed
   const int n = ok ? qn_node[lane] : 0;
   const int s = ok ? qn_state[lane] : 0;
   const float age = ok ? qn_age[lane] : 0.0f;
   float rate = 0.0f;
+  bool compute = false;
+  unsigned long long* slot = nullptr;
   if (ok) {
-    if (s == k.edge_from) rate = qn_press[lane];
-    else rate = nodal_rate(sh.kind[s], sh.p0[s], sh.p1[s], age, p.hprec);
+    if (s == k.edge_from) {
+      rate = qn_press[lane];
+    } else if (hm && hm->slot[s] >= 0) {
+      const int32_t j = p.entry[n];
+      const int64_t since = k.step - (int64_t)j;
+      compute = true;
+      if (j != kEntryInvalid && since >= 0 && since < kMemoW) {
+        slot = &hm->e[hm->slot[s]][(uint32_t)j & (kMemoW - 1)];
+        const unsigned long long v = *reinterpret_cast<volatile unsigned long long*>(slot);
+        if ((uint32_t)(v >> 32) == (uint32_t)k.step) {
+          rate = __uint_as_float((uint32_t)v);
+          compute = false;
+        }
+      }
+    } else {
+      rate = nodal_rate(sh.kind[s], sh.p0[s], sh.p1[s], age, p.hprec);
+    }
+  }
+  if (compute) {
+    rate = nodal_rate(sh.kind[s], sh.p0[s], sh.p1[s], age, p.hprec);
+    // racing writers of one slot store identical bits
+    if (slot) *reinterpret_cast<volatile unsigned long long*>(slot) = ((unsigned long long)(uint32_t)k.step << 32) | __float_as_uint(rate);
   }
   lmax = fmaxf(lmax, rate);
   bool fire = false;
@@ -569,30 +640,12 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
       ns = sh.succ[s];
       nage = 0.0f;
       reinterpret_cast<ST*>(p.states)[n] = (ST)ns;
+      if (p.entry) p.entry[n] = (int32_t)k.step;  // age cohort of the new compartment
       atomicAdd(&sh.cnt[ns], 1);
       atomicAdd(&sh.cnt[s], -1);
       if (!k.write_inf && ((ns == k.infectious) != (s == k.infectious))) {
         atomicXor(mask_nxt + p.tile_base + (n >> 5), 1u << (n & 31));
-        if (p.cnt) {  // incremental counts: +-1 on every out-neighbour's pending delta
-          const int nxt = (int)((k.step & 1) ^ 1);
-          const int64_t e0 = __ldg(p.out_ro + n), e1 = __ldg(p.out_ro + n + 1);  // out-row of local node n
-          const bool up = ns == k.infectious;
-          for (int64_t e = e0; e < e1; ++e) {
-            const int32_t j = __ldg(p.out_col + e);  // global id
-            const uint32_t one = 1u << (16 * (j & 1));  // chunk boundaries are even: parity is global
-            uint32_t* dn;
-            if (p.world > 1) {
-              // node-partitioned: the owner's pending-delta array, in this
-              // device's memory or a peer's over NVLink
-              const int owner = (int)((int64_t)j / p.part_chunk);
-              dn = p.peer_pend[nxt][owner] + (((int64_t)j - (int64_t)owner * p.part_chunk) >> 1);
-            } else {
-              dn = p.pend[nxt] + (j >> 1);
-            }
-            if (up) atomicAdd(dn, one);
-            else atomicSub(dn, one);
-          }
-        }
+        if (p.cnt) push = (ns == k.infectious) ? 1 : -1;  // incremental counts: pushes below
       }
     } else {
       nage = __fadd_rn(age, k.tau_f);  // queued nodes are never terminal
@@ -601,15 +654,38 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
     if (k.write_inf) inf_nxt[n] = from_f32<IT>(inf_value(p, k, ns, nage));
     if (MAT) p.rates[n] = rate;
   }
+  if (p.cnt) {
+    // +-1 on every out-neighbour's pending delta.  Rows of <= 32 edges are
+    // pushed by their own lane; longer rows (scale-free hubs) by the whole
+    // warp, 32 edges per iteration, so one hub does not serialise the step.
+    const int nxt = (int)((k.step & 1) ^ 1);
+    int64_t e0 = 0, e1 = 0;
+    if (push) {
+      e0 = __ldg(p.out_ro + n);  // out-row of local node n
+      e1 = __ldg(p.out_ro + n + 1);
+    }
+    const bool wide = push && (e1 - e0 > 32);
+    if (push && !wide)
+      for (int64_t e = e0; e < e1; ++e) push_delta(p, nxt, __ldg(p.out_col + e), push > 0);
+    unsigned wides = __ballot_sync(kFull, wide);
+    while (wides) {
+      const int src = __ffs(wides) - 1;
+      wides &= wides - 1;
+      const int64_t a0 = __shfl_sync(kFull, e0, src), a1 = __shfl_sync(kFull, e1, src);
+      const bool up = __shfl_sync(kFull, push, src) > 0;
+      for (int64_t e = a0 + lane; e < a1; e += 32) push_delta(p, nxt, __ldg(p.out_col + e), up);
+    }
+  }
   __syncwarp();
 }
 
 // phase B on this warp's own queue
 template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
 __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
-                                            int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
+                                            int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt,
+                                            HazardMemo* hm = nullptr) {
   drain_entries<ST, AT, IT, MAT, WARPS>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp], sh.q_press[warp],
-                                        lane, cnt, lmax, mask_nxt, inf_nxt);
+                                        lane, cnt, lmax, mask_nxt, inf_nxt, hm);
 }
 
 // phase A outcome of one tile (pressure already gathered): cheap outcomes
@@ -617,7 +693,8 @@ __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst
 template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
 __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
                                              int lane, int64_t tile, int64_t n, bool valid, int s, float age,
-                                             float pressure, int& qn, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
+                                             float pressure, int& qn, float& lmax, uint32_t* mask_nxt, IT* inf_nxt,
+                                             HazardMemo* hm = nullptr) {
   const bool isS = s == k.edge_from;
   const bool term = valid && sh.term[s] != 0;
   const bool defer = valid && !term && (!isS || pressure > 0.0f);
@@ -647,7 +724,7 @@ __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepCons
   }
   qn += __popc(dm);
   if (qn >= 32) {
-    drain_queue<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt);
+    drain_queue<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt, hm);
     if (lane < qn - 32) {
       sh.q_node[warp][lane] = sh.q_node[warp][32 + lane];
       sh.q_state[warp][lane] = sh.q_state[warp][32 + lane];
@@ -825,43 +902,55 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   constexpr int WARPS = BLOCK / 32;
   __shared__ StepShared<WARPS> sh;
   __shared__ StepConst s_k;
+  __shared__ HazardMemo s_hm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_launch_dependents();
   load_tables<WARPS>(p, sh, tid);  // static model tables: before the dependency wait
+  if (p.entry) memo_init<BLOCK>(s_hm, p, tid);
+  HazardMemo* hmp = p.entry ? &s_hm : nullptr;
   pdl_wait();
   if (tid == 0) {
     s_k = step_const(p, true);
     if (blockIdx.x == 0) commit_step_start(p, s_k);
   }
-  __syncthreads();
-  const StepConst k = s_k;
-  const int cur = (int)(k.step & 1);
-  uint32_t* mask_nxt = p.mask[cur ^ 1];
   const ST* __restrict__ states = reinterpret_cast<const ST*>(p.states);
   const AT* __restrict__ ages = reinterpret_cast<const AT*>(p.ages);
   uint16_t* __restrict__ cnt = p.cnt;
-  uint16_t* __restrict__ pend = reinterpret_cast<uint16_t*>(p.pend[cur]);
   const uint32_t N = (uint32_t)p.n, ntiles = (uint32_t)p.ntiles;
   const uint32_t stride = gridDim.x * WARPS;
   struct In { int s; float age; uint32_t c, d; };
   // arrays are padded to whole 128-node units: every lane loads unconditionally
-  auto load = [&](uint32_t t, In& in) {
+  auto load = [&](uint32_t t, const uint16_t* pend, In& in) {
     const uint32_t n = t * 32u + (uint32_t)lane;
     in.s = (int)states[n];
     in.age = to_f32<AT>(ages[n]);
     in.c = cnt[n];
     in.d = pend[n];
   };
-  float lmax = 0.0f;
-  int qn = 0;
+  // the first two tiles' loads need only the buffer parity, which the host
+  // knows: they overlap thread 0's scalar reads instead of waiting for them
   uint32_t t = blockIdx.x * WARPS + warp;
   In in0{}, in1{};
-  if (t < ntiles) load(t, in0);
-  if (t + stride < ntiles) load(t + stride, in1);
+  if (p.host_parity >= 0) {
+    const uint16_t* pend_h = reinterpret_cast<const uint16_t*>(p.pend[p.host_parity & 1]);
+    if (t < ntiles) load(t, pend_h, in0);
+    if (t + stride < ntiles) load(t + stride, pend_h, in1);
+  }
+  __syncthreads();
+  const StepConst k = s_k;
+  const int cur = (int)(k.step & 1);
+  uint32_t* mask_nxt = p.mask[cur ^ 1];
+  uint16_t* __restrict__ pend = reinterpret_cast<uint16_t*>(p.pend[cur]);
+  if (cur != p.host_parity) {  // no host mirror, or out of step: load now
+    if (t < ntiles) load(t, pend, in0);
+    if (t + stride < ntiles) load(t + stride, pend, in1);
+  }
+  float lmax = 0.0f;
+  int qn = 0;
   for (; t < ntiles; t += stride) {
     const In in = in0;
     in0 = in1;
-    if (t + 2 * stride < ntiles) load(t + 2 * stride, in1);
+    if (t + 2 * stride < ntiles) load(t + 2 * stride, pend, in1);
     const uint32_t n = t * 32u + (uint32_t)lane;
     const bool valid = n < N;
     uint32_t c = in.c;
@@ -875,9 +964,9 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
                                ? (p.ptab_mul ? __fmul_rn((float)c, p.ptab_c) : __ldg(p.ptab + c))
                                : 0.0f;
     tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, (int64_t)t, (int64_t)n, valid, s, in.age, pressure,
-                                            qn, lmax, mask_nxt, nullptr);
+                                            qn, lmax, mask_nxt, nullptr, hmp);
   }
-  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
+  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr, hmp);
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
 
@@ -1427,10 +1516,11 @@ struct fs_engine {
   int* bad_flag = nullptr;
   // CUDA graphs of one batch (index: materialise last step)
   cudaStream_t cap_stream = nullptr;
-  cudaGraphExec_t batch_exec[2][2][3] = {};  // [materialise][scalar slot][step % 3 when exchanging]
+  cudaGraphExec_t batch_exec[2][2][6] = {};  // [materialise][scalar slot][step % 6]: parity and exchange slot are baked in
   bool compaction_ready = false;
   int stream_evict_first = 0;
   // incremental count mode
+  int32_t* entry = nullptr;           // hazard memo: per-node entry step
   bool incr = false;
   uint32_t* peer_pend[2][FS_MAX_PARTITIONS] = {};  // partitioned incremental: every rank's delta arrays
   bool peers_linked = false;
@@ -1496,6 +1586,8 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.pre = use_pre ? e->pre : nullptr;
   p.count_mode = e->count_mode;
   p.stream_evict_first = e->stream_evict_first;
+  p.host_parity = (int)(e->h_step & 1);
+  p.entry = e->entry;
   p.cnt = e->incr ? e->cnt : nullptr;
   p.pend[0] = e->delta[0];
   p.pend[1] = e->delta[1];
@@ -1630,6 +1722,16 @@ int launch_begin_batch(fs_engine* e, cudaStream_t st) {
     else
       k_sync_buffers<float><<<blocks2, 256, 0, st>>>(e->dstate + e->s_cur, (float*)e->b.infectivity[0], (float*)e->b.infectivity[1], n);
   }
+  FS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// hazard memo: every node's cohort unknown, every slot's tag stale
+int reset_memo(fs_engine* e, cudaStream_t st) {
+  if (!e->entry) return 0;
+  const int64_t n = (e->g.num_nodes + 127) / 128 * 128;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
+  k_fill<int32_t><<<std::max(1, blocks), 256, 0, st>>>(e->entry, n, kEntryInvalid);
   FS_CUDA(cudaGetLastError());
   return 0;
 }
@@ -1864,6 +1966,19 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
       e->stream_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sms * socc, (e->ntiles + 15) / 16));
     }
   }
+  {
+    // hazard memo for models with age-dependent holding times
+    bool costly = false;
+    for (int c2 = 0; c2 < m->num_compartments; ++c2) costly |= m->comp[c2].hazard >= FS_HZ_LOGNORMAL;
+    // the memo pays off when a CTA holds many nodes of each age cohort
+    // (large N); at N ~ 1e6 its setup costs more than it saves
+    const char* mv = getenv("FS_MEMO");
+    const bool want = mv ? atoi(mv) != 0 : (e->incr && n >= (int64_t)8 * 1024 * 1024);
+    if (costly && want && !getenv("FS_NO_MEMO")) {
+      TRY(dalloc(&e->entry, (size_t)((n + 127) / 128) * 128));
+      TRY(reset_memo(e, nullptr));
+    }
+  }
   if (getenv("FS_NO_PDL")) e->pdl = false;
   if (getenv("FS_DEBUG_TIMES")) {
     TRY(dalloc(&e->dbg, (size_t)std::max(e->step_grid, e->step_grid_general) * 4 * 16));
@@ -1898,7 +2013,7 @@ void fs_engine_destroy(fs_engine* e) {
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   void* ptrs[] = {e->dstate, e->acc, e->log_clock, e->log_tau, e->log_counts, e->ptab,
                   e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag,
-                  e->cnt, e->delta[0], e->delta[1]};
+                  e->cnt, e->delta[0], e->delta[1], e->entry};
   for (void* q : ptrs) if (q) cudaFree(q);
   delete e;
 }
@@ -1936,7 +2051,7 @@ int fs_engine_run_batch(fs_engine* e, int32_t materialize, void* stream) {
   const int s0 = e->s_cur;
   const int64_t h0 = e->h_step;
   // the exchange's accumulator slot and mask buffer are baked in at capture
-  cudaGraphExec_t& exec = e->batch_exec[materialize ? 1 : 0][s0][e->comm ? (int)(h0 % 3) : 0];
+  cudaGraphExec_t& exec = e->batch_exec[materialize ? 1 : 0][s0][(int)(h0 % 6)];
   if (!exec) {
     cudaGraph_t graph = nullptr;
     FS_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
@@ -2043,6 +2158,10 @@ int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream) {
     rc = recount(e, in->step, st);
     if (rc) return rc;
   }
+  if (in->step != cur.s.step) {  // memo tags and cohorts are relative to the step counter
+    rc = reset_memo(e, st);
+    if (rc) return rc;
+  }
   FS_CUDA(cudaStreamSynchronize(st));
   e->h_step = in->step;
   return 0;
@@ -2101,6 +2220,12 @@ int fs_engine_store_infectivity(fs_engine* e, void* out, void* stream) {
   }
   FS_CUDA(cudaMemcpyAsync(out, e->b.infectivity[cur], (size_t)n * (e->mixed ? 2 : 4), cudaMemcpyDeviceToDevice, st));
   return 0;
+}
+
+int fs_engine_reset_age_memo(fs_engine* e, void* stream) {
+  if (!e) return set_error(FS_EINVAL, "null engine");
+  FS_CUDA(cudaSetDevice(e->device));
+  return reset_memo(e, (cudaStream_t)stream);
 }
 
 int fs_engine_delta_buffers(fs_engine* e, void** out2) {

@@ -385,6 +385,10 @@ class _Engine:
         for dst, src in zip(self.bufs, bufs):
             dst.copy_(src)
         self.set_scalars(sc)
+        self.reset_age_memo()
+
+    def reset_age_memo(self) -> None:
+        _lib.check(self.lib.fs_engine_reset_age_memo(self.handle, self.stream))
 
     def read_log(self, first_step: int, n: int):
         M = self.plan.num_compartments
@@ -552,6 +556,8 @@ class RenewalState:
         if name in ("pressure", "rates"):
             self._ensure_debug_buffers()
         self._t[name].copy_(_device.to_device(_host_cast(arr, dtype), self._dev))
+        if name in ("states", "ages") and self._engine is not None:
+            self._engine.reset_age_memo()  # host-written nodes no longer follow their age cohorts
 
     def _push_host(self) -> None:
         """Upload every downloaded array the caller edited in place."""
@@ -838,6 +844,7 @@ def run_renewal(g, m, cfg: RenewalConfig, seed: int, t_final: float, grid_points
     state = init_renewal_state(g, m, cfg, seed, seed_count, seed_compartment)
     plan = _build_plan(g, m, cfg, state.mixed_precision)
     eng = state._bind(plan, seed, materialize=False)
+    setup = time.perf_counter() - t0
     b = cfg.steps_per_batch
     times = [0.0]
     rows = [state.counts.copy()]
@@ -854,6 +861,6 @@ def run_renewal(g, m, cfg: RenewalConfig, seed: int, t_final: float, grid_points
     t_arr = np.asarray(times)
     steps = min(int(np.searchsorted(t_arr, t_final, side="left")), done)
     rec = make_record(t_arr, np.asarray(rows), m.compartments, g.num_nodes, t_final, grid_points,
-                      extra_summary={"step_count": steps, "wall_clock": wall, "engine": "renewal"})
+                      extra_summary={"step_count": steps, "wall_clock": wall, "engine": "renewal", "setup_s": setup})
     state._unbind()
     return rec
