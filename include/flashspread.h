@@ -292,6 +292,36 @@ int fs_gen_regular(int64_t n, int32_t k, uint64_t seed, int64_t row_lo, int64_t 
  * distinct degree and writes the sorted neighbours to out[k] */
 int fs_gen_regular_row_host(int64_t n, int32_t k, uint64_t seed, int64_t node, int32_t* out);
 
+/* ------------------------------------------------------------------------
+ * Markovian tau-leaping engine (R/markov.py:34-228).
+ * All-exponential models with constant transmission; influence = number of
+ * infectious in-neighbours x the uniform weight, kept by pushes along the
+ * outgoing CSR; tau = min(theta N / sum(rates), p_max / max(rates),
+ * tau_max) with the sum in numpy's pairwise order (bit-identical to
+ * R/markov.py:149-154).  `states` int32[N] and `rates` f64[N] are caller
+ * owned; fs_scalars carries clock / step / seed / counts (tau_next = the tau
+ * of the last step). */
+typedef struct fs_markov_config {  /* R/markov.py:34-46 `MarkovConfig` */
+  double theta, p_max, tau_max;
+  int32_t steps_per_batch;
+  int32_t pad_;
+} fs_markov_config;
+typedef struct fs_markov fs_markov;
+int fs_markov_create(const fs_graph* g, const fs_model* m, const fs_markov_config* c, int32_t* states,
+                     double* rates, const fs_scalars* scal, int device, fs_markov** out);
+void fs_markov_destroy(fs_markov* e);
+/* R/markov.py:143-181 `markov_step` x nsteps (eager) */
+int fs_markov_step(fs_markov* e, int32_t nsteps, void* stream);
+/* steps_per_batch steps as one CUDA-graph replay */
+int fs_markov_run_batch(fs_markov* e, void* stream);
+int fs_markov_get_scalars(fs_markov* e, fs_scalars* out, void* stream);
+/* write scalars (and the seed); counts are rebuilt from the states */
+int fs_markov_set_scalars(fs_markov* e, const fs_scalars* in, void* stream);
+int fs_markov_read_log(fs_markov* e, int64_t first_step, int32_t n, double* clocks, double* taus,
+                       int64_t* counts, void* stream);
+/* R/markov.py:68-81 `influence_gather` of the current states (host f64[N]) */
+int fs_markov_influence(fs_markov* e, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

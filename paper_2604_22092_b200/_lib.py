@@ -139,6 +139,11 @@ class FsPartition(ctypes.Structure):
     ]
 
 
+class FsMarkovConfig(ctypes.Structure):
+    _fields_ = [("theta", _c_f64), ("p_max", _c_f64), ("tau_max", _c_f64), ("steps_per_batch", _c_i32),
+                ("pad_", _c_i32)]
+
+
 _SIGNATURES = {
     "fs_abi_version": (_c_i32, []),
     "fs_last_error": (ctypes.c_char_p, []),
@@ -161,6 +166,15 @@ _SIGNATURES = {
     "fs_comm_init": (_c_i32, [_c_i32, _c_i32, _vp, _c_i32, ctypes.POINTER(_vp)]),
     "fs_comm_destroy": (None, [_vp]),
     "fs_engine_destroy": (None, [_vp]),
+    "fs_markov_create": (_c_i32, [ctypes.POINTER(FsGraph), ctypes.POINTER(FsModel), ctypes.POINTER(FsMarkovConfig),
+                                  _vp, _vp, ctypes.POINTER(FsScalars), _c_i32, ctypes.POINTER(_vp)]),
+    "fs_markov_destroy": (None, [_vp]),
+    "fs_markov_step": (_c_i32, [_vp, _c_i32, _vp]),
+    "fs_markov_run_batch": (_c_i32, [_vp, _vp]),
+    "fs_markov_get_scalars": (_c_i32, [_vp, ctypes.POINTER(FsScalars), _vp]),
+    "fs_markov_set_scalars": (_c_i32, [_vp, ctypes.POINTER(FsScalars), _vp]),
+    "fs_markov_read_log": (_c_i32, [_vp, _c_i64, _c_i32, _vp, _vp, _vp, _vp]),
+    "fs_markov_influence": (_c_i32, [_vp, _vp, _vp]),
     "fs_engine_uses_count_gather": (_c_i32, [_vp]),
     "fs_engine_current_buffer": (_c_i32, [_vp, _vp]),
     "fs_engine_begin_batch": (_c_i32, [_vp, _vp]),
