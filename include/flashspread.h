@@ -319,6 +319,9 @@ int fs_markov_get_scalars(fs_markov* e, fs_scalars* out, void* stream);
 int fs_markov_set_scalars(fs_markov* e, const fs_scalars* in, void* stream);
 int fs_markov_read_log(fs_markov* e, int64_t first_step, int32_t n, double* clocks, double* taus,
                        int64_t* counts, void* stream);
+/* recompute rates[] from the current states and influence (the state.rates
+ * the reference holds after a step, R/markov.py:178) */
+int fs_markov_refresh_rates(fs_markov* e, void* stream);
 /* R/markov.py:68-81 `influence_gather` of the current states (host f64[N]) */
 int fs_markov_influence(fs_markov* e, double* out, void* stream);
 

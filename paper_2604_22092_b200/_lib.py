@@ -175,6 +175,7 @@ _SIGNATURES = {
     "fs_markov_set_scalars": (_c_i32, [_vp, ctypes.POINTER(FsScalars), _vp]),
     "fs_markov_read_log": (_c_i32, [_vp, _c_i64, _c_i32, _vp, _vp, _vp, _vp]),
     "fs_markov_influence": (_c_i32, [_vp, _vp, _vp]),
+    "fs_markov_refresh_rates": (_c_i32, [_vp, _vp]),
     "fs_engine_uses_count_gather": (_c_i32, [_vp]),
     "fs_engine_current_buffer": (_c_i32, [_vp, _vp]),
     "fs_engine_begin_batch": (_c_i32, [_vp, _vp]),

@@ -552,6 +552,16 @@ int fs_markov_read_log(fs_markov* e, int64_t first_step, int32_t n, double* cloc
   return 0;
 }
 
+int fs_markov_refresh_rates(fs_markov* e, void* stream) {
+  // rates of the current states and influence (what R/markov.py:178 leaves in
+  // state.rates after a step); the next step recomputes the same values
+  if (!e) return set_error(FS_EINVAL, "null engine");
+  MK_CUDA(cudaSetDevice(e->device));
+  k_mk_rates<<<e->grid, 256, 0, (cudaStream_t)stream>>>(e->p);
+  MK_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int fs_markov_influence(fs_markov* e, double* out, void* stream) {
   // influence = count * w (R/markov.py:68-81 for uniform weights), after the
   // pending pushes are folded: computed from the current states

@@ -152,6 +152,9 @@ class MarkovState:
 
     @property
     def rates(self) -> np.ndarray:
+        self._push_host()
+        if self._eng is not None:
+            _lib.check(self._lib.fs_markov_refresh_rates(self._eng, self._stream))
         return self._rates.cpu().numpy()
 
     @rates.setter

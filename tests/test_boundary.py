@@ -35,7 +35,8 @@ def test_library_loads_and_exports_every_declared_symbol():
 
 def test_ctypes_layouts_match_c(tmp_path):
     src = tmp_path / "layout.c"
-    structs = ["fs_graph", "fs_compartment", "fs_model", "fs_config", "fs_scalars", "fs_state_buffers", "fs_partition"]
+    structs = ["fs_graph", "fs_compartment", "fs_model", "fs_config", "fs_scalars", "fs_state_buffers", "fs_partition",
+               "fs_markov_config"]
     body = "\n".join(f'printf("{s} %zu\\n", sizeof({s}));' for s in structs)
     offs = {
         "fs_model": ["beta", "shedding", "shed_mu", "shed_peak", "comp"],
@@ -43,6 +44,7 @@ def test_ctypes_layouts_match_c(tmp_path):
         "fs_graph": ["row_offsets", "weights_dtype", "uniform_weight", "d_max"],
         "fs_config": ["steps_per_batch", "count_gather"],
         "fs_partition": ["num_nodes_global", "mask_segment_words", "rank", "world", "comm"],
+        "fs_markov_config": ["p_max", "tau_max", "steps_per_batch"],
     }
     for s, fields in offs.items():
         for f in fields:
@@ -53,7 +55,7 @@ def test_ctypes_layouts_match_c(tmp_path):
     got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
     cls = {"fs_graph": _lib.FsGraph, "fs_compartment": _lib.FsCompartment, "fs_model": _lib.FsModel,
            "fs_config": _lib.FsConfig, "fs_scalars": _lib.FsScalars, "fs_state_buffers": _lib.FsStateBuffers,
-           "fs_partition": _lib.FsPartition}
+           "fs_partition": _lib.FsPartition, "fs_markov_config": _lib.FsMarkovConfig}
     for s, c in cls.items():
         assert int(got[s]) == ctypes.sizeof(c), s
     for key, v in got.items():
