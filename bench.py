@@ -47,6 +47,8 @@ WORKLOADS = {
     "c5": dict(desc="C5: SEIR log-normal, uniform-degree k=10, N=1e9, node-partitioned across the GPUs "
                     "(NCCL mask all-gather + max/count all-reduce per step)",
                kind="regular_dev", n=1_000_000_000, k=10, model="seir", cpu_n=10_000_000, t_final=10.0),
+    "m2": dict(desc="M2 (SURVEY §8f row 3): Markovian SIR (beta 0.25, gamma 0.15), uniform-degree k=10, N=1e6",
+               kind="fixed", n=1_000_000, k=10, model="sir_markov", engine="markov"),
     "c4": dict(desc="C4: SEIR log-normal, uniform-degree k=10, N=1e8, bf16/fp16 mixed-precision storage",
                kind="regular_dev", n=100_000_000, k=10, model="seir", mixed=True, cpu_n=10_000_000),
 }
@@ -70,7 +72,12 @@ def build_inputs(w):
         g = fs.gen_fixed_degree_device(w["n"], w["k"], seed=GRAPH_SEED)
     else:
         g = fs.gen_barabasi_albert(w["n"], w["k"], seed=GRAPH_SEED)
-    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0) if w["model"] == "seir" else fs.seir_weibull_erlang(0.25)
+    if w["model"] == "seir":
+        m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    elif w["model"] == "sir_markov":
+        m = fs.sir_model(0.25, 0.15)
+    else:
+        m = fs.seir_weibull_erlang(0.25)
     return g, m
 
 
@@ -190,6 +197,9 @@ def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     w = WORKLOADS[args.workload]
+    if w.get("engine") == "markov":
+        print(json.dumps({"impl": "reference", "unavailable": "the CPU oracle port restates the renewal path only"}))
+        return
     if "cpu_n" in w:  # bounded sample of a workload too large for host RAM
         import paper_2604_22092_b200 as fs
 
@@ -208,6 +218,65 @@ def run_reference(args, rank: int, world: int) -> None:
                    "sim_seed": SIM_SEED},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "G-NUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def run_markov_bench(args, w) -> None:
+    """The Markovian engine (R/markov.py) on the same graph family: each of
+    the K steps (four kernels) timed alone after an L2 flush; e2e =
+    run_markov to t_final from the host graph.  No CPU baseline: the oracle
+    port restates the renewal path only."""
+    import torch
+
+    import paper_2604_22092_b200 as fs
+    from paper_2604_22092_b200 import _lib
+    from paper_2604_22092_b200.renewal import _pick_seed_nodes
+
+    g, m = build_inputs(w)
+    cfg = fs.MarkovConfig()
+    n = g.num_nodes
+    picked = _pick_seed_nodes(n, SIM_SEED, 10, torch.device("cuda")).cpu().numpy()
+    st = fs.init_markov_state(g, m, picked)
+    eng = st._bind(cfg, SIM_SEED)
+    lib = st._lib
+    _lib.check(lib.fs_markov_step(eng, args.warmup, st._stream))
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    flush_rd = torch.ones(128 << 20, dtype=torch.int32, device="cuda")
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            flush_rd.max()
+            starts[k].record()
+            _lib.check(lib.fs_markov_step(eng, 1, st._stream))
+            ends[k].record()
+        torch.cuda.synchronize()
+    total_ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    st._unbind()
+    e2e = None
+    if not args.no_e2e:
+        g.__dict__.pop("_fs_device_cache", None)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rec = fs.run_markov(g, m, cfg, SIM_SEED, 50.0)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        steps_run = rec.summary["step_count"]
+        e2e = {"value": n * steps_run / wall / 1e9, "unit": "G-NUPS",
+               "h2d_bytes_per_step": (g.row_offsets.nbytes + g.col_indices.nbytes) / steps_run,
+               "d2h_bytes_per_step": 8 * (1 + m.num_compartments), "steps": steps_run, "wall_s": wall,
+               "what": "run_markov(t_final=50) from a host CsrGraph: CSR H2D + init + CUDA-graph batches + log D2H"}
+    ms = total_ms / args.steps
+    print(json.dumps({
+        "metric": "Giga-NUPS (node updates/s)", "value": n / (ms / 1e3) / 1e9, "unit": "G-NUPS", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 rates, integer influence",
+        "data": "synthetic (reference generators, graph seed 1, sim seed 7)",
+        "config": {"workload": w["desc"], "n": n, "edges": g.num_edges, "engine": "markov (4 kernels per step)",
+                   "l2": "flushed before every timed step (512 MiB write + 512 MiB read of another buffer)"},
+        "roofline": None, "gpu_launches": 4 * args.steps, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": None,
     }))
 
 
@@ -334,6 +403,9 @@ def main() -> None:
     if world > 1:
         run_partitioned(args, WORKLOADS[args.workload], rank, world, local)
         dist.destroy_process_group()
+        return
+    if WORKLOADS[args.workload].get("engine") == "markov":
+        run_markov_bench(args, WORKLOADS[args.workload])
         return
 
     w = WORKLOADS[args.workload]
