@@ -376,6 +376,8 @@ def main() -> None:
                     help="default: c2 on one GPU (the headline config), c5 (N=1e9 partitioned) on several")
     ap.add_argument("--cpu-steps", type=int, default=30)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="use the node-partitioned (NCCL) path even on one GPU (checks the multi-GPU code path)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -400,7 +402,11 @@ def main() -> None:
     import paper_2604_22092_b200 as fs
     from paper_2604_22092_b200 import renewal as R
 
-    if world > 1:
+    if world > 1 or args.partitioned:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            dist.init_process_group("nccl", rank=0, world_size=1)
         run_partitioned(args, WORKLOADS[args.workload], rank, world, local)
         dist.destroy_process_group()
         return

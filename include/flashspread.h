@@ -206,6 +206,11 @@ int fs_engines_exchange_local(fs_engine* const* engines, int32_t count, void* st
  * the other engines' pointers directly (one device) or peer mappings from
  * fs_ipc_open_handle (one process per GPU). */
 int fs_engine_delta_buffers(fs_engine* e, void** out2);
+/* host-side step exchange (partitioned engines without a communicator): the
+ * last step's accumulator — 16 count deltas and the max-rate bits, 17 u64 —
+ * out to the host and, reduced over ranks, back before the next step */
+int fs_engine_acc_get(fs_engine* e, uint64_t* out17, void* stream);
+int fs_engine_acc_set(fs_engine* e, const uint64_t* in17, void* stream);
 int fs_engine_set_peer_deltas(fs_engine* e, void* const* ptrs);
 int fs_ipc_get_handle(void* dptr, uint8_t* out, int32_t len);
 int fs_ipc_open_handle(const uint8_t* handle, int32_t device, void** out);

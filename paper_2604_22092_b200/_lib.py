@@ -157,6 +157,8 @@ _SIGNATURES = {
                                               ctypes.POINTER(_vp)]),
     "fs_engines_exchange_local": (_c_i32, [_vp, _c_i32, _vp]),
     "fs_engine_delta_buffers": (_c_i32, [_vp, _vp]),
+    "fs_engine_acc_get": (_c_i32, [_vp, _vp, _vp]),
+    "fs_engine_acc_set": (_c_i32, [_vp, _vp, _vp]),
     "fs_engine_reset_age_memo": (_c_i32, [_vp, _vp]),
     "fs_engine_set_peer_deltas": (_c_i32, [_vp, _vp]),
     "fs_ipc_get_handle": (_c_i32, [_vp, _vp, _c_i32]),

@@ -2228,6 +2228,33 @@ int fs_engine_reset_age_memo(fs_engine* e, void* stream) {
   return reset_memo(e, (cudaStream_t)stream);
 }
 
+int fs_engine_acc_get(fs_engine* e, uint64_t* out17, void* stream) {
+  if (!e || !out17) return set_error(FS_EINVAL, "null argument");
+  if (e->h_step < 1) return set_error(FS_ESTATE, "no step to exchange");
+  FS_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const StepAcc* A = e->acc + (e->h_step - 1) % 3;
+  unsigned mb = 0;
+  FS_CUDA(cudaMemcpyAsync(out17, &A->d[0], FS_MAX_COMPARTMENTS * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  FS_CUDA(cudaMemcpyAsync(&mb, &A->max_bits, sizeof mb, cudaMemcpyDeviceToHost, st));
+  FS_CUDA(cudaStreamSynchronize(st));
+  out17[FS_MAX_COMPARTMENTS] = mb;
+  return 0;
+}
+
+int fs_engine_acc_set(fs_engine* e, const uint64_t* in17, void* stream) {
+  if (!e || !in17) return set_error(FS_EINVAL, "null argument");
+  if (e->h_step < 1) return set_error(FS_ESTATE, "no step to exchange");
+  FS_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  StepAcc* A = e->acc + (e->h_step - 1) % 3;
+  const unsigned mb = (unsigned)in17[FS_MAX_COMPARTMENTS];
+  FS_CUDA(cudaMemcpyAsync(&A->d[0], in17, FS_MAX_COMPARTMENTS * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  FS_CUDA(cudaMemcpyAsync(&A->max_bits, &mb, sizeof mb, cudaMemcpyHostToDevice, st));
+  FS_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
 int fs_engine_delta_buffers(fs_engine* e, void** out2) {
   if (!e || !out2) return set_error(FS_EINVAL, "null argument");
   if (!e->incr) return set_error(FS_ESTATE, "engine does not use incremental counts");

@@ -262,30 +262,40 @@ class DistributedRun:
     torch.distributed group used once, to broadcast the NCCL unique id."""
 
     def __init__(self, graph_local, m, cfg: RenewalConfig, seed: int, plan: PartitionPlan, rank: int,
-                 seed_count=None, pg=None):
+                 seed_count=None, pg=None, transport: str = "nccl"):
+        """transport "nccl": the per-step all-reduce is an NCCL group inside
+        the engine's launches (and CUDA graphs); "host": eager steps only, the
+        accumulator is all-reduced through `pg` (any torch.distributed
+        backend) — lets several processes share one GPU in tests."""
         import torch.distributed as dist
 
         dev = _device.device()
         lib = _lib.load()
         self.plan, self.cfg, self.M, self.rank = plan, cfg, m.num_compartments, rank
-        buf = (ctypes.c_uint8 * 256)()
-        if rank == 0:
-            nb = _lib.check(lib.fs_comm_unique_id(buf, 256))
-            payload = [bytes(buf)[:nb]]
-        else:
-            payload = [None]
-        if plan.world > 1:
-            dist.broadcast_object_list(payload, src=0, group=pg)
-        idb = (ctypes.c_uint8 * 256).from_buffer_copy(payload[0].ljust(256, b"\0"))
+        self.transport, self.pg = transport, pg
         comm = ctypes.c_void_p()
-        _lib.check(lib.fs_comm_init(plan.world, rank, idb, dev.index, ctypes.byref(comm)))
+        if transport == "nccl":
+            buf = (ctypes.c_uint8 * 256)()
+            if rank == 0:
+                nb = _lib.check(lib.fs_comm_unique_id(buf, 256))
+                payload = [bytes(buf)[:nb]]
+            else:
+                payload = [None]
+            if plan.world > 1:
+                dist.broadcast_object_list(payload, src=0, group=pg)
+            idb = (ctypes.c_uint8 * 256).from_buffer_copy(payload[0].ljust(256, b"\0"))
+            _lib.check(lib.fs_comm_init(plan.world, rank, idb, dev.index, ctypes.byref(comm)))
+        elif transport != "host":
+            raise ValueError("transport must be 'nccl' or 'host'")
         self.comm = comm
         ids = _seed_ids(m, plan.num_nodes, seed, seed_count, dev)
         mask0 = _initial_mask(plan, ids, m.edge_to == m.infectious, dev)
         self.masks = [mask0, mask0.clone()]
-        self.part = _Partition(graph_local, m, cfg, seed, plan, rank, ids, self.masks, comm.value, dev)
+        self.part = _Partition(graph_local, m, cfg, seed, plan, rank, ids, self.masks, comm.value or None, dev)
         self.steps = 0
         self._opened = []
+        if transport == "host" and plan.world > 1 and not self.part.incremental:
+            raise InvalidConfigError("the host transport needs the incremental-count mode (no mask exchange)")
         if plan.world > 1 and self.part.incremental:
             self._link_peers_ipc(dev, pg)
 
@@ -318,13 +328,33 @@ class DistributedRun:
 
     def run_batch(self):
         first = self.steps
-        self.part.run_batch()
-        self.steps += self.cfg.steps_per_batch
+        if self.transport == "host":
+            self.step(self.cfg.steps_per_batch)
+        else:
+            self.part.run_batch()
+            self.steps += self.cfg.steps_per_batch
         return self.part.read_log(first, self.cfg.steps_per_batch)
 
     def step(self, nsteps: int = 1) -> None:
-        self.part.step(nsteps)
-        self.steps += nsteps
+        if self.transport == "nccl":
+            self.part.step(nsteps)
+            self.steps += nsteps
+            return
+        import torch.distributed as dist
+
+        lib = _lib.load()
+        acc = np.zeros(17, dtype=np.uint64)
+        for _ in range(nsteps):
+            self.part.step(1)
+            _lib.check(lib.fs_engine_acc_get(self.part.handle, acc.ctypes.data, self.part.stream))
+            d = torch.from_numpy(acc[:16].view(np.int64).copy())
+            mx = torch.tensor([int(acc[16])], dtype=torch.int64)
+            dist.all_reduce(d, op=dist.ReduceOp.SUM, group=self.pg)  # two's complement sums
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=self.pg)  # rates >= 0: bits order like values
+            acc[:16] = d.numpy().view(np.uint64)
+            acc[16] = np.uint64(mx.item())
+            _lib.check(lib.fs_engine_acc_set(self.part.handle, acc.ctypes.data, self.part.stream))
+            self.steps += 1
 
     def close(self) -> None:
         lib = _lib.load()

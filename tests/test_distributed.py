@@ -160,3 +160,55 @@ def test_nccl_world1_matches_single_engine():
     p.join(timeout=60)
     assert p.exitcode == 0
     assert same and s1 == s2
+
+
+def _ipc_worker(rank: int, world: int, port: int, steps: int, out_q) -> None:
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2604_22092_b200.distributed import DistributedRun
+
+    n = 30_000
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    plan = partition_plan(n, world)
+    lo, hi = plan.ranges[rank]
+    g = fs.gen_fixed_degree_device(n, 10, seed=2, row_lo=lo, row_hi=hi)
+    run = DistributedRun(g, m, fs.RenewalConfig(), 7, plan, rank, transport="host")
+    assert run.part.incremental
+    run.step(steps)
+    s = run.part.scalars()
+    out_q.put((rank, run.part.states.cpu().numpy(), run.part.ages.cpu().numpy(),
+               np.array(s.counts[:4], dtype=np.int64), s.clock))
+    dist.barrier()
+    run.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_processes_push_through_cuda_ipc():
+    """Two ranks as two processes on the one GPU: the step kernels push into
+    each other's pending-delta arrays through CUDA IPC mappings (the
+    multi-GPU path's transport, minus NVLink), the accumulator is all-reduced
+    over gloo; the result equals the single-engine run bit for bit."""
+    steps, world = 60, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, rest) for r, *rest in (q.get(timeout=600) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    n = 30_000
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    cfg = fs.RenewalConfig()
+    whole = fs.gen_fixed_degree_device(n, 10, seed=2)
+    st = fs.init_renewal_state(whole, m, cfg, 7)
+    for _ in range(steps):
+        fs.renewal_step(st, whole, m, cfg, 7)
+    assert np.array_equal(np.concatenate([res[r][0] for r in range(world)]), st.states)
+    assert np.array_equal(np.concatenate([res[r][1] for r in range(world)]).view(np.uint32), st.ages.view(np.uint32))
+    for r in range(world):
+        assert np.array_equal(res[r][2], st.counts) and res[r][3] == st.clock
