@@ -478,29 +478,36 @@ def main() -> None:
     e2e = None
     if not args.no_e2e:
         t_final = float(w.get("t_final", 50.0))
-        torch.cuda.synchronize()
+        reps = 1 if device_graph else 3  # host graphs: median of 3 end-to-end runs (host jitter)
         if device_graph:
-            del g, st, eng, plan, snap, snap0
-            torch.cuda.empty_cache()
-            t0 = time.perf_counter()
-            g = fs.gen_fixed_degree_device(w["n"], w["k"], seed=GRAPH_SEED)
-            h2d = 0
-            src = f"a graph generated on the device (fs_gen_regular, inside the timed region)"
-        else:
-            g.__dict__.pop("_fs_device_cache", None)
-            t0 = time.perf_counter()
-            h2d = g.row_offsets.nbytes + g.col_indices.nbytes
-            src = "a host CsrGraph (CSR H2D inside the timed region)"
-        rec = fs.run_renewal(g, m, cfg, SIM_SEED, t_final)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
+            del st, eng, plan, snap, snap0
+        walls, setups = [], []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            if device_graph:
+                del g
+                torch.cuda.empty_cache()
+                t0 = time.perf_counter()
+                g = fs.gen_fixed_degree_device(w["n"], w["k"], seed=GRAPH_SEED)
+                h2d = 0
+                src = "a graph generated on the device (fs_gen_regular, inside the timed region)"
+            else:
+                g.__dict__.pop("_fs_device_cache", None)
+                t0 = time.perf_counter()
+                h2d = g.row_offsets.nbytes + g.col_indices.nbytes
+                src = "a host CsrGraph (CSR H2D inside the timed region)"
+            rec = fs.run_renewal(g, m, cfg, SIM_SEED, t_final)
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)
+            setups.append(rec.summary.get("setup_s"))
+        wall = statistics.median(walls)
         steps_run = int(np.ceil(rec.summary["step_count"] / cfg.steps_per_batch) * cfg.steps_per_batch)
         d2h = 8 * (2 + m.num_compartments) * steps_run
         e2e = {"value": n * steps_run / wall / 1e9, "unit": "G-NUPS", "h2d_bytes_per_step": h2d / steps_run,
-               "d2h_bytes_per_step": d2h / steps_run, "steps": steps_run, "wall_s": wall,
-               "setup_s": rec.summary.get("setup_s"),
+               "d2h_bytes_per_step": d2h / steps_run, "steps": steps_run, "wall_s": wall, "walls_s": walls,
+               "setup_s": setups,
                "what": f"run_renewal(t_final={t_final}) from {src}: init + {steps_run} steps in "
-                       f"CUDA-graph batches + per-batch log D2H + record",
+                       f"CUDA-graph batches + per-batch log D2H + record; median of {reps} runs",
                "final_R": rec.summary["final_R"], "peak_I": rec.summary["peak_I"]}
 
     pk = peaks()

@@ -199,7 +199,8 @@ _SIGNATURES = {
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
-LIB_PATH = Path(__file__).resolve().parent / "libflashspread_b200.so"
+# FS_LIB_PATH selects another build of the same ABI (A/B measurements only)
+LIB_PATH = Path(os.environ.get("FS_LIB_PATH") or Path(__file__).resolve().parent / "libflashspread_b200.so")
 _lib = None
 
 
