@@ -290,7 +290,7 @@ struct fs_engine {
   bool incr = false;
   uint32_t* peer_pend[2][FS_MAX_PARTITIONS] = {};  // partitioned incremental: every rank's delta arrays
   bool peers_linked = false;
-  bool stream = false;         // k_step_stream fast path of the incremental mode
+  bool stream = false;         // k_step_incr fast path of the incremental mode
   StepFn stream_fn[2] = {nullptr, nullptr};
   int stream_grid = 0;
   uint16_t* cnt = nullptr;

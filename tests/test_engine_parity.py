@@ -280,3 +280,22 @@ def test_run_renewal_record_matches_reference():
     s = z["summary"]
     assert (rec.summary["peak_I"], rec.summary["peak_I_time"], rec.summary["final_R"], rec.summary["step_count"]) == (
         s[0], s[1], s[2], int(s[3]))
+
+
+@pytest.mark.parametrize("env", [
+    {"FS_MEMO": "1"},                        # age-cohort hazard memo (default only at N >= 8M)
+    {"FS_NO_STREAM": "1"},                   # incremental counts in the general kernel
+    {"FS_NO_PDL": "1", "FS_MEMO": "1"},
+])
+@pytest.mark.parametrize("name", ["c1", "c1_mixed", "ba_merge", "sir"])
+def test_engine_variants_bit_exact(name, env, monkeypatch):
+    """Kernel variants the engine selects by size or switch (read when an
+    engine is created) against the reference goldens, stepwise and replayed."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    st, log, cps, ref = run_engine_case(name)
+    assert_matches(st, log, cps, ref)
+    st, log, _, ref = run_engine_case(name, batches_via_graph=True)
+    assert np.array_equal(log["counts"], ref["counts"])
+    assert np.array_equal(st.states.astype(np.int32), ref["states"])
+    assert np.array_equal(st.ages.astype(np.float32), ref["ages"])
