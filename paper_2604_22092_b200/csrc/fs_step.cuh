@@ -661,7 +661,7 @@ __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst
 // now, possible transitions appended to the warp queue (drained at 32)
 template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
 __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
-                                             int lane, int64_t tile, int64_t n, bool valid, int s, float age,
+                                             int lane, uint32_t tile, uint32_t n, bool valid, int s, float age,
                                              float pressure, int& qn, float& lmax, uint32_t* mask_nxt, IT* inf_nxt,
                                              HazardMemo* hm = nullptr) {
   const bool isS = s == k.edge_from;
@@ -848,7 +848,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
         }
       }
     }
-    tile_outcome<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, tile, n, valid, in.s, in.age, pressure, qn, lmax,
+    tile_outcome<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, (uint32_t)tile, (uint32_t)n, valid, in.s, in.age, pressure, qn, lmax,
                                          mask_nxt, inf_nxt);
   }
   if (qn > 0) drain_queue<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, inf_nxt);
@@ -932,7 +932,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     const float pressure = (valid && (s == k.edge_from || MAT))
                                ? (p.ptab_mul ? __fmul_rn((float)c, p.ptab_c) : __ldg(p.ptab + c))
                                : 0.0f;
-    tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, (int64_t)t, (int64_t)n, valid, s, in.age, pressure,
+    tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure,
                                             qn, lmax, mask_nxt, nullptr, hmp);
   }
   if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr, hmp);
@@ -1102,7 +1102,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
     __syncwarp();
     // the slot is consumed: refill it with tile t + slots
     if (t + L.slots < t1) issue_cols(t + L.slots, sl);
-    tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure, qn, lmax,
+    tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, (uint32_t)t, (uint32_t)n, valid, s, in.age, pressure, qn, lmax,
                                             mask_nxt, nullptr);
     sl = (sl + 1 == L.slots) ? 0 : sl + 1;
   }
