@@ -223,7 +223,7 @@ def run_reference(args, rank: int, world: int) -> None:
 
 def run_markov_bench(args, w) -> None:
     """The Markovian engine (R/markov.py) on the same graph family: each of
-    the K steps (four kernels) timed alone after an L2 flush; e2e =
+    the K steps (two kernels) timed alone after an L2 flush; e2e =
     run_markov to t_final from the host graph.  No CPU baseline: the oracle
     port restates the renewal path only."""
     import torch
@@ -274,9 +274,9 @@ def run_markov_bench(args, w) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64 rates, integer influence",
         "data": "synthetic (reference generators, graph seed 1, sim seed 7)",
-        "config": {"workload": w["desc"], "n": n, "edges": g.num_edges, "engine": "markov (4 kernels per step)",
+        "config": {"workload": w["desc"], "n": n, "edges": g.num_edges, "engine": "markov (2 kernels per step)",
                    "l2": "flushed before every timed step (512 MiB write + 512 MiB read of another buffer)"},
-        "roofline": None, "gpu_launches": 4 * args.steps, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": None,
+        "roofline": None, "gpu_launches": 2 * args.steps, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": None,
     }))
 
 

@@ -1,17 +1,16 @@
 // fs_markov.cu — the Markovian tau-leaping engine (R/markov.py) on sm_100a:
 // SURVEY.md §8f row 3, the paper's companion engine.
 //
-// One reference markov_step (R/markov.py:143-181) is four launches, captured
+// One reference markov_step (R/markov.py:143-181) is two launches, captured
 // in a CUDA graph per batch:
-//   k_mk_rates   fold the previous step's pushes into the per-node
+//   k_mk_sum     fold the previous step's pushes into the per-node
 //                infectious in-neighbour counts, rate = beta * count * w (S)
-//                or the exponential holding rate, f64 rates[N], block max
-//                into a u64 atomicMax (rates >= 0: bits order like values);
-//   k_mk_leaves  the leaves of numpy's pairwise summation of rates[] (blocks
-//                of <= 128 with 8 interleaved accumulators), so the total
-//                rate is bit-identical to the reference's state.rates.sum();
-//   k_mk_tree    one CTA: the pairwise tree above the leaves, level by level,
-//                then tau = min(theta N / total, p_max / max, tau_max)
+//                or the exponential holding rate, f64 rates[N], max by u64
+//                atomicMax (rates >= 0: bits order like values), and their
+//                sum in numpy's pairwise order (leaves of <= 128 with 8
+//                interleaved accumulators, then the tree), bit-identical to
+//                the reference's state.rates.sum(); the last CTA sets
+//                tau = min(theta N / total, p_max / max, tau_max)
 //                (R/markov.py:149-154) and the clock;
 //   k_mk_fire    u < -expm1(-rate * tau) on the reference's uniforms, state
 //                transitions, count deltas (last-CTA fold into the scalars
@@ -30,6 +29,8 @@
 namespace fs {
 
 constexpr uint32_t kMkBias = 0x8000u;  // pending delta d stored as d + 0x8000
+constexpr int kMkLeafBlock = 32;       // leaves summed per CTA of k_mk_leaves (<= 32 * 128 rates)
+constexpr int kMkLvl = 8;              // max height of a block-local subtree (32 leaves: 6)
 
 struct MkScalars {
   double clock;
@@ -38,8 +39,8 @@ struct MkScalars {
   unsigned long long max_bits;  // max rate (f64 bits) of the current rates
   int64_t counts[FS_MAX_COMPARTMENTS];
   unsigned long long delta[FS_MAX_COMPARTMENTS];  // this step's count deltas (two's complement)
-  unsigned int ticket;
-  int pad_;
+  unsigned int ticket;      // k_mk_fire's last-CTA election
+  unsigned int sum_ticket;  // k_mk_sum's
 };
 
 struct MkParams {
@@ -63,6 +64,13 @@ struct MkParams {
   const int32_t* level_end; // prefix ends of each level in the internal list
   int nlevels;
   int root;
+  // block-local part of the tree: leaf blocks of kMkLeafBlock leaves; the
+  // internal nodes whose leaves all fall in one block, per block and level
+  const int32_t* loc_l;
+  const int32_t* loc_r;
+  const int32_t* loc_out;
+  const int32_t* blk_lvl;   // [nblocks][kMkLvl + 1] prefix offsets into loc_*, by level 1..kMkLvl
+  int nblocks;
   double* log_clock;
   double* log_tau;
   int64_t* log_counts;
@@ -106,54 +114,106 @@ __global__ void __launch_bounds__(256) k_mk_rates(const MkParams p) {
   if ((threadIdx.x & 31) == 0 && mx) atomicMax(&p.S->max_bits, mx);
 }
 
-// numpy's pairwise_sum leaf (n <= 128): 8 interleaved accumulators, then
-// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the remainder in order;
-// n < 8: a plain running sum from 0
-__device__ double np_leaf_sum(const double* a, int n) {
-  if (n < 8) {
-    double s = 0.0;
-    for (int i = 0; i < n; ++i) s = __dadd_rn(s, a[i]);
-    return s;
+// One launch for the rates and their pairwise sum.  CTA b owns the block
+// of kMkLeafBlock consecutive leaves of numpy's pairwise summation, i.e. a
+// contiguous run of <= 4096 nodes: it folds their pending pushes, computes
+// their f64 rates (written out for k_mk_fire, staged in shared memory),
+// sums each leaf with 8 threads — one per interleaved accumulator, exactly
+// numpy's order — and folds the internal nodes local to the block; the last
+// CTA to finish folds the cross-block top of the tree level by level and
+// sets tau = min(theta N / total, p_max / max, tau_max) and the clock.
+__global__ void __launch_bounds__(256) k_mk_sum(const MkParams p) {
+  __shared__ double a[kMkLeafBlock * 128];
+  __shared__ double racc[kMkLeafBlock][8];
+  __shared__ bool last;
+  const int b = blockIdx.x, t = threadIdx.x;
+  MkScalars* S = p.S;
+  const int64_t L0 = (int64_t)b * kMkLeafBlock, L1 = min(L0 + kMkLeafBlock, p.nleaf);
+  const int64_t lo = p.leaf_lo[L0];
+  const int64_t hi = p.leaf_lo[L1 - 1] + p.leaf_len[L1 - 1];
+  uint16_t* pend = reinterpret_cast<uint16_t*>(p.pend[(int)(S->step & 1)]);
+  unsigned long long mx = 0ull;
+  for (int64_t i = t; i < hi - lo; i += blockDim.x) {
+    const int64_t v = lo + i;
+    uint32_t c = p.cnt[v];
+    const uint32_t d = pend[v];
+    if (d != kMkBias) {
+      c = c + d - kMkBias;
+      p.cnt[v] = (uint16_t)c;
+      pend[v] = (uint16_t)kMkBias;
+    }
+    const double r = mk_rate(p, p.states[v], c);
+    p.rates[v] = r;
+    a[i] = r;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(r);
+    mx = bits > mx ? bits : mx;
   }
-  double r[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = a[j];
-  int i = 8;
-  for (; i < n - (n % 8); i += 8)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-  return res;
-}
-
-__global__ void __launch_bounds__(256) k_mk_leaves(const MkParams p) {
-  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < p.nleaf; l += (int64_t)gridDim.x * blockDim.x)
-    p.leaf_val[l] = np_leaf_sum(p.rates + p.leaf_lo[l], p.leaf_len[l]);
-}
-
-__global__ void __launch_bounds__(1024) k_mk_tree(const MkParams p) {
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = w > mx ? w : mx;
+  }
+  if ((t & 31) == 0 && mx) atomicMax(&S->max_bits, mx);
+  __syncthreads();
+  const int li = t >> 3, j = t & 7;
+  const int64_t leaf = L0 + li;
+  int n = 0, off = 0;
+  if (leaf < L1) {
+    n = p.leaf_len[leaf];
+    off = (int)(p.leaf_lo[leaf] - lo);
+    if (n >= 8) {  // accumulator j: a[j], a[j+8], ... up to n - n % 8
+      double r = a[off + j];
+      for (int i = 8; i < n - (n % 8); i += 8) r = __dadd_rn(r, a[off + i + j]);
+      racc[li][j] = r;
+    }
+  }
+  __syncthreads();
+  if (leaf < L1 && j == 0) {
+    double res;
+    if (n < 8) {
+      res = 0.0;
+      for (int i = 0; i < n; ++i) res = __dadd_rn(res, a[off + i]);
+    } else {
+      const double* r = racc[li];
+      res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      for (int i = n - (n % 8); i < n; ++i) res = __dadd_rn(res, a[off + i]);
+    }
+    p.leaf_val[leaf] = res;
+  }
+  __syncthreads();
+  const int32_t* lv = p.blk_lvl + (size_t)b * (kMkLvl + 1);
+  for (int h = 0; h < kMkLvl; ++h) {
+    for (int i = lv[h] + t; i < lv[h + 1]; i += blockDim.x)
+      p.leaf_val[p.loc_out[i]] = __dadd_rn(p.leaf_val[p.loc_l[i]], p.leaf_val[p.loc_r[i]]);
+    __syncthreads();
+  }
+  // the last CTA folds the top of the tree
+  __threadfence();
+  __syncthreads();
+  if (t == 0) last = atomicAdd(&S->sum_ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   int start = 0;
-  for (int lv = 0; lv < p.nlevels; ++lv) {
-    const int end = p.level_end[lv];
-    for (int i = start + threadIdx.x; i < end; i += blockDim.x)
-      p.leaf_val[p.tree_out[i]] = __dadd_rn(p.leaf_val[p.tree_l[i]], p.leaf_val[p.tree_r[i]]);
+  for (int lvl = 0; lvl < p.nlevels; ++lvl) {
+    const int end = p.level_end[lvl];
+    for (int i = start + t; i < end; i += blockDim.x)
+      p.leaf_val[p.tree_out[i]] = __dadd_rn(__ldcg(&p.leaf_val[p.tree_l[i]]), __ldcg(&p.leaf_val[p.tree_r[i]]));
+    __threadfence_block();
     __syncthreads();
     start = end;
   }
-  if (threadIdx.x == 0) {
-    MkScalars* S = p.S;
-    const double total = p.n ? p.leaf_val[p.root] : 0.0;
-    const double mx = __longlong_as_double((long long)S->max_bits);
+  if (t == 0) {
+    const double total = p.n ? __ldcg(&p.leaf_val[p.root]) : 0.0;
+    const double m = __longlong_as_double((long long)atomicAdd(&S->max_bits, 0ull));
     double tau;
-    if (total <= 0.0 || mx <= 0.0) {
+    if (total <= 0.0 || m <= 0.0) {
       tau = p.tau_max;
     } else {
       // min(theta * N / total, p_max / max_rate, tau_max), left to right
       tau = __ddiv_rn(__dmul_rn(p.theta, (double)p.n), total);
-      const double b = __ddiv_rn(p.p_max, mx);
-      if (b < tau) tau = b;
+      const double c2 = __ddiv_rn(p.p_max, m);
+      if (c2 < tau) tau = c2;
       if (p.tau_max < tau) tau = p.tau_max;
     }
     S->tau = tau;
@@ -161,7 +221,8 @@ __global__ void __launch_bounds__(1024) k_mk_tree(const MkParams p) {
     const int64_t slot = S->step % p.log_cap;
     p.log_clock[slot] = S->clock;
     p.log_tau[slot] = tau;
-    S->max_bits = 0ull;  // the next k_mk_rates maxes afresh
+    S->max_bits = 0ull;  // next step maxes afresh
+    S->sum_ticket = 0u;
   }
 }
 
@@ -291,6 +352,7 @@ struct fs_markov {
   int64_t* leaf_lo = nullptr;
   int32_t* leaf_len = nullptr;
   int32_t *tl = nullptr, *tr = nullptr, *tout = nullptr, *lend = nullptr;
+  int32_t *loc_l = nullptr, *loc_r = nullptr, *loc_out = nullptr, *blk_lvl = nullptr;
   uint16_t* cnt = nullptr;
   uint32_t* pend[2] = {nullptr, nullptr};
   double* log_clock = nullptr;
@@ -319,11 +381,8 @@ int mk_alloc(T** p, size_t n) {
 }
 
 int mk_launch(fs_markov* e, int nsteps, cudaStream_t st) {
-  const int lb = (int)std::max<int64_t>(1, std::min<int64_t>((e->p.nleaf + 255) / 256, (int64_t)e->sms * 8));
   for (int k = 0; k < nsteps; ++k) {
-    k_mk_rates<<<e->grid, 256, 0, st>>>(e->p);
-    k_mk_leaves<<<lb, 256, 0, st>>>(e->p);
-    k_mk_tree<<<1, 1024, 0, st>>>(e->p);
+    k_mk_sum<<<e->p.nblocks, 256, 0, st>>>(e->p);
     k_mk_fire<<<e->grid, 256, 0, st>>>(e->p);
     ++e->h_step;
   }
@@ -384,33 +443,76 @@ int fs_markov_create(const fs_graph* g, const fs_model* m, const fs_markov_confi
   const int root0 = t.build(0, n, &h);
   const int nleaf = (int)t.leaf_lo.size(), nint = (int)t.l.size();
   auto vid = [&](int id) { return id < 0 ? (-id - 1) : nleaf + id; };  // leaves first, then internal
-  std::vector<int> order(nint);
-  for (int i = 0; i < nint; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return t.level[a] < t.level[b]; });
-  std::vector<int32_t> hl(nint), hr(nint), ho(nint), lend;
-  for (int k = 0; k < nint; ++k) {
-    const int i = order[k];
+  // leaf span of every internal node (children precede parents in t.l / t.r)
+  std::vector<int> first(nint), last(nint);
+  auto span_lo = [&](int id) { return id < 0 ? (-id - 1) : first[id]; };
+  auto span_hi = [&](int id) { return id < 0 ? (-id - 1) : last[id]; };
+  for (int i = 0; i < nint; ++i) {
+    first[i] = span_lo(t.l[i]);
+    last[i] = span_hi(t.r[i]);
+  }
+  const int nblocks = (nleaf + kMkLeafBlock - 1) / kMkLeafBlock;
+  std::vector<std::vector<int>> loc(nblocks * kMkLvl);
+  std::vector<int> top;
+  for (int i = 0; i < nint; ++i) {
+    const int b0 = first[i] / kMkLeafBlock, b1 = last[i] / kMkLeafBlock;
+    if (b0 == b1 && t.level[i] <= kMkLvl) loc[(size_t)b0 * kMkLvl + (t.level[i] - 1)].push_back(i);
+    else top.push_back(i);
+  }
+  std::vector<int32_t> ll, lr, lo_, blv((size_t)nblocks * (kMkLvl + 1));
+  for (int b = 0; b < nblocks; ++b) {
+    blv[(size_t)b * (kMkLvl + 1)] = (int32_t)ll.size();
+    for (int h = 0; h < kMkLvl; ++h) {
+      for (int i : loc[(size_t)b * kMkLvl + h]) {
+        ll.push_back(vid(t.l[i]));
+        lr.push_back(vid(t.r[i]));
+        lo_.push_back(nleaf + i);
+      }
+      blv[(size_t)b * (kMkLvl + 1) + h + 1] = (int32_t)ll.size();
+    }
+  }
+  std::stable_sort(top.begin(), top.end(), [&](int a, int b) { return t.level[a] < t.level[b]; });
+  const int ntop = (int)top.size();
+  std::vector<int32_t> hl(ntop), hr(ntop), ho(ntop), lend;
+  for (int k = 0; k < ntop; ++k) {
+    const int i = top[k];
     hl[k] = vid(t.l[i]);
     hr[k] = vid(t.r[i]);
     ho[k] = nleaf + i;
-    if (k + 1 == nint || t.level[order[k + 1]] != t.level[i]) lend.push_back(k + 1);
+    if (k + 1 == ntop || t.level[top[k + 1]] != t.level[i]) lend.push_back(k + 1);
   }
   p.nleaf = nleaf;
   p.nlevels = (int)lend.size();
   p.root = vid(root0);
+  p.nblocks = nblocks;
+  const int nloc = (int)ll.size();
+  MK_TRY(mk_alloc(&e->loc_l, nloc));
+  MK_TRY(mk_alloc(&e->loc_r, nloc));
+  MK_TRY(mk_alloc(&e->loc_out, nloc));
+  MK_TRY(mk_alloc(&e->blk_lvl, blv.size()));
+  if (nloc) {
+    MK_CUDA(cudaMemcpy(e->loc_l, ll.data(), nloc * sizeof(int32_t), cudaMemcpyHostToDevice));
+    MK_CUDA(cudaMemcpy(e->loc_r, lr.data(), nloc * sizeof(int32_t), cudaMemcpyHostToDevice));
+    MK_CUDA(cudaMemcpy(e->loc_out, lo_.data(), nloc * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  MK_CUDA(cudaMemcpy(e->blk_lvl, blv.data(), blv.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  p.loc_l = e->loc_l;
+  p.loc_r = e->loc_r;
+  p.loc_out = e->loc_out;
+  p.blk_lvl = e->blk_lvl;
   MK_TRY(mk_alloc(&e->vals, (size_t)nleaf + nint));
   MK_TRY(mk_alloc(&e->leaf_lo, nleaf));
   MK_TRY(mk_alloc(&e->leaf_len, nleaf));
-  MK_TRY(mk_alloc(&e->tl, nint));
-  MK_TRY(mk_alloc(&e->tr, nint));
-  MK_TRY(mk_alloc(&e->tout, nint));
+  MK_TRY(mk_alloc(&e->tl, ntop));
+  MK_TRY(mk_alloc(&e->tr, ntop));
+  MK_TRY(mk_alloc(&e->tout, ntop));
   MK_TRY(mk_alloc(&e->lend, lend.size()));
   MK_CUDA(cudaMemcpy(e->leaf_lo, t.leaf_lo.data(), nleaf * sizeof(int64_t), cudaMemcpyHostToDevice));
   MK_CUDA(cudaMemcpy(e->leaf_len, t.leaf_len.data(), nleaf * sizeof(int32_t), cudaMemcpyHostToDevice));
-  if (nint) {
-    MK_CUDA(cudaMemcpy(e->tl, hl.data(), nint * sizeof(int32_t), cudaMemcpyHostToDevice));
-    MK_CUDA(cudaMemcpy(e->tr, hr.data(), nint * sizeof(int32_t), cudaMemcpyHostToDevice));
-    MK_CUDA(cudaMemcpy(e->tout, ho.data(), nint * sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (ntop) {
+    MK_CUDA(cudaMemcpy(e->tl, hl.data(), ntop * sizeof(int32_t), cudaMemcpyHostToDevice));
+    MK_CUDA(cudaMemcpy(e->tr, hr.data(), ntop * sizeof(int32_t), cudaMemcpyHostToDevice));
+    MK_CUDA(cudaMemcpy(e->tout, ho.data(), ntop * sizeof(int32_t), cudaMemcpyHostToDevice));
     MK_CUDA(cudaMemcpy(e->lend, lend.data(), lend.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
   p.leaf_val = e->vals;
@@ -459,7 +561,8 @@ void fs_markov_destroy(fs_markov* e) {
   cudaSetDevice(e->device);
   for (auto& x : e->exec) if (x) cudaGraphExecDestroy(x);
   if (e->cap) cudaStreamDestroy(e->cap);
-  void* ptrs[] = {e->S, e->vals, e->leaf_lo, e->leaf_len, e->tl, e->tr, e->tout, e->lend, e->cnt, e->pend[0],
+  void* ptrs[] = {e->S, e->vals, e->leaf_lo, e->leaf_len, e->tl, e->tr, e->tout, e->lend, e->loc_l, e->loc_r,
+                  e->loc_out, e->blk_lvl, e->cnt, e->pend[0],
                   e->pend[1], e->log_clock, e->log_tau, e->log_counts};
   for (void* q : ptrs) if (q) cudaFree(q);
   delete e;
