@@ -49,6 +49,9 @@ WORKLOADS = {
                kind="regular_dev", n=1_000_000_000, k=10, model="seir", cpu_n=10_000_000, t_final=10.0),
     "m2": dict(desc="M2 (SURVEY §8f row 3): Markovian SIR (beta 0.25, gamma 0.15), uniform-degree k=10, N=1e6",
                kind="fixed", n=1_000_000, k=10, model="sir_markov", engine="markov"),
+    "c2w": dict(desc="C2 per GPU, weak scaling: SEIR log-normal, uniform-degree k=10, N=1e6 nodes per GPU, "
+                     "node-partitioned (peer pushes + NCCL all-reduce per step)",
+                kind="regular_dev", n=1_000_000, k=10, model="seir", per_gpu=True),
     "c4": dict(desc="C4: SEIR log-normal, uniform-degree k=10, N=1e8, bf16/fp16 mixed-precision storage",
                kind="regular_dev", n=100_000_000, k=10, model="seir", mixed=True, cpu_n=10_000_000),
 }
@@ -196,7 +199,7 @@ def cpu_ensemble(g, m, warm: int, steps: int, workers: int | None = None, mixed:
 def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
-    w = WORKLOADS[args.workload]
+    w = WORKLOADS["c2" if args.workload == "c2w" else args.workload]  # the CPU has no per-GPU split
     if w.get("engine") == "markov":
         print(json.dumps({"impl": "reference", "unavailable": "the CPU oracle port restates the renewal path only"}))
         return
@@ -293,7 +296,8 @@ def run_partitioned(args, w, rank: int, world: int, local: int) -> None:
     import paper_2604_22092_b200 as fs
     from paper_2604_22092_b200.distributed import DistributedRun, partition_plan, run_renewal_distributed
 
-    n_total = w["n"]
+    weak = bool(w.get("per_gpu"))
+    n_total = w["n"] * world if weak else w["n"]
     plan = partition_plan(n_total, world)
     lo, hi = plan.ranges[rank]
     m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
@@ -305,19 +309,39 @@ def run_partitioned(args, w, rank: int, world: int, local: int) -> None:
     run = DistributedRun(g, m, cfg, SIM_SEED, plan, rank)
     run.step(args.warmup)
     run.run_batch()  # capture the batch graph (NCCL inside) outside the timed region
-    nb = max(1, args.steps // cfg.steps_per_batch)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        e0.record()
-        for _ in range(nb):
-            run.part.run_batch()
-        e1.record()
+    if weak:
+        # per-GPU inputs fit in L2: each step timed alone after an L2 flush
+        steps = args.steps
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+        flush_rd = torch.ones(128 << 20, dtype=torch.int32, device="cuda")
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        dist.barrier()
         torch.cuda.synchronize()
-    dist.barrier()
-    steps = nb * cfg.steps_per_batch
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        with ClockSampler(local) as clk:
+            for k in range(steps):
+                flush.zero_()
+                flush_rd.max()
+                starts[k].record()
+                run.step(1)
+                ends[k].record()
+            torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(starts, ends))], dtype=torch.float64, device="cuda")
+    else:
+        nb = max(1, args.steps // cfg.steps_per_batch)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            e0.record()
+            for _ in range(nb):
+                run.part.run_batch()
+            e1.record()
+            torch.cuda.synchronize()
+        dist.barrier()
+        steps = nb * cfg.steps_per_batch
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     run.close()
@@ -349,12 +373,14 @@ def run_partitioned(args, w, rank: int, world: int, local: int) -> None:
     print(json.dumps({
         "metric": "Giga-NUPS (node updates/s)", "value": n_total * steps / (total_ms / 1e3) / 1e9, "unit": "G-NUPS",
         "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None,
         "dtype": "i8/f16/bf16 storage, f32 rates, f64 hazard/q" if mixed else "f32 (f64 hazard/q)",
         "data": "synthetic (GPU uniform-degree generator fs_gen_regular, graph seed 1, sim seed 7)",
         "config": {"workload": w["desc"], "n": n_total, "edges": int(edges.item()), "strategy": "per-node",
-                   "gather": "count (1-bit mask)", "parallelism": f"node-partitioned x{world} (NCCL)",
-                   "l2": "inputs larger than L2; steps timed back to back as CUDA-graph batches",
+                   "gather": "incremental counts, cross-rank pushes into peer memory (CUDA IPC / NVLink)",
+                   "parallelism": f"node-partitioned x{world} (peer pushes + NCCL all-reduce of 17 words per step)",
+                   "l2": ("flushed before every timed step (512 MiB write + 512 MiB read of another buffer)" if weak
+                          else "inputs larger than L2; steps timed back to back as CUDA-graph batches"),
                    "steps_from": f"t=0 after {args.warmup} warm-up steps"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"] * world, "unit": "GB/s",
                      "frac": achieved / (pk["hbm_gbs"] * world), "traffic": None,
@@ -389,7 +415,9 @@ def main() -> None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.workload is None:
-        args.workload = "c2" if world == 1 else "c5"
+        # N=1: the headline C2; N>1: the same per-GPU work, node-partitioned
+        # (weak scaling, so the driver's per-N efficiency compares like with like)
+        args.workload = "c2" if world == 1 else "c2w"
     if world > 1:
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
     if args.impl == "reference":
