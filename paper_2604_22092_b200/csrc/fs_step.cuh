@@ -644,6 +644,10 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
       const bool up = __shfl_sync(kFull, push, src) > 0;
       for (int64_t e = a0 + lane; e < a1; e += 32) push_delta(p, nxt, __ldg(p.out_col + e), up);
     }
+    // partitioned: the pushes into peer GPUs' memory are ordered before
+    // anything this thread's rank does next — in particular before the NCCL
+    // all-reduce the next step waits on — so they are visible to the owner
+    if (p.world > 1 && __any_sync(kFull, push != 0)) __threadfence_system();
   }
   __syncwarp();
 }
