@@ -217,6 +217,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         )
     lib = ctypes.CDLL(str(p))
     for name, (res, args) in _SIGNATURES.items():
+        if os.environ.get("FS_LIB_PATH") and not hasattr(lib, name):
+            continue  # an older build under A/B measurement
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

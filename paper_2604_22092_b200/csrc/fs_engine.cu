@@ -360,6 +360,7 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.out_ro = e->g.out_row_offsets;
   p.out_col = e->g.out_col_indices;
   p.world = e->incr ? e->world : 1;
+  p.hubs = e->g.d_max > 32 ? 1 : 0;  // local rows; partitioned rows of a symmetric graph mirror the degrees
   p.part_chunk = e->mask_seg_words * 32;
   for (int par = 0; par < 2; ++par)
     for (int r = 0; r < FS_MAX_PARTITIONS; ++r) p.peer_pend[par][r] = e->peer_pend[par][r];
@@ -725,7 +726,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     // streaming kernel: per-node arrays readable to a multiple of 128 nodes
     if (buf->padded >= 2 && !getenv("FS_NO_STREAM")) {
       e->stream = true;
-      for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0);
+      for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, false, g->d_max > 32);
       int socc = 1;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&socc, (const void*)e->stream_fn[0], 512, 0) != cudaSuccess || socc < 1) socc = 1;
       if (getenv("FS_INCR_CTAS_PER_SM")) socc = std::max(1, std::min(socc, atoi(getenv("FS_INCR_CTAS_PER_SM"))));
@@ -743,6 +744,8 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     if (costly && want && !getenv("FS_NO_MEMO")) {
       TRY(dalloc(&e->entry, (size_t)((n + 127) / 128) * 128));
       TRY(reset_memo(e, nullptr));
+      if (e->stream)  // the memo's shared-memory table only in the variant that uses it
+        for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, true, g->d_max > 32);
     }
   }
   if (getenv("FS_NO_PDL")) e->pdl = false;
@@ -817,7 +820,9 @@ int fs_engine_run_batch(fs_engine* e, int32_t materialize, void* stream) {
   const int s0 = e->s_cur;
   const int64_t h0 = e->h_step;
   // the exchange's accumulator slot and mask buffer are baked in at capture
-  cudaGraphExec_t& exec = e->batch_exec[materialize ? 1 : 0][s0][(int)(h0 % 6)];
+  // baked in: the step parity (early loads) and, with a communicator, the
+  // exchange slot step % 3 — so key by step % 6 only when exchanging
+  cudaGraphExec_t& exec = e->batch_exec[materialize ? 1 : 0][s0][e->comm ? (int)(h0 % 6) : (int)(h0 & 1)];
   if (!exec) {
     cudaGraph_t graph = nullptr;
     FS_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));

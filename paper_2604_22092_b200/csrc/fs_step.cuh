@@ -8,6 +8,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <type_traits>
 #include "fs_device.cuh"
 #include "fs_internal.h"
 
@@ -89,6 +90,7 @@ struct StepParams {
   const int64_t* out_ro;         // outgoing CSR of the local rows (the incoming one for symmetric graphs)
   const int32_t* out_col;        // global ids
   int world;                     // > 1: pushes go to the owner's pending deltas (peer_pend)
+  int hubs;                      // some out-row exceeds 32 edges: warp-cooperative pushes
   int64_t part_chunk;            // nodes per rank
   uint32_t* peer_pend[2][FS_MAX_PARTITIONS];  // every rank's pending-delta arrays, by parity
   int stream_evict_first;        // CSR stream larger than L2: evict-first hint on column loads
@@ -556,7 +558,7 @@ __device__ __forceinline__ void push_delta(const StepParams& p, int nxt, int32_t
   else atomicSub(dn, one);
 }
 
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true>
 __device__ __forceinline__ void drain_entries(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh,
                                               const int* qn_node, const int* qn_state, const float* qn_age,
                                               const float* qn_press, int lane, int cnt, float& lmax,
@@ -633,11 +635,11 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
       e0 = __ldg(p.out_ro + n);  // out-row of local node n
       e1 = __ldg(p.out_ro + n + 1);
     }
-    const bool wide = push && (e1 - e0 > 32);
+    const bool wide = HUBS && p.hubs && push && (e1 - e0 > 32);
     if (push && !wide)
       for (int64_t e = e0; e < e1; ++e) push_delta(p, nxt, __ldg(p.out_col + e), push > 0);
-    unsigned wides = __ballot_sync(kFull, wide);
-    while (wides) {
+    unsigned wides = HUBS ? __ballot_sync(kFull, wide) : 0u;
+    while (HUBS && wides) {
       const int src = __ffs(wides) - 1;
       wides &= wides - 1;
       const int64_t a0 = __shfl_sync(kFull, e0, src), a1 = __shfl_sync(kFull, e1, src);
@@ -653,17 +655,17 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
 }
 
 // phase B on this warp's own queue
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true>
 __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
                                             int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt,
                                             HazardMemo* hm = nullptr) {
-  drain_entries<ST, AT, IT, MAT, WARPS>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp], sh.q_press[warp],
-                                        lane, cnt, lmax, mask_nxt, inf_nxt, hm);
+  drain_entries<ST, AT, IT, MAT, WARPS, HUBS>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
+                                              sh.q_press[warp], lane, cnt, lmax, mask_nxt, inf_nxt, hm);
 }
 
 // phase A outcome of one tile (pressure already gathered): cheap outcomes
 // now, possible transitions appended to the warp queue (drained at 32)
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS>
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true>
 __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
                                              int lane, uint32_t tile, uint32_t n, bool valid, int s, float age,
                                              float pressure, int& qn, float& lmax, uint32_t* mask_nxt, IT* inf_nxt,
@@ -697,7 +699,7 @@ __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepCons
   }
   qn += __popc(dm);
   if (qn >= 32) {
-    drain_queue<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt, hm);
+    drain_queue<ST, AT, IT, MAT, WARPS, HUBS>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt, hm);
     if (lane < qn - 32) {
       sh.q_node[warp][lane] = sh.q_node[warp][32 + lane];
       sh.q_state[warp][lane] = sh.q_state[warp][32 + lane];
@@ -870,17 +872,20 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
 // Phase B (the deferral queue: hazards, uniforms, Bernoulli, pushes) is the
 // same as k_step's.
 // ---------------------------------------------------------------------------
-template <typename ST, typename AT, bool MAT, int BLOCK>
+template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   constexpr int WARPS = BLOCK / 32;
   __shared__ StepShared<WARPS> sh;
   __shared__ StepConst s_k;
-  __shared__ HazardMemo s_hm;
+  __shared__ typename std::conditional<MEMO, HazardMemo, char>::type s_hm;  // memo variant only
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_launch_dependents();
   load_tables<WARPS>(p, sh, tid);  // static model tables: before the dependency wait
-  if (p.entry) memo_init<BLOCK>(s_hm, p, tid);
-  HazardMemo* hmp = p.entry ? &s_hm : nullptr;
+  HazardMemo* hmp = nullptr;
+  if constexpr (MEMO) {
+    memo_init<BLOCK>(s_hm, p, tid);
+    hmp = &s_hm;
+  }
   pdl_wait();
   if (tid == 0) {
     s_k = step_const(p, true);
@@ -910,7 +915,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     if (t + stride < ntiles) load(t + stride, pend_h, in1);
   }
   __syncthreads();
-  const StepConst k = s_k;
+  const StepConst& k = s_k;  // read from shared memory where used: keeps the hot loop's registers free
   const int cur = (int)(k.step & 1);
   uint32_t* mask_nxt = p.mask[cur ^ 1];
   uint16_t* __restrict__ pend = reinterpret_cast<uint16_t*>(p.pend[cur]);
@@ -936,10 +941,10 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     const float pressure = (valid && (s == k.edge_from || MAT))
                                ? (p.ptab_mul ? __fmul_rn((float)c, p.ptab_c) : __ldg(p.ptab + c))
                                : 0.0f;
-    tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure,
-                                            qn, lmax, mask_nxt, nullptr, hmp);
+    tile_outcome<ST, AT, float, MAT, WARPS, HUBS>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure,
+                                                  qn, lmax, mask_nxt, nullptr, hmp);
   }
-  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr, hmp);
+  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS, HUBS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr, hmp);
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
 
@@ -1190,7 +1195,7 @@ using TmaFn = void (*)(const StepParams, const TmaLayout);
 
 // instantiation units
 StepFn pick_step(bool mixed, int gather, int strat, bool mat, int& block);  // fs_step_general.cu
-StepFn pick_stream(bool mixed, bool mat);                                   // fs_step_incr.cu
+StepFn pick_stream(bool mixed, bool mat, bool memo, bool hubs);             // fs_step_incr.cu
 MergeFn pick_merge(bool inf_bf16, int mode, int& block);                    // fs_step_incr.cu
 TmaFn pick_tma(bool mixed, bool smem_mask, bool mat, bool ptab_mul, int block);  // fs_step_tma.cu
 

@@ -4,9 +4,17 @@
 
 namespace fs {
 
-StepFn pick_stream(bool mixed, bool mat) {
-  if (mixed) return mat ? k_step_incr<int8_t, __half, true, 512> : k_step_incr<int8_t, __half, false, 512>;
-  return mat ? k_step_incr<int32_t, float, true, 512> : k_step_incr<int32_t, float, false, 512>;
+template <bool MEMO, bool HUBS>
+StepFn pick_stream2(bool mixed, bool mat) {
+  if (mixed) return mat ? k_step_incr<int8_t, __half, true, MEMO, HUBS, 512> : k_step_incr<int8_t, __half, false, MEMO, HUBS, 512>;
+  return mat ? k_step_incr<int32_t, float, true, MEMO, HUBS, 512> : k_step_incr<int32_t, float, false, MEMO, HUBS, 512>;
+}
+
+// MEMO: the age-cohort hazard memo's shared table; HUBS: warp-cooperative
+// pushes for rows over 32 edges (compiled out for bounded-degree graphs)
+StepFn pick_stream(bool mixed, bool mat, bool memo, bool hubs) {
+  if (memo) return hubs ? pick_stream2<true, true>(mixed, mat) : pick_stream2<true, false>(mixed, mat);
+  return hubs ? pick_stream2<false, true>(mixed, mat) : pick_stream2<false, false>(mixed, mat);
 }
 
 

@@ -388,7 +388,9 @@ class _Engine:
         self.reset_age_memo()
 
     def reset_age_memo(self) -> None:
-        _lib.check(self.lib.fs_engine_reset_age_memo(self.handle, self.stream))
+        fn = getattr(self.lib, "fs_engine_reset_age_memo", None)  # absent only in older A/B builds
+        if fn is not None:
+            _lib.check(fn(self.handle, self.stream))
 
     def read_log(self, first_step: int, n: int):
         M = self.plan.num_compartments
