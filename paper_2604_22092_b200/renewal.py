@@ -173,7 +173,12 @@ class _DeviceGraph:
         self.weights = None if self.uniform else _device.to_device(w, dev)
         self.weights_bf16 = mixed
         self.d_max = int(np.diff(ro).max()) if self.num_nodes else 0
-        self.symmetric = _is_symmetric(self)
+        # cached on the host graph like the reference caches its transpose
+        # (R/graph.py:187-191 build_outgoing): a property of the arrays
+        sym = g.__dict__.get("_fs_symmetric")
+        if sym is None:
+            sym = g.__dict__["_fs_symmetric"] = _is_symmetric(self)
+        self.symmetric = sym
 
     def view(self) -> _lib.FsGraph:
         return _lib.FsGraph(
