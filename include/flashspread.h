@@ -248,6 +248,10 @@ int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream);
  * writing ages or states from outside the engine (host edits, snapshot
  * restores) so no node is assumed to follow its cohort. */
 int fs_engine_reset_age_memo(fs_engine* e, void* stream);
+/* the caller wrote `states` between steps: re-derive what the engine keeps
+ * from them (age cohorts; with incremental counts, the pushes the edited
+ * nodes' changes of infectious status imply for the step after next) */
+int fs_engine_states_edited(fs_engine* e, void* stream);
 /* re-derive the infectious mask / general buffer from a freshly uploaded
  * infectivity array (host edits between steps); `inf` has the storage dtype */
 int fs_engine_load_infectivity(fs_engine* e, const void* inf, void* stream);

@@ -160,6 +160,7 @@ _SIGNATURES = {
     "fs_engine_acc_get": (_c_i32, [_vp, _vp, _vp]),
     "fs_engine_acc_set": (_c_i32, [_vp, _vp, _vp]),
     "fs_engine_reset_age_memo": (_c_i32, [_vp, _vp]),
+    "fs_engine_states_edited": (_c_i32, [_vp, _vp]),
     "fs_engine_set_peer_deltas": (_c_i32, [_vp, _vp]),
     "fs_ipc_get_handle": (_c_i32, [_vp, _vp, _c_i32]),
     "fs_ipc_open_handle": (_c_i32, [_vp, _c_i32, ctypes.POINTER(_vp)]),

@@ -63,6 +63,27 @@ __global__ void k_init_counts(const int64_t* __restrict__ ro, const int32_t* __r
   }
 }
 
+// host edited the states between steps: the next step writes the next mask
+// from the edited states, so every node whose infectious status now differs
+// from its bit in the current mask pushes +-1 into the pending deltas that
+// step's successor folds — exactly the pushes a transition would have made
+template <typename ST>
+__global__ void k_edit_pushes(const ST* __restrict__ states, const uint32_t* __restrict__ mask_cur, int64_t n,
+                              int infectious, const int64_t* __restrict__ out_ro, const int32_t* __restrict__ out_col,
+                              uint32_t* __restrict__ pend_nxt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool now = (int)states[i] == infectious;
+    const bool was = (mask_cur[i >> 5] >> (i & 31)) & 1u;
+    if (now == was) continue;
+    for (int64_t e = out_ro[i], e1 = out_ro[i + 1]; e < e1; ++e) {
+      const int32_t j = out_col[e];
+      const uint32_t one = 1u << (16 * (j & 1));
+      if (now) atomicAdd(pend_nxt + (j >> 1), one);
+      else atomicSub(pend_nxt + (j >> 1), one);
+    }
+  }
+}
+
 // first node n with row_offsets[n] >= chunk start, for every chunk boundary
 __global__ void k_chunk_first(const int64_t* __restrict__ ro, int64_t n, int64_t e, int64_t epb,
                               int64_t nchunks, int64_t* __restrict__ out) {
@@ -990,6 +1011,26 @@ int fs_engine_store_infectivity(fs_engine* e, void* out, void* stream) {
     return 0;
   }
   FS_CUDA(cudaMemcpyAsync(out, e->b.infectivity[cur], (size_t)n * (e->mixed ? 2 : 4), cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+int fs_engine_states_edited(fs_engine* e, void* stream) {
+  if (!e) return set_error(FS_EINVAL, "null engine");
+  FS_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = reset_memo(e, st);  // edited nodes no longer follow their age cohorts
+  if (rc || !e->incr) return rc;
+  if (e->world > 1) return set_error(FS_ESTATE, "host state edits are not supported on partitioned engines");
+  const int cur = (int)(e->h_step & 1);
+  const int64_t n = e->g.num_nodes;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8));
+  if (e->mixed)
+    k_edit_pushes<int8_t><<<blocks, 256, 0, st>>>((const int8_t*)e->b.states, e->b.imask[cur], n, e->m.infectious,
+                                                  e->g.out_row_offsets, e->g.out_col_indices, e->delta[cur ^ 1]);
+  else
+    k_edit_pushes<int32_t><<<blocks, 256, 0, st>>>((const int32_t*)e->b.states, e->b.imask[cur], n, e->m.infectious,
+                                                   e->g.out_row_offsets, e->g.out_col_indices, e->delta[cur ^ 1]);
+  FS_CUDA(cudaGetLastError());
   return 0;
 }
 

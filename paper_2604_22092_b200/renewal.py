@@ -392,6 +392,9 @@ class _Engine:
         self.set_scalars(sc)
         self.reset_age_memo()
 
+    def states_edited(self) -> None:
+        _lib.check(self.lib.fs_engine_states_edited(self.handle, self.stream))
+
     def reset_age_memo(self) -> None:
         fn = getattr(self.lib, "fs_engine_reset_age_memo", None)  # absent only in older A/B builds
         if fn is not None:
@@ -563,13 +566,18 @@ class RenewalState:
         if name in ("pressure", "rates"):
             self._ensure_debug_buffers()
         self._t[name].copy_(_device.to_device(_host_cast(arr, dtype), self._dev))
-        if name in ("states", "ages") and self._engine is not None:
+        if name == "states" and self._engine is not None:
+            self._engine.states_edited()  # age cohorts, and the pushes of implied status changes
+        elif name == "ages" and self._engine is not None:
             self._engine.reset_age_memo()  # host-written nodes no longer follow their age cohorts
 
     def _push_host(self) -> None:
         """Upload every downloaded array the caller edited in place."""
         if self._mirror:
-            for name, (arr, snap) in list(self._mirror.items()):
+            # infectivity first: its upload rebuilds the engine's counts, which
+            # the pushes implied by edited states then build on
+            order = {"infectivity": 0, "counts": 1, "states": 2}
+            for name, (arr, snap) in sorted(self._mirror.items(), key=lambda kv: order.get(kv[0], 3)):
                 if arr.shape != snap.shape or arr.tobytes() != snap.tobytes():
                     self._upload(name, arr)
             self._mirror.clear()

@@ -299,3 +299,38 @@ def test_engine_variants_bit_exact(name, env, monkeypatch):
     assert np.array_equal(log["counts"], ref["counts"])
     assert np.array_equal(st.states.astype(np.int32), ref["states"])
     assert np.array_equal(st.ages.astype(np.float32), ref["ages"])
+
+
+@pytest.mark.parametrize("gather", ["incremental", "count"])
+@pytest.mark.parametrize("edit_inf", [False, True])
+def test_host_state_edits_mid_run(gather, edit_inf):
+    """States written between steps (T/test_renewal.py:118-120, 245-246 edit
+    them): the next step still gathers the infectivity of the previous one
+    (R/renewal.py:500-505), the step after sees the edited nodes — also with
+    incremental counts, which must push the implied status changes."""
+    g, m = graph("er_300"), model("sir")
+    cfg = fs.RenewalConfig(gather=gather)
+    st = fs.init_renewal_state(g, m, cfg, 5)
+    ref = O.init_state(g, m, cfg, 5)
+    for _ in range(30):
+        fs.renewal_step(st, g, m, cfg, 5)
+        O.step(ref, g, m, cfg, 5)
+    s_nodes = np.flatnonzero(ref.states == 0)[:6]
+    i_nodes = np.flatnonzero(ref.states == 1)[:2]
+    for arr in (st.states, ref.states):
+        arr[s_nodes] = 1  # S -> I by hand
+        arr[i_nodes] = 2  # I -> R by hand
+    c = np.bincount(ref.states.astype(np.int64), minlength=3)
+    st.counts = c
+    ref.counts = c.copy()
+    if edit_inf:  # infectivity made consistent with the edit as well
+        inf = np.where(ref.states == 1, np.float32(m.beta), np.float32(0.0)).astype(np.float32)
+        st.infectivity = inf
+        ref.infectivity = inf.copy()
+    for _ in range(40):
+        fs.renewal_step(st, g, m, cfg, 5)
+        O.step(ref, g, m, cfg, 5)
+        assert np.array_equal(st.counts, ref.counts)
+    assert np.array_equal(st.states.astype(np.int32), ref.states.astype(np.int32))
+    assert np.array_equal(st.pressure, ref.pressure)
+    assert st.clock == ref.clock
