@@ -307,7 +307,9 @@ struct fs_engine {
   bool compaction_ready = false;
   int stream_evict_first = 0;
   // incremental count mode
-  int32_t* entry = nullptr;           // hazard memo: per-node entry step
+  int32_t* entry = nullptr;           // cohort table: per-node entry step
+  unsigned long long* ctab = nullptr;  // [2][kCohortSlots][kCohortW]
+  unsigned long long* cage = nullptr;  // [2][kCohortW]
   bool incr = false;
   uint32_t* peer_pend[2][FS_MAX_PARTITIONS] = {};  // partitioned incremental: every rank's delta arrays
   bool peers_linked = false;
@@ -375,6 +377,16 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.stream_evict_first = e->stream_evict_first;
   p.host_parity = (int)(e->h_step & 1);
   p.entry = e->entry;
+  p.ctab = e->entry ? e->ctab : nullptr;
+  p.cage = e->cage;
+  p.ncslots = 0;
+  for (int c = 0; c < FS_MAX_COMPARTMENTS; ++c) {
+    p.cslot[c] = -1;
+    if (c < e->m.num_compartments && e->m.comp[c].hazard >= FS_HZ_LOGNORMAL && p.ncslots < kCohortSlots) {
+      p.cslot[c] = p.ncslots;
+      p.cslot_comp[p.ncslots++] = c;
+    }
+  }
   p.cnt = e->incr ? e->cnt : nullptr;
   p.pend[0] = e->delta[0];
   p.pend[1] = e->delta[1];
@@ -520,6 +532,8 @@ int reset_memo(fs_engine* e, cudaStream_t st) {
   const int64_t n = (e->g.num_nodes + 127) / 128 * 128;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
   k_fill<int32_t><<<std::max(1, blocks), 256, 0, st>>>(e->entry, n, kEntryInvalid);
+  FS_CUDA(cudaMemsetAsync(e->ctab, 0xFF, sizeof(unsigned long long) * 2 * kCohortSlots * kCohortW, st));
+  FS_CUDA(cudaMemsetAsync(e->cage, 0xFF, sizeof(unsigned long long) * 2 * kCohortW, st));
   FS_CUDA(cudaGetLastError());
   return 0;
 }
@@ -758,12 +772,15 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     // hazard memo for models with age-dependent holding times
     bool costly = false;
     for (int c2 = 0; c2 < m->num_compartments; ++c2) costly |= m->comp[c2].hazard >= FS_HZ_LOGNORMAL;
-    // the memo pays off when a CTA holds many nodes of each age cohort
-    // (large N); at N ~ 1e6 its setup costs more than it saves
+    // the cohort table is prepared by the incremental step kernel; its
+    // preparation adds ~2 us to a step, so it is on where steps are long
+    // (N >= 4M: C4, C5) and off at N ~ 1e6
     const char* mv = getenv("FS_MEMO");
-    const bool want = mv ? atoi(mv) != 0 : (e->incr && n >= (int64_t)8 * 1024 * 1024);
+    const bool want = mv ? atoi(mv) != 0 : (e->stream && n >= (int64_t)4 * 1024 * 1024);
     if (costly && want && !getenv("FS_NO_MEMO")) {
       TRY(dalloc(&e->entry, (size_t)((n + 127) / 128) * 128));
+      TRY(dalloc(&e->ctab, (size_t)2 * kCohortSlots * kCohortW));
+      TRY(dalloc(&e->cage, (size_t)2 * kCohortW));
       TRY(reset_memo(e, nullptr));
       if (e->stream)  // the memo's shared-memory table only in the variant that uses it
         for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, true, g->d_max > 32);
@@ -803,7 +820,7 @@ void fs_engine_destroy(fs_engine* e) {
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   void* ptrs[] = {e->dstate, e->acc, e->log_clock, e->log_tau, e->log_counts, e->ptab,
                   e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag,
-                  e->cnt, e->delta[0], e->delta[1], e->entry};
+                  e->cnt, e->delta[0], e->delta[1], e->entry, e->ctab, e->cage};
   for (void* q : ptrs) if (q) cudaFree(q);
   delete e;
 }

@@ -22,8 +22,8 @@ constexpr size_t kMaxSmemMaskBytes = 188u * 1024u;  // + ~34 KB static (queues) 
 
 enum Gather { G_COUNT_SMEM = 0, G_COUNT_GLOBAL = 1, G_F32 = 2, G_PRE = 3, G_INCR = 4 };
 constexpr int32_t kEntryInvalid = INT32_MIN;  // age not known to follow its cohort (init, host edits)
-constexpr int kMemoSlots = 2;                  // age-dependent compartments memoised per CTA
-constexpr int kMemoW = 1 << 10;                // entry steps per compartment (direct-mapped ring)
+constexpr int kCohortSlots = 2;                // age-dependent compartments with a cohort table
+constexpr int kCohortW = 1 << 10;              // cohorts (entry steps) per table: a ring
 
 constexpr uint32_t kDeltaBias = 0x8000u;  // pending delta d is stored as d + 0x8000 (|d| <= d_max < 2^15)
 enum Strat { S_THREAD = 0, S_WARP = 1 };
@@ -97,7 +97,12 @@ struct StepParams {
   int host_parity;               // the host's mirror of (step & 1) for this launch (early loads), -1: none
   // age-cohort hazard memo: entry step of each node's
   // current compartment; the per-CTA memo itself lives in shared memory
-  int32_t* entry;                // [N] or nullptr (memo off)
+  int32_t* entry;                // [N] or nullptr (cohort table off)
+  unsigned long long* ctab;      // [2 parity][kCohortSlots][kCohortW] (step tag << 32 | rate bits)
+  unsigned long long* cage;      // [2 parity][kCohortW] (step tag << 32 | f32 age bits)
+  int ncslots;
+  int cslot[FS_MAX_COMPARTMENTS];      // compartment -> table slot, -1: none
+  int cslot_comp[kCohortSlots];        // table slot -> compartment
   unsigned long long* dbg;       // optional per-CTA %globaltimer stamps [grid][4]
   // model / config
   fs_model model;
@@ -107,28 +112,6 @@ struct StepParams {
   float inf_val;                 // stored infectivity of an I node (count mode), promoted
 };
 
-// Per-CTA, per-step memo of nodal hazard rates by age cohort: every node
-// that entered compartment c at step j carries the same age bits (the same
-// f32 recurrence age += f32(tau) since), hence the same rate, so the f64
-// hazard (R/hazards.py:122-132) runs once per (CTA, c, j) instead of once
-// per node.  Entries are (step tag << 32 | rate bits); racing writers store
-// identical values.  Results are bit-identical with or without it.
-struct HazardMemo {
-  unsigned long long e[kMemoSlots][kMemoW];
-  int slot[FS_MAX_COMPARTMENTS];  // compartment -> memo slot, -1: not memoised
-};
-
-template <int BLOCK>
-__device__ __forceinline__ void memo_init(HazardMemo& hm, const StepParams& p, int tid) {
-  for (int i = tid; i < kMemoSlots * kMemoW; i += BLOCK) (&hm.e[0][0])[i] = ~0ull;  // tag 0xFFFFFFFF: stale
-  if (tid == 0) {
-    int next = 0;
-    for (int c = 0; c < FS_MAX_COMPARTMENTS; ++c) {
-      const bool costly = c < p.model.num_compartments && p.model.comp[c].hazard >= FS_HZ_LOGNORMAL;
-      hm.slot[c] = (costly && next < kMemoSlots) ? next++ : -1;
-    }
-  }
-}
 
 struct MergeParams {
   const int64_t* ro;
@@ -448,6 +431,7 @@ struct StepConst {
 template <int WARPS>
 struct StepShared {
   int succ[FS_MAX_COMPARTMENTS], term[FS_MAX_COMPARTMENTS], kind[FS_MAX_COMPARTMENTS];
+  int cslot[FS_MAX_COMPARTMENTS];  // cohort-table slot per compartment (-1: none / table off)
   double p0[FS_MAX_COMPARTMENTS], p1[FS_MAX_COMPARTMENTS];
   int cnt[FS_MAX_COMPARTMENTS];
   float wmax[WARPS];
@@ -467,6 +451,7 @@ __device__ __forceinline__ void load_tables(const StepParams& p, StepShared<WARP
     sh.p0[tid] = c.p0;
     sh.p1[tid] = c.p1;
     sh.cnt[tid] = 0;
+    sh.cslot[tid] = p.ctab ? p.cslot[tid] : -1;
   }
 }
 
@@ -541,6 +526,47 @@ __device__ __forceinline__ float inf_value(const StepParams& p, const StepConst&
 
 // phase B: settle `cnt` queued nodes of this warp, one per lane — rate
 // (pressure or hazard), uniform, Bernoulli, successor / age / infectivity
+// Cohort hazard table.  Every node that entered compartment c at step j
+// carries, at step k, the same age bits a_j(k) — all non-terminal nodes add
+// the same f32(tau) each step and round to the same storage type — hence the
+// same rate.  While step k runs, its CTAs prepare the table of step k+1: for
+// each live cohort j in (k+1-W, k], a_j(k+1) = round(a_j(k) + f32(tau_k))
+// (0 for the cohort entering at k) and the f64 hazard of every age-dependent
+// compartment at that age, tagged with k+1.  Step k+1 then looks rates up by
+// the node's entry step instead of evaluating the hazard.  Tags make stale or
+// never-prepared slots (engine start, host edits, other kernels) fall back to
+// direct evaluation; a cohort's age chain restarts only from a fresh cohort.
+// Results are bit-identical with or without the table.
+template <typename AT>
+__device__ __forceinline__ void cohort_prep(const StepParams& p, const StepConst& k, int tid, int nthreads_cta) {
+  const int par_c = (int)(k.step & 1), par_n = par_c ^ 1;
+  const uint32_t tag_c = (uint32_t)k.step, tag_n = (uint32_t)(k.step + 1);
+  for (int idx = (int)blockIdx.x + tid * (int)gridDim.x; idx < kCohortW; idx += nthreads_cta * (int)gridDim.x) {
+    const int64_t j = (k.step + 1) - (((k.step + 1) - idx) & (kCohortW - 1));  // cohort of slot idx at k+1
+    unsigned long long age_word = ~0ull;  // invalid
+    if (j == k.step) {
+      age_word = ((unsigned long long)tag_n << 32) | __float_as_uint(0.0f);  // fired this step: age 0
+    } else if (j < k.step) {
+      const unsigned long long cur = p.cage[par_c * kCohortW + idx];
+      if ((uint32_t)(cur >> 32) == tag_c) {  // its age at step k is known: advance it
+        const float a = to_f32<AT>(from_f32<AT>(__fadd_rn(__uint_as_float((uint32_t)cur), k.tau_f)));
+        age_word = ((unsigned long long)tag_n << 32) | __float_as_uint(a);
+      }
+    }
+    p.cage[par_n * kCohortW + idx] = age_word;
+    for (int sl = 0; sl < p.ncslots; ++sl) {
+      unsigned long long w = ~0ull;
+      if (age_word != ~0ull) {
+        const int c = p.cslot_comp[sl];
+        const fs_compartment& cc = p.model.comp[c];
+        const float r = nodal_rate(cc.hazard, cc.p0, cc.p1, __uint_as_float((uint32_t)age_word), p.hprec);
+        w = ((unsigned long long)tag_n << 32) | __float_as_uint(r);
+      }
+      p.ctab[((size_t)par_n * kCohortSlots + sl) * kCohortW + idx] = w;
+    }
+  }
+}
+
 // incremental counts: +-1 on node j's pending delta (buffer `nxt`), in this
 // device's memory or, node-partitioned, the owner's — possibly a peer GPU's
 // over NVLink.  Chunk boundaries are even, so the 16-bit lane
@@ -562,7 +588,7 @@ template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS 
 __device__ __forceinline__ void drain_entries(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh,
                                               const int* qn_node, const int* qn_state, const float* qn_age,
                                               const float* qn_press, int lane, int cnt, float& lmax,
-                                              uint32_t* mask_nxt, IT* inf_nxt, HazardMemo* hm = nullptr) {
+                                              uint32_t* mask_nxt, IT* inf_nxt) {
   __syncwarp();
   const bool ok = lane < cnt;
   int push = 0;  // +1 / -1: this node's infectious status changed
@@ -571,31 +597,27 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
   const float age = ok ? qn_age[lane] : 0.0f;
   float rate = 0.0f;
   bool compute = false;
-  unsigned long long* slot = nullptr;
   if (ok) {
     if (s == k.edge_from) {
       rate = qn_press[lane];
-    } else if (hm && hm->slot[s] >= 0) {
-      const int32_t j = p.entry[n];
-      const int64_t since = k.step - (int64_t)j;
+    } else {
       compute = true;
-      if (j != kEntryInvalid && since >= 0 && since < kMemoW) {
-        slot = &hm->e[hm->slot[s]][(uint32_t)j & (kMemoW - 1)];
-        const unsigned long long v = *reinterpret_cast<volatile unsigned long long*>(slot);
-        if ((uint32_t)(v >> 32) == (uint32_t)k.step) {
-          rate = __uint_as_float((uint32_t)v);
-          compute = false;
+      const int sl = sh.cslot[s];
+      if (sl >= 0) {  // the cohort table prepared by the previous step
+        const int32_t j = p.entry[n];
+        const int64_t since = k.step - (int64_t)j;
+        if (j != kEntryInvalid && since >= 1 && since < kCohortW) {
+          const unsigned long long v =
+              __ldg(p.ctab + ((size_t)(k.step & 1) * kCohortSlots + sl) * kCohortW + ((uint32_t)j & (kCohortW - 1)));
+          if ((uint32_t)(v >> 32) == (uint32_t)k.step) {
+            rate = __uint_as_float((uint32_t)v);
+            compute = false;
+          }
         }
       }
-    } else {
-      rate = nodal_rate(sh.kind[s], sh.p0[s], sh.p1[s], age, p.hprec);
     }
   }
-  if (compute) {
-    rate = nodal_rate(sh.kind[s], sh.p0[s], sh.p1[s], age, p.hprec);
-    // racing writers of one slot store identical bits
-    if (slot) *reinterpret_cast<volatile unsigned long long*>(slot) = ((unsigned long long)(uint32_t)k.step << 32) | __float_as_uint(rate);
-  }
+  if (compute) rate = nodal_rate(sh.kind[s], sh.p0[s], sh.p1[s], age, p.hprec);
   lmax = fmaxf(lmax, rate);
   bool fire = false;
   if (rate > 0.0f) {
@@ -657,10 +679,9 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
 // phase B on this warp's own queue
 template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true>
 __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
-                                            int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt,
-                                            HazardMemo* hm = nullptr) {
+                                            int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
   drain_entries<ST, AT, IT, MAT, WARPS, HUBS>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
-                                              sh.q_press[warp], lane, cnt, lmax, mask_nxt, inf_nxt, hm);
+                                              sh.q_press[warp], lane, cnt, lmax, mask_nxt, inf_nxt);
 }
 
 // phase A outcome of one tile (pressure already gathered): cheap outcomes
@@ -668,8 +689,7 @@ __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst
 template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true>
 __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
                                              int lane, uint32_t tile, uint32_t n, bool valid, int s, float age,
-                                             float pressure, int& qn, float& lmax, uint32_t* mask_nxt, IT* inf_nxt,
-                                             HazardMemo* hm = nullptr) {
+                                             float pressure, int& qn, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
   const bool isS = s == k.edge_from;
   const bool term = valid && sh.term[s] != 0;
   const bool defer = valid && !term && (!isS || pressure > 0.0f);
@@ -699,7 +719,7 @@ __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepCons
   }
   qn += __popc(dm);
   if (qn >= 32) {
-    drain_queue<ST, AT, IT, MAT, WARPS, HUBS>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt, hm);
+    drain_queue<ST, AT, IT, MAT, WARPS, HUBS>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt);
     if (lane < qn - 32) {
       sh.q_node[warp][lane] = sh.q_node[warp][32 + lane];
       sh.q_state[warp][lane] = sh.q_state[warp][32 + lane];
@@ -877,15 +897,9 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   constexpr int WARPS = BLOCK / 32;
   __shared__ StepShared<WARPS> sh;
   __shared__ StepConst s_k;
-  __shared__ typename std::conditional<MEMO, HazardMemo, char>::type s_hm;  // memo variant only
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_launch_dependents();
   load_tables<WARPS>(p, sh, tid);  // static model tables: before the dependency wait
-  HazardMemo* hmp = nullptr;
-  if constexpr (MEMO) {
-    memo_init<BLOCK>(s_hm, p, tid);
-    hmp = &s_hm;
-  }
   pdl_wait();
   if (tid == 0) {
     s_k = step_const(p, true);
@@ -942,9 +956,12 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
                                ? (p.ptab_mul ? __fmul_rn((float)c, p.ptab_c) : __ldg(p.ptab + c))
                                : 0.0f;
     tile_outcome<ST, AT, float, MAT, WARPS, HUBS>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure,
-                                                  qn, lmax, mask_nxt, nullptr, hmp);
+                                                  qn, lmax, mask_nxt, nullptr);
   }
-  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS, HUBS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr, hmp);
+  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS, HUBS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
+  // next step's cohort hazards: lane 0 of each warp prepares at most one slot
+  if constexpr (MEMO)
+    if (lane == 0) cohort_prep<AT>(p, k, warp, WARPS);
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
 
