@@ -88,7 +88,8 @@ class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,clocks.mem,power.draw,"
+         "power.limit,temperature.gpu")
 
     def __init__(self, index: int):
         self.index = index
@@ -124,8 +125,21 @@ class ClockSampler:
             for n, v in zip(names, parts[2:]):
                 if v.lower() == "active":
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        extra = {"mem_mhz": [], "power_w": [], "power_limit_w": [], "temp_c": []}
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            for key, v in zip(extra, parts[6:10]):
+                try:
+                    extra[key].append(float(v))
+                except ValueError:
+                    pass
+        # memory clock / power / temperature: the box-to-box spread of the
+        # HBM-bound numbers shows up here, not in the SM clock
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+               "samples": len(sm)}
+        for key, vals in extra.items():
+            out[key] = (max(vals) if key == "power_w" else statistics.median(vals)) if vals else None
+        return out
 
 
 def roofline_block(achieved: float, pk: dict, traffic, ms_per_step: float, b_alg: float) -> dict:

@@ -334,6 +334,54 @@ int fs_markov_refresh_rates(fs_markov* e, void* stream);
 /* R/markov.py:68-81 `influence_gather` of the current states (host f64[N]) */
 int fs_markov_influence(fs_markov* e, double* out, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Device-side trajectory records and ensemble analysis (SURVEY.md §8f row
+ * 4; the consumers of the per-step log).  Every pointer is device memory
+ * unless noted; all arithmetic is f64. */
+
+/* make_record (R/trajectory.py:31-61) for `trials` logs at once.  Trial t's
+ * log is times[t*max_steps + s], counts[(t*max_steps + s)*ncomp + c] for
+ * s < lens[t] (times non-decreasing, from 0).  grid f64[grid_points] is the
+ * reference's np.linspace(0, t_final, grid_points).  Writes fractions
+ * f64[trials][grid_points][ncomp] (grid-major, the memory order of the
+ * reference's Fortran-order record; = f64(count) / f64(num_nodes) of the last
+ * sample at or before each grid time, bit-identical to numpy) and, when
+ * i_idx / r_idx >= 0, summary f64[trials][3] = peak_I, grid time of the first
+ * peak, final_R (entries of an absent compartment are left untouched). */
+int fs_traj_records(const double* times, const int64_t* counts, const int64_t* lens, int64_t trials,
+                    int64_t max_steps, int32_t ncomp, const double* grid, int32_t grid_points,
+                    int64_t num_nodes, int32_t i_idx, int32_t r_idx, double* fractions, double* summary,
+                    void* stream);
+/* x f64[runs][cols] -> out f64[cols] = x.mean(axis=0) (R/analysis.py:137-138;
+ * sequential in run order, then / runs: bit-identical to numpy) */
+int fs_ensemble_mean(const double* x, int64_t runs, int64_t cols, double* out, void* stream);
+/* np.quantile(column, q, method="linear") of ncols columns of n values
+ * (value i of column c at x[i*row_stride + c*col_stride]), 1 <= n <= 16384.
+ * prev / next / gamma are HOST arrays of nq <= 8 entries: numpy's
+ * _get_indexes (-1 = last) and _get_gamma for each quantile.  out
+ * f64[nq][ncols]; numpy's _lerp, bit-identical (quantile_band
+ * R/analysis.py:141-148, _percentile_ci :160-162). */
+int fs_column_quantiles(const double* x, int64_t n, int64_t ncols, int64_t row_stride, int64_t col_stride,
+                        int32_t nq, const int64_t* prev, const int64_t* next, const double* gamma,
+                        double* out, void* stream);
+/* The resampling loop of fidelity (R/analysis.py:226-240): ensembles a
+ * f64[na][ncomp*grid_points], b f64[nb][...]; multinomial resample counts
+ * int64[resamples][na] / [resamples][nb] (the reference's
+ * _resample_weights draws, weights = count / n); per_run_peak / _final
+ * f64[na] (fs_run_deviation; ignored when i_idx / r_idx < 0);
+ * weights_scratch f64[resamples*(na+nb)].  samples f64[6][resamples]:
+ * l_inf, l2, err_peak_i, err_final_r, w.per_run_peak, w.per_run_final. */
+int fs_bootstrap_metrics(const double* a, int64_t na, const double* b, int64_t nb, int32_t ncomp,
+                         int32_t grid_points, const int64_t* counts_a, const int64_t* counts_b,
+                         int64_t resamples, int32_t i_idx, int32_t r_idx, const double* per_run_peak,
+                         const double* per_run_final, double* weights_scratch, double* samples,
+                         void* stream);
+/* per run i: peak_dev[i] = |max_g a[i][i_idx][g] - ref_peak|, final_dev[i] =
+ * |a[i][r_idx][G-1] - ref_final| (R/analysis.py:218-224; bit-identical) */
+int fs_run_deviation(const double* a, int64_t runs, int32_t ncomp, int32_t grid_points, int32_t i_idx,
+                     int32_t r_idx, double ref_peak, double ref_final, double* peak_dev, double* final_dev,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

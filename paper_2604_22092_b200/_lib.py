@@ -196,6 +196,13 @@ _SIGNATURES = {
     "fs_gen_regular": (_c_i32, [_c_i64, _c_i32, _c_u64, _c_i64, _c_i64, _vp, _vp, _c_i64, ctypes.POINTER(_c_i64), _vp]),
     "fs_gen_regular_row_host": (_c_i32, [_c_i64, _c_i32, _c_u64, _c_i64, _vp]),
     "fs_refresh_active": (_c_i32, [_vp, _c_i32, _c_i64, _vp, _c_i32, _vp, _c_i64, ctypes.POINTER(_c_i64), _vp]),
+    "fs_traj_records": (_c_i32, [_vp, _vp, _vp, _c_i64, _c_i64, _c_i32, _vp, _c_i32, _c_i64, _c_i32, _c_i32, _vp,
+                                 _vp, _vp]),
+    "fs_ensemble_mean": (_c_i32, [_vp, _c_i64, _c_i64, _vp, _vp]),
+    "fs_column_quantiles": (_c_i32, [_vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_i32, _vp, _vp, _vp, _vp, _vp]),
+    "fs_bootstrap_metrics": (_c_i32, [_vp, _c_i64, _vp, _c_i64, _c_i32, _c_i32, _vp, _vp, _c_i64, _c_i32, _c_i32,
+                                      _vp, _vp, _vp, _vp, _vp]),
+    "fs_run_deviation": (_c_i32, [_vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_f64, _c_f64, _vp, _vp, _vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

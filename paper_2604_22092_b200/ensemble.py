@@ -7,7 +7,8 @@ seeds `derive_seed(seed, trial)` and results ordered by trial
 GPU at the same time: every trial owns an engine on its own CUDA stream,
 the graph's device copy is shared, and the host loop keeps `concurrency`
 trials in flight, launching one CUDA-graph batch per trial per round and
-reading each trial's per-batch log as it lands.  Each trial is exactly
+reading each trial's per-batch log as it lands; the trajectory records
+of all trials are built by one device launch (analysis.make_records).  Each trial is exactly
 `run_renewal(g, m, cfg, derive_seed(seed, trial), ...)` (same kernels, same
 per-trial RNG keys), so the ensemble is bit-identical to the sequential one
 and to the reference's CPU ensemble (tests/test_ensemble.py).
@@ -23,7 +24,8 @@ import torch
 from . import _device
 from .renewal import RenewalConfig, _build_plan, _check_conservation, init_renewal_state
 from .rng import derive_seed
-from .trajectory import DEFAULT_GRID_POINTS, TrajectoryRecord, make_record
+from .analysis import make_records
+from .trajectory import DEFAULT_GRID_POINTS, TrajectoryRecord
 
 __all__ = ["run_ensemble"]
 
@@ -51,16 +53,16 @@ class _Trial:
         self.done += b
         self.clock = float(clocks[-1])
 
-    def record(self, g, m, t_final: float, grid_points: int) -> TrajectoryRecord:
+    def finish(self, t_final: float):
+        """(times, counts, summary) of the finished trial; the record itself
+        is built with every other trial's by one device launch."""
         wall = time.perf_counter() - self.t0
         t_arr = np.asarray(self.times)
         steps = min(int(np.searchsorted(t_arr, t_final, side="left")), self.done)
-        rec = make_record(t_arr, np.asarray(self.rows), m.compartments, g.num_nodes, t_final, grid_points,
-                          extra_summary={"step_count": steps, "wall_clock": wall, "engine": "renewal"})
         with torch.cuda.stream(self.stream):
             self.state._unbind()
         self.stream.synchronize()
-        return rec
+        return t_arr, np.asarray(self.rows), {"step_count": steps, "wall_clock": wall, "engine": "renewal"}
 
 
 def run_ensemble(engine: str, g, m, cfg, seed: int, t_final: float, runs: int,
@@ -76,7 +78,7 @@ def run_ensemble(engine: str, g, m, cfg, seed: int, t_final: float, runs: int,
     b = cfg.steps_per_batch
     free = [torch.cuda.Stream() for _ in range(max(1, min(concurrency, runs)))]
     plan = _build_plan(g, m, cfg, bool(cfg.mixed_precision))  # one device copy of the graph for every trial
-    out: list[TrajectoryRecord | None] = [None] * runs
+    out: list[tuple | None] = [None] * runs
     pending = list(range(runs))
     live: list[_Trial] = []
     torch.cuda.current_stream().synchronize()  # the graph upload precedes the trial streams
@@ -91,7 +93,8 @@ def run_ensemble(engine: str, g, m, cfg, seed: int, t_final: float, runs: int,
             if tr.clock < t_final:
                 still.append(tr)
             else:
-                out[tr.trial] = tr.record(g, m, t_final, grid_points)
+                out[tr.trial] = tr.finish(t_final)
                 free.append(tr.stream)
         live = still
-    return out  # type: ignore[return-value]
+    return make_records([(t, c) for t, c, _ in out], m.compartments, g.num_nodes, t_final, grid_points,
+                        [s for _, _, s in out])
