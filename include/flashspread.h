@@ -297,6 +297,21 @@ int fs_refresh_active(const void* states, int32_t states_dtype, int64_t n,
 int fs_gen_regular(int64_t n, int32_t k, uint64_t seed, int64_t row_lo, int64_t row_hi,
                    int64_t* row_offsets, int32_t* col, int64_t col_capacity, int64_t* num_edges,
                    void* stream);
+/* Barabási–Albert preferential attachment (the model of the reference's
+ * gen_barabasi_albert, R/graph.py:331-365: m-clique seed, each new node
+ * attaches to m distinct nodes drawn from the endpoint list) and G(N, p)
+ * with p = min(d_avg / (N-1), 1) (gen_erdos_renyi, R/graph.py:252-286), on
+ * the device with counter-based draws (csrc/fs_gen_random.cu).  Same
+ * output convention as fs_gen_regular: rows [row_lo, row_hi) of the
+ * symmetric incoming CSR, global column ids, slices sorted; col == NULL is
+ * the sizing call.  Deterministic for a seed; not the reference's numpy
+ * stream, so parity is by the model's properties (tests/test_graphgen.py). */
+int fs_gen_barabasi_albert(int64_t n, int32_t m, uint64_t seed, int64_t row_lo, int64_t row_hi,
+                           int64_t* row_offsets, int32_t* col, int64_t col_capacity, int64_t* num_edges,
+                           void* stream);
+int fs_gen_erdos_renyi(int64_t n, double d_avg, uint64_t seed, int64_t row_lo, int64_t row_hi,
+                       int64_t* row_offsets, int32_t* col, int64_t col_capacity, int64_t* num_edges,
+                       void* stream);
 /* host evaluation of one row of the same construction (tests); returns the
  * distinct degree and writes the sorted neighbours to out[k] */
 int fs_gen_regular_row_host(int64_t n, int32_t k, uint64_t seed, int64_t node, int32_t* out);

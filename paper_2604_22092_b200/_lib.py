@@ -194,6 +194,10 @@ _SIGNATURES = {
     "fs_hazard_eval": (_c_i32, [ctypes.POINTER(FsCompartment), _vp, _c_i64, _vp, _c_i32, _vp]),
     "fs_erfcx_eval": (_c_i32, [_vp, _c_i64, _vp, _vp]),
     "fs_gen_regular": (_c_i32, [_c_i64, _c_i32, _c_u64, _c_i64, _c_i64, _vp, _vp, _c_i64, ctypes.POINTER(_c_i64), _vp]),
+    "fs_gen_barabasi_albert": (_c_i32, [_c_i64, _c_i32, _c_u64, _c_i64, _c_i64, _vp, _vp, _c_i64,
+                                        ctypes.POINTER(_c_i64), _vp]),
+    "fs_gen_erdos_renyi": (_c_i32, [_c_i64, _c_f64, _c_u64, _c_i64, _c_i64, _vp, _vp, _c_i64,
+                                    ctypes.POINTER(_c_i64), _vp]),
     "fs_gen_regular_row_host": (_c_i32, [_c_i64, _c_i32, _c_u64, _c_i64, _vp]),
     "fs_refresh_active": (_c_i32, [_vp, _c_i32, _c_i64, _vp, _c_i32, _vp, _c_i64, ctypes.POINTER(_c_i64), _vp]),
     "fs_traj_records": (_c_i32, [_vp, _vp, _vp, _c_i64, _c_i64, _c_i32, _vp, _c_i32, _c_i64, _c_i32, _c_i32, _vp,

@@ -7,6 +7,8 @@ model needs ~100 GB / ~1 TB of host memory.
 HBM with ``fs_gen_regular`` (csrc/fs_graphgen.cu: union of keyed random
 Hamiltonian cycles), optionally only the rows
 [row_lo, row_hi) a rank of a node-partitioned run owns.
+``gen_barabasi_albert_device`` / ``gen_erdos_renyi_device`` do the same for
+the reference's other two models (csrc/fs_gen_random.cu).
 
 ``DeviceCsrGraph`` quacks like ``CsrGraph`` for the renewal API: the engine
 uses the device arrays as they are, and the host attributes
@@ -25,7 +27,8 @@ from . import _device, _lib
 from .errors import InfeasibleDegreeSequenceError, IndexOutOfRangeError
 from .graph import MAX_NODES, DegreeStats
 
-__all__ = ["DeviceCsrGraph", "gen_fixed_degree_device", "regular_row_host"]
+__all__ = ["DeviceCsrGraph", "gen_fixed_degree_device", "gen_barabasi_albert_device", "gen_erdos_renyi_device",
+           "regular_row_host"]
 
 
 class DeviceCsrGraph:
@@ -129,3 +132,46 @@ def regular_row_host(N: int, d: int, seed: int, node: int) -> np.ndarray:
     out = np.zeros(max(1, d), dtype=np.int32)
     k = _lib.check(lib.fs_gen_regular_row_host(N, d, seed & ((1 << 64) - 1), node, out.ctypes.data))
     return out[:k].copy()
+
+
+def _sized_generate(fn, args, N: int, row_lo: int, row_hi: int | None) -> DeviceCsrGraph:
+    """Sizing call (offsets + edge count), then the fill call."""
+    row_hi = N if row_hi is None else int(row_hi)
+    if not 0 <= row_lo <= row_hi <= N:
+        raise IndexOutOfRangeError("bad row range")
+    dev = _device.device()
+    st = _device.stream_handle(dev)
+    rows = row_hi - row_lo
+    ro = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+    e = ctypes.c_int64()
+    _lib.check(fn(*args, row_lo, row_hi, _lib.ptr(ro), None, 0, ctypes.byref(e), st))
+    ne = int(e.value)
+    col = torch.zeros(ne + 4, dtype=torch.int32, device=dev)
+    _lib.check(fn(*args, row_lo, row_hi, _lib.ptr(ro), _lib.ptr(col), ne, ctypes.byref(e), st))
+    d_max = int((ro[1:] - ro[:-1]).max().item()) if rows else 0
+    return DeviceCsrGraph(N, row_lo, rows, ne, ro, col, d_max)
+
+
+def gen_barabasi_albert_device(N: int, m: int, seed: int, row_lo: int = 0, row_hi: int | None = None) -> DeviceCsrGraph:
+    """Preferential attachment from an m-clique (the model of the reference's
+    gen_barabasi_albert, R/graph.py:331-365; same argument checks), built on
+    the device by fs_gen_barabasi_albert.  Same law, not the same numpy draw
+    stream: the graph differs from the reference's for the same seed."""
+    if N < 2 or N > MAX_NODES:
+        raise IndexOutOfRangeError("need 2 <= N <= 2^31-1")
+    if not (1 <= m < N):
+        raise InfeasibleDegreeSequenceError(f"need 1 <= m < N, got m={m}")
+    lib = _lib.load()
+    return _sized_generate(lib.fs_gen_barabasi_albert, (N, m, seed & ((1 << 64) - 1)), N, row_lo, row_hi)
+
+
+def gen_erdos_renyi_device(N: int, d_avg: float, seed: int, row_lo: int = 0, row_hi: int | None = None) -> DeviceCsrGraph:
+    """G(N, p), p = min(d_avg / (N-1), 1) (the model of the reference's
+    gen_erdos_renyi, R/graph.py:252-286; same argument checks), built on the
+    device by fs_gen_erdos_renyi."""
+    if N < 2 or N > MAX_NODES:
+        raise IndexOutOfRangeError("need N >= 2")
+    if d_avg < 0:
+        raise ValueError("d_avg must be >= 0")
+    lib = _lib.load()
+    return _sized_generate(lib.fs_gen_erdos_renyi, (N, float(d_avg), seed & ((1 << 64) - 1)), N, row_lo, row_hi)

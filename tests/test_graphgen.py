@@ -85,3 +85,117 @@ def test_engine_on_generated_graph_matches_oracle():
         assert np.array_equal(st.ages.view(np.uint16 if mixed else np.uint32),
                               ref.ages.view(np.uint16 if mixed else np.uint32))
         assert st.clock == ref.clock
+
+
+# ---------------------------------------------------- BA and G(N, p) (fs_gen_random.cu) --
+
+def _structure_checks(h, n):
+    ro, col = h.row_offsets, h.col_indices
+    src = np.repeat(np.arange(n), np.diff(ro))
+    assert np.all(col >= 0) and np.all(col < n)
+    assert not np.any(src == col)                                         # no self-loops
+    for i in range(0, n, max(1, n // 500)):                               # sorted, no duplicates
+        r = col[ro[i]:ro[i + 1]]
+        assert np.all(r[1:] > r[:-1])
+    fwd = src.astype(np.int64) * n + col
+    bwd = col.astype(np.int64) * n + src
+    assert np.array_equal(np.sort(fwd), np.sort(bwd))                     # symmetric
+    return src, col
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m", [(20_000, 5), (3_000, 1), (500, 3), (2, 1), (64, 63)])
+def test_ba_device_structure(n, m):
+    g = fs.gen_barabasi_albert_device(n, m, seed=4)
+    h = g.to_host()
+    assert g.num_edges == 2 * ((n - m) * m + m * (m - 1) // 2)           # the reference's edge count
+    src, col = _structure_checks(h, n)
+    earlier = np.bincount(src[col < src], minlength=n)                   # each new node attaches to m
+    assert np.all(earlier[m:] == m)
+    assert np.all(earlier[:m] == np.arange(m))                           # the m-clique seed
+    again = fs.gen_barabasi_albert_device(n, m, seed=4).to_host()
+    assert np.array_equal(again.col_indices, h.col_indices)              # deterministic for a seed
+
+
+@pytest.mark.gpu
+def test_ba_device_degree_law_matches_reference_generator():
+    """Same attachment law as the reference's generator (host port):
+    degree-m fraction (BA theory 2/(m+2)), mean log-degree, hub sizes."""
+    n, m = 20_000, 5
+    dev = np.diff(fs.gen_barabasi_albert_device(n, m, seed=1).row_offsets)
+    ref = np.diff(fs.gen_barabasi_albert(n, m, seed=1).row_offsets)
+    assert dev.sum() == ref.sum() and dev.min() == ref.min() == m
+    assert abs(np.mean(dev == m) - np.mean(ref == m)) < 0.02
+    assert abs(np.mean(np.log(dev)) - np.mean(np.log(ref))) < 0.02
+    top_d, top_r = np.sort(dev)[-20:].mean(), np.sort(ref)[-20:].mean()
+    assert 0.5 < top_d / top_r < 2.0
+    # CCDF tail exponent ~ 2 for both (P(k >= x) ~ x^-2)
+    for d in (dev, ref):
+        f1, f2 = np.mean(d >= 20), np.mean(d >= 80)
+        assert 10 < f1 / f2 < 24
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,d", [(20_000, 8.0), (3_001, 2.5), (50, 100.0), (10, 0.0), (1_000, 999.0)])
+def test_er_device_structure_and_law(n, d):
+    g = fs.gen_erdos_renyi_device(n, d, seed=6)
+    h = g.to_host()
+    p = min(d / (n - 1), 1.0)
+    pairs = n * (n - 1) // 2
+    if p >= 1.0:
+        assert g.num_edges == 2 * pairs
+    elif p == 0.0:
+        assert g.num_edges == 0
+    else:
+        mu, sd = pairs * p, np.sqrt(pairs * p * (1 - p))
+        assert abs(g.num_edges / 2 - mu) < 6 * sd
+    if g.num_edges:
+        _structure_checks(h, n)
+    if 0 < p < 1 and n >= 3000:
+        deg = np.diff(h.row_offsets)
+        assert abs(deg.var() / deg.mean() - (1 - p)) < 0.1                # binomial degrees
+    again = fs.gen_erdos_renyi_device(n, d, seed=6).to_host()
+    assert np.array_equal(again.col_indices, h.col_indices)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["ba", "er"])
+def test_random_generators_partition_slices(kind):
+    n = 30_000
+    gen = (lambda **kw: fs.gen_barabasi_albert_device(n, 5, seed=2, **kw)) if kind == "ba" else \
+          (lambda **kw: fs.gen_erdos_renyi_device(n, 10.0, seed=2, **kw))
+    whole = gen().to_host()
+    cuts = [0, 7_168, 19_456, n]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        part = gen(row_lo=lo, row_hi=hi)
+        assert np.array_equal(part.row_offsets + whole.row_offsets[lo], whole.row_offsets[lo:hi + 1])
+        assert np.array_equal(part.col_indices, whole.col_indices[whole.row_offsets[lo]:whole.row_offsets[hi]])
+
+
+@pytest.mark.gpu
+def test_engine_on_device_ba_graph_matches_oracle():
+    """C3's graph family built on the device: the merge-strategy engine
+    (hub rows) is bit-exact against the oracle on it."""
+    from oracle import spreadsim_port as O
+
+    g = fs.gen_barabasi_albert_device(20_000, 5, seed=1)
+    h = g.to_host()
+    m = fs.seir_weibull_erlang(0.25)
+    cfg = fs.RenewalConfig()
+    st = fs.init_renewal_state(g, m, cfg, 7)
+    ref = O.init_state(h, m, cfg, 7)
+    for _ in range(2):
+        fs.run_batch(st, g, m, cfg, 7)
+        O.run_batch(ref, h, m, cfg, 7)
+    assert np.array_equal(st.counts, ref.counts)
+    assert np.array_equal(st.states.astype(np.int32), ref.states.astype(np.int32))
+    assert np.array_equal(st.ages.view(np.uint32), ref.ages.view(np.uint32))
+    assert st.clock == ref.clock
+
+
+@pytest.mark.parametrize("fn,args", [("gen_barabasi_albert_device", (10, 10)), ("gen_barabasi_albert_device", (10, 0)),
+                                     ("gen_barabasi_albert_device", (1, 1)), ("gen_erdos_renyi_device", (1, 2.0)),
+                                     ("gen_erdos_renyi_device", (10, -1.0))])
+def test_random_generator_argument_checks(fn, args):
+    with pytest.raises((fs.errors.GraphError, ValueError)):
+        getattr(fs, fn)(*args, seed=0)
