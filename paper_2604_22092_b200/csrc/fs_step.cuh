@@ -898,6 +898,14 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   __shared__ StepShared<WARPS> sh;
   __shared__ StepConst s_k;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#if FS_STEP_PROBE  // build with -DFS_STEP_PROBE=1 and run with FS_DEBUG_TIMES=1 (scripts/cta_times_incr.py)
+  __shared__ unsigned long long s_entry;
+  if (p.dbg && tid == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    s_entry = now;
+  }
+#endif
   pdl_launch_dependents();
   load_tables<WARPS>(p, sh, tid);  // static model tables: before the dependency wait
   pdl_wait();
@@ -930,6 +938,17 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   }
   __syncthreads();
   const StepConst& k = s_k;  // read from shared memory where used: keeps the hot loop's registers free
+#if FS_STEP_PROBE  // per-CTA stamps [smid | entry, work end, constants ready, finish]
+  if (p.dbg && tid == 0) {
+    unsigned long long now;
+    unsigned sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    unsigned long long* dbg = p.dbg + ((size_t)(k.step & 15) * gridDim.x + blockIdx.x) * 4;
+    dbg[0] = ((unsigned long long)sm << 48) | (s_entry & 0xFFFFFFFFFFFFull);
+    dbg[2] = now;
+  }
+#endif
   const int cur = (int)(k.step & 1);
   uint32_t* mask_nxt = p.mask[cur ^ 1];
   uint16_t* __restrict__ pend = reinterpret_cast<uint16_t*>(p.pend[cur]);
@@ -962,7 +981,21 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   // next step's cohort hazards: lane 0 of each warp prepares at most one slot
   if constexpr (MEMO)
     if (lane == 0) cohort_prep<AT>(p, k, warp, WARPS);
+#if FS_STEP_PROBE
+  if (p.dbg && lane == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    atomicMax(p.dbg + ((size_t)(k.step & 15) * gridDim.x + blockIdx.x) * 4 + 1, now);
+  }
+#endif
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
+#if FS_STEP_PROBE
+  if (p.dbg && tid == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    p.dbg[((size_t)(k.step & 15) * gridDim.x + blockIdx.x) * 4 + 3] = now;
+  }
+#endif
 }
 
 // thread-per-node count over a slice staged in shared memory: lane-private
