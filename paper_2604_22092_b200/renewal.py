@@ -24,6 +24,7 @@ shared library or a CUDA device every entry point raises
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass
 
@@ -864,7 +865,9 @@ def run_renewal(g, m, cfg: RenewalConfig, seed: int, t_final: float, grid_points
     times = [0.0]
     rows = [state.counts.copy()]
     done, clock = 0, 0.0
+    trace = [] if os.environ.get("FS_E2E_TRACE") else None  # per-batch wall times (diagnostics)
     while clock < t_final:
+        tb = time.perf_counter()
         eng.run_batch(materialize=False)
         clocks, _, counts = eng.read_log(done, b)
         _check_conservation(counts, state._n)
@@ -872,10 +875,18 @@ def run_renewal(g, m, cfg: RenewalConfig, seed: int, t_final: float, grid_points
         rows.extend(counts)
         done += b
         clock = float(clocks[-1])
+        if trace is not None:
+            trace.append(round((time.perf_counter() - tb) * 1e3, 2))
     wall = time.perf_counter() - t0
     t_arr = np.asarray(times)
     steps = min(int(np.searchsorted(t_arr, t_final, side="left")), done)
     rec = make_record(t_arr, np.asarray(rows), m.compartments, g.num_nodes, t_final, grid_points,
                       extra_summary={"step_count": steps, "wall_clock": wall, "engine": "renewal", "setup_s": setup})
+    if trace is not None:
+        rec.summary["batch_ms"] = trace
+        tu = time.perf_counter()
     state._unbind()
+    if trace is not None:
+        rec.summary["record_ms"] = round((tu - t0 - wall) * 1e3, 2)
+        rec.summary["unbind_ms"] = round((time.perf_counter() - tu) * 1e3, 2)
     return rec
