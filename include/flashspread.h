@@ -181,6 +181,11 @@ typedef struct fs_engine fs_engine;
 int fs_abi_version(void);
 const char* fs_last_error(void);
 int fs_device_sm_count(int device);
+/* page-lock / release a host range (cudaHostRegister): host CSR arrays are
+ * registered once per graph so every later upload is a direct DMA and the
+ * pages cannot be reclaimed between runs (paper_2604_22092_b200/renewal.py) */
+int fs_host_register(void* p, int64_t bytes);
+int fs_host_unregister(void* p);
 
 /* Engine: renewal.py:321-355 `_build_plan` + the device side of
  * `init_renewal_state` (370-410).  Reads `*scal` (host) as the initial

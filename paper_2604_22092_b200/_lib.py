@@ -148,6 +148,8 @@ _SIGNATURES = {
     "fs_abi_version": (_c_i32, []),
     "fs_last_error": (ctypes.c_char_p, []),
     "fs_device_sm_count": (_c_i32, [_c_i32]),
+    "fs_host_register": (_c_i32, [_vp, _c_i64]),
+    "fs_host_unregister": (_c_i32, [_vp]),
     "fs_engine_create": (_c_i32, [ctypes.POINTER(FsGraph), ctypes.POINTER(FsModel), ctypes.POINTER(FsConfig),
                                    ctypes.POINTER(FsStateBuffers), ctypes.POINTER(FsScalars), _c_i32,
                                    ctypes.POINTER(_vp)]),

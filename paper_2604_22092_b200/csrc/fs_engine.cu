@@ -562,6 +562,25 @@ int fs_device_sm_count(int device) {
   return v;
 }
 
+int fs_host_register(void* p, int64_t bytes) {
+  if (!p || bytes <= 0) return set_error(FS_EINVAL, "fs_host_register: empty range");
+  const cudaError_t e = cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(FS_ECUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
+  }
+  return 0;
+}
+
+int fs_host_unregister(void* p) {
+  const cudaError_t e = cudaHostUnregister(p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(FS_ECUDA, "cudaHostUnregister: %s", cudaGetErrorString(e));
+  }
+  return 0;
+}
+
 static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, const fs_state_buffers* buf,
                          const fs_scalars* scal, int device, const fs_partition* part, fs_engine** out) {
   if (!g || !m || !c || !buf || !scal || !out) return set_error(FS_EINVAL, "null argument");
