@@ -892,6 +892,9 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
 // Phase B (the deferral queue: hazards, uniforms, Bernoulli, pushes) is the
 // same as k_step's.
 // ---------------------------------------------------------------------------
+#ifndef FS_PF_DEPTH
+#define FS_PF_DEPTH 2
+#endif
 template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   constexpr int WARPS = BLOCK / 32;
@@ -930,11 +933,15 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   // the first two tiles' loads need only the buffer parity, which the host
   // knows: they overlap thread 0's scalar reads instead of waiting for them
   uint32_t t = blockIdx.x * WARPS + warp;
-  In in0{}, in1{};
+  constexpr int PD = FS_PF_DEPTH;  // tiles in flight per warp (register ring, compile-time indices)
+  In inq[PD];
+#pragma unroll
+  for (int i = 0; i < PD; ++i) inq[i] = In{};
   if (p.host_parity >= 0) {
     const uint16_t* pend_h = reinterpret_cast<const uint16_t*>(p.pend[p.host_parity & 1]);
-    if (t < ntiles) load(t, pend_h, in0);
-    if (t + stride < ntiles) load(t + stride, pend_h, in1);
+#pragma unroll
+    for (int i = 0; i < PD; ++i)
+      if (t + i * stride < ntiles) load(t + i * stride, pend_h, inq[i]);
   }
   __syncthreads();
   const StepConst& k = s_k;  // read from shared memory where used: keeps the hot loop's registers free
@@ -953,15 +960,17 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   uint32_t* mask_nxt = p.mask[cur ^ 1];
   uint16_t* __restrict__ pend = reinterpret_cast<uint16_t*>(p.pend[cur]);
   if (cur != p.host_parity) {  // no host mirror, or out of step: load now
-    if (t < ntiles) load(t, pend, in0);
-    if (t + stride < ntiles) load(t + stride, pend, in1);
+#pragma unroll
+    for (int i = 0; i < PD; ++i)
+      if (t + i * stride < ntiles) load(t + i * stride, pend, inq[i]);
   }
   float lmax = 0.0f;
   int qn = 0;
   for (; t < ntiles; t += stride) {
-    const In in = in0;
-    in0 = in1;
-    if (t + 2 * stride < ntiles) load(t + 2 * stride, pend, in1);
+    const In in = inq[0];
+#pragma unroll
+    for (int i = 0; i < PD - 1; ++i) inq[i] = inq[i + 1];
+    if (t + PD * stride < ntiles) load(t + PD * stride, pend, inq[PD - 1]);
     const uint32_t n = t * 32u + (uint32_t)lane;
     const bool valid = n < N;
     uint32_t c = in.c;
