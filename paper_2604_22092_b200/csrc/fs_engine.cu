@@ -808,8 +808,8 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   if (getenv("FS_NO_PDL")) e->pdl = false;
   if (getenv("FS_DEBUG_TIMES")) {
     const size_t g = (size_t)std::max(std::max(e->step_grid, e->step_grid_general), e->stream_grid);
-    TRY(dalloc(&e->dbg, g * 4 * 16));
-    FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * g * 4 * 16));
+    TRY(dalloc(&e->dbg, g * (4 + 32) * 16));  // per-CTA block, then the per-warp block of the probe build
+    FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * g * (4 + 32) * 16));
   }
   FS_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
   FS_CUDA(cudaGetLastError());
@@ -1267,7 +1267,7 @@ extern "C" int fs_engine_debug_times(fs_engine* e, unsigned long long* out, int3
   const int n = e->stream ? e->stream_grid : e->step_grid;  // [16 steps][grid][4] of the kernel in use
   if (max_ctas < n) return set_error(FS_EINVAL, "fs_engine_debug_times: need room for %d CTAs", n);
   FS_CUDA(cudaDeviceSynchronize());
-  FS_CUDA(cudaMemcpy(out, e->dbg, sizeof(unsigned long long) * 4 * 16 * n, cudaMemcpyDeviceToHost));
-  FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * 4 * 16 * n));
+  FS_CUDA(cudaMemcpy(out, e->dbg, sizeof(unsigned long long) * (4 + 32) * 16 * n, cudaMemcpyDeviceToHost));
+  FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * (4 + 32) * 16 * n));
   return n;
 }

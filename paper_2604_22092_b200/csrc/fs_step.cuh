@@ -658,15 +658,34 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
       e1 = __ldg(p.out_ro + n + 1);
     }
     const bool wide = HUBS && p.hubs && push && (e1 - e0 > 32);
-    if (push && !wide)
-      for (int64_t e = e0; e < e1; ++e) push_delta(p, nxt, __ldg(p.out_col + e), push > 0);
+    // column loads are batched ahead of their atomics: a load-then-push loop
+    // would wait one memory round trip per edge (each push needs its column)
+    constexpr int kPB = 8;
+    if (push && !wide) {
+      for (int64_t b = e0; b < e1; b += kPB) {
+        int32_t cj[kPB];
+#pragma unroll
+        for (int j = 0; j < kPB; ++j) cj[j] = (b + j < e1) ? __ldg(p.out_col + b + j) : -1;
+#pragma unroll
+        for (int j = 0; j < kPB; ++j)
+          if (cj[j] >= 0) push_delta(p, nxt, cj[j], push > 0);
+      }
+    }
     unsigned wides = HUBS ? __ballot_sync(kFull, wide) : 0u;
     while (HUBS && wides) {
       const int src = __ffs(wides) - 1;
       wides &= wides - 1;
       const int64_t a0 = __shfl_sync(kFull, e0, src), a1 = __shfl_sync(kFull, e1, src);
       const bool up = __shfl_sync(kFull, push, src) > 0;
-      for (int64_t e = a0 + lane; e < a1; e += 32) push_delta(p, nxt, __ldg(p.out_col + e), up);
+      constexpr int kHB = 4;  // 4 x 32 edges of the hub row in flight per round
+      for (int64_t b = a0 + lane; b < a1; b += 32 * kHB) {
+        int32_t cj[kHB];
+#pragma unroll
+        for (int j = 0; j < kHB; ++j) cj[j] = (b + 32 * j < a1) ? __ldg(p.out_col + b + 32 * j) : -1;
+#pragma unroll
+        for (int j = 0; j < kHB; ++j)
+          if (cj[j] >= 0) push_delta(p, nxt, cj[j], up);
+      }
     }
     // partitioned: the pushes into peer GPUs' memory are ordered before
     // anything this thread's rank does next — in particular before the NCCL
@@ -966,6 +985,9 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   }
   float lmax = 0.0f;
   int qn = 0;
+#if FS_STEP_PROBE
+  int pr_def = 0, pr_drains = 0;
+#endif
   for (; t < ntiles; t += stride) {
     const In in = inq[0];
 #pragma unroll
@@ -983,10 +1005,27 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     const float pressure = (valid && (s == k.edge_from || MAT))
                                ? (p.ptab_mul ? __fmul_rn((float)c, p.ptab_c) : __ldg(p.ptab + c))
                                : 0.0f;
+#if FS_STEP_PROBE
+    const int q0 = qn;
+#endif
     tile_outcome<ST, AT, float, MAT, WARPS, HUBS>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure,
                                                   qn, lmax, mask_nxt, nullptr);
+#if FS_STEP_PROBE
+    pr_def += qn - q0 + (qn < q0 ? 32 : 0);
+    pr_drains += qn < q0;
+#endif
   }
   if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS, HUBS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
+#if FS_STEP_PROBE  // per-warp [phase end, deferred << 20 | mid-loop drains] after the per-CTA block
+  if (p.dbg && lane == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    unsigned long long* w = p.dbg + (size_t)16 * gridDim.x * 4 +
+                            (((size_t)(k.step & 15) * gridDim.x + blockIdx.x) * 32 + (size_t)warp * 2);
+    w[0] = now;
+    w[1] = ((unsigned long long)pr_def << 20) | (unsigned long long)(pr_drains + (qn > 0 ? 1 : 0));
+  }
+#endif
   // next step's cohort hazards: lane 0 of each warp prepares at most one slot
   if constexpr (MEMO)
     if (lane == 0) cohort_prep<AT>(p, k, warp, WARPS);

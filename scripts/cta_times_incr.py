@@ -20,7 +20,7 @@ st = fs.init_renewal_state(g, m, cfg, 7)
 plan = R._build_plan(g, m, cfg, cfg.mixed_precision)
 eng = st._bind(plan, 7, False)
 eng.step(10, False, False)
-buf = np.zeros((16, 2048, 4), dtype=np.uint64)
+buf = np.zeros(16 * 2048 * 36, dtype=np.uint64)
 lib.fs_engine_debug_times(eng.handle, buf.ctypes.data, 2048)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 flush_rd = torch.ones(128 << 20, dtype=torch.int32, device="cuda")
@@ -32,7 +32,8 @@ for k in range(16):
     ev.append((a, b))
 torch.cuda.synchronize()
 grid = lib.fs_engine_debug_times(eng.handle, buf.ctypes.data, 2048)
-b = buf[:, :grid, :].astype(np.int64)
+b = buf[: 16 * grid * 4].reshape(16, grid, 4).astype(np.int64)
+wb = buf[16 * grid * 4: 16 * grid * 36].reshape(16, grid, 16, 2).astype(np.int64)
 smid = (b[:, :, 0] >> 48)
 b[:, :, 0] &= (1 << 48) - 1
 ms = [x.elapsed_time(y) * 1e3 for x, y in ev]
@@ -80,3 +81,25 @@ sms = sorted(per_sm)
 print("SM ids %d..%d; mean duration by SM id decile:" % (sms[0], sms[-1]),
       [round(float(np.mean([np.mean(per_sm[x]) for x in sms[i:i + 15]])), 2) for i in range(0, len(sms), 15)])
 print("slowest by duration:", [(int(i), int(sm0[i]), round(float(dm[i]), 2)) for i in np.argsort(dm)[-10:]])
+
+# per warp: phase end relative to the CTA's constants-ready stamp, deferred nodes, drains
+WE, WD, WN = [], [], []
+for s_ in range(16):
+    if b[s_, :, 0].min() == 0:
+        continue
+    WE.append((wb[s_, :, :, 0] - b[s_, :, 2][:, None]) / 1e3)
+    WD.append(wb[s_, :, :, 1] >> 20)
+    WN.append(wb[s_, :, :, 1] & 0xFFFFF)
+WE, WD, WN = np.array(WE), np.array(WD), np.array(WN)
+print("warp phase end (us after constants) p10 %.2f p50 %.2f p90 %.2f max %.2f" % tuple(np.percentile(WE, [10, 50, 90, 100])))
+print("deferred per warp p10 %d p50 %d p90 %d max %d; drains p50 %d max %d" % (*np.percentile(WD, [10, 50, 90, 100]), np.median(WN), WN.max()))
+for d in range(int(WN.max()) + 1):
+    sel = WN == d
+    if sel.any():
+        print(f"  drains={d}: warps {sel.mean()*100:.1f}%  phase end mean {WE[sel].mean():.2f} us")
+cta_end = WE.max(axis=2)
+slow = cta_end > np.percentile(cta_end, 90)
+print("slowest-10%% CTAs: mean deferred/warp %.1f vs others %.1f; max drains/warp %.2f vs %.2f" % (
+    WD.mean(axis=2)[slow].mean(), WD.mean(axis=2)[~slow].mean(), WN.max(axis=2)[slow].mean(), WN.max(axis=2)[~slow].mean()))
+c = np.corrcoef(WE.reshape(-1), WD.reshape(-1))[0, 1]
+print("corr(warp phase end, deferred) %.2f" % c)
