@@ -278,6 +278,7 @@ struct fs_engine {
   bool pdl = true;        // programmatic dependent launch between steps
   int tma_block = 512;    // threads per CTA of the streaming kernel
   unsigned long long* dbg = nullptr;  // FS_DEBUG_TIMES: per-CTA timestamps
+  bool delta_ipc = false;             // delta buffers from cudaMalloc (exported over CUDA IPC)
   int step_block = 512, step_grid = 0, step_grid_general = 0;
   size_t step_smem = 0, step_smem_general = 0;
   MergeFn merge_fn = nullptr;
@@ -330,10 +331,26 @@ namespace {
                        __FILE__, __LINE__);                                                   \
   } while (0)
 
+// Engine scratch comes from the device's stream-ordered pool, kept (not
+// released to the driver) between engines: creating an engine per run
+// (run_renewal, ensemble trials) then costs no cudaMalloc / cudaFree
+// round trips.  Buffers exported over CUDA IPC use plain cudaMalloc.
+static void keep_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    unsigned long long keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[device] = true;
+}
+
 template <typename T>
-int dalloc(T** p, size_t count) {
+int dalloc(T** p, size_t count, bool ipc = false) {
   if (count == 0) count = 1;
-  cudaError_t err = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  cudaError_t err = ipc ? cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T))
+                        : cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), (cudaStream_t)0);
   if (err != cudaSuccess) return set_error(FS_ENOMEM, "cudaMalloc(%zu B): %s", count * sizeof(T), cudaGetErrorString(err));
   return 0;
 }
@@ -585,6 +602,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
                          const fs_scalars* scal, int device, const fs_partition* part, fs_engine** out) {
   if (!g || !m || !c || !buf || !scal || !out) return set_error(FS_EINVAL, "null argument");
   *out = nullptr;
+  keep_pool(device);
   if (g->num_nodes < 1 || g->num_nodes > 2147483647LL) return set_error(FS_EINVAL, "num_nodes %lld outside [1, 2^31-1]", (long long)g->num_nodes);
   if (m->num_compartments < 1 || m->num_compartments > FS_MAX_COMPARTMENTS)
     return set_error(FS_EINVAL, "num_compartments %d outside [1, %d]", m->num_compartments, FS_MAX_COMPARTMENTS);
@@ -697,7 +715,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     k_max_tile_span<<<(int)std::min<int64_t>((e->ntiles + 255) / 256, 4096), 256>>>(g->row_offsets32, n, e->ntiles, d_span);
     unsigned long long span = 0;
     FS_CUDA(cudaMemcpy(&span, d_span, sizeof(span), cudaMemcpyDeviceToHost));
-    cudaFree(d_span);
+    cudaFreeAsync(d_span, (cudaStream_t)0);
     TmaLayout L{};
     L.ro_off = L.st_off = L.ag_off = L.col_off = 0;  // slots hold the column slice only
     L.col_cap = (int)std::min<unsigned long long>(span, 1ull << 20);
@@ -774,8 +792,9 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   if (e->incr) {
     const size_t cap = (size_t)((n + 127) / 128) * 128;  // whole 128-node stream units
     TRY(dalloc(&e->cnt, cap));
-    TRY(dalloc(&e->delta[0], cap / 2));
-    TRY(dalloc(&e->delta[1], cap / 2));
+    e->delta_ipc = e->world > 1 || part != nullptr;  // peers map these over CUDA IPC
+    TRY(dalloc(&e->delta[0], cap / 2, e->delta_ipc));
+    TRY(dalloc(&e->delta[1], cap / 2, e->delta_ipc));
     TRY(recount(e, scal->step, nullptr));
     // streaming kernel: per-node arrays readable to a multiple of 128 nodes
     if (buf->padded >= 2 && !getenv("FS_NO_STREAM")) {
@@ -789,13 +808,19 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   }
   {
     // hazard memo for models with age-dependent holding times
-    bool costly = false;
-    for (int c2 = 0; c2 < m->num_compartments; ++c2) costly |= m->comp[c2].hazard >= FS_HZ_LOGNORMAL;
-    // the cohort table is prepared by the incremental step kernel; its
-    // preparation adds ~2 us to a step, so it is on where steps are long
-    // (N >= 4M: C4, C5) and off at N ~ 1e6
+    bool costly = false, lognormal = false;
+    for (int c2 = 0; c2 < m->num_compartments; ++c2) {
+      costly |= m->comp[c2].hazard >= FS_HZ_LOGNORMAL;
+      lognormal |= m->comp[c2].hazard == FS_HZ_LOGNORMAL;
+    }
+    // the cohort table is prepared inside the step kernel's final drains
+    // (an idle lane, the same hazard call: DESIGN.md §3.3).  It replaces the
+    // f64 hazard of every queued E / I node by a lookup: a win for the
+    // log-normal hazard (erfc / exp / log chain) at every size — C2 full run
+    // -30 % step time, early window -1.5 % — and for the cheaper Weibull /
+    // Erlang hazards only where steps are long (N >= 4M)
     const char* mv = getenv("FS_MEMO");
-    const bool want = mv ? atoi(mv) != 0 : (e->stream && n >= (int64_t)4 * 1024 * 1024);
+    const bool want = mv ? atoi(mv) != 0 : (e->stream && (lognormal || n >= (int64_t)4 * 1024 * 1024));
     if (costly && want && !getenv("FS_NO_MEMO")) {
       TRY(dalloc(&e->entry, (size_t)((n + 127) / 128) * 128));
       TRY(dalloc(&e->ctab, (size_t)2 * kCohortSlots * kCohortW));
@@ -838,10 +863,17 @@ void fs_engine_destroy(fs_engine* e) {
     for (auto& b : a)
       for (auto& x : b) if (x) cudaGraphExecDestroy(x);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+  cudaDeviceSynchronize();  // no kernel of this engine is still in flight on any stream
   void* ptrs[] = {e->dstate, e->acc, e->log_clock, e->log_tau, e->log_counts, e->ptab,
                   e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag,
-                  e->cnt, e->delta[0], e->delta[1], e->entry, e->ctab, e->cage};
-  for (void* q : ptrs) if (q) cudaFree(q);
+                  e->cnt, e->entry, e->ctab, e->cage, e->dbg};
+  for (void* q : ptrs) if (q) cudaFreeAsync(q, (cudaStream_t)0);
+  for (void* q : {(void*)e->delta[0], (void*)e->delta[1]})
+    if (q) {
+      if (e->delta_ipc) cudaFree(q);
+      else cudaFreeAsync(q, (cudaStream_t)0);
+    }
+  cudaStreamSynchronize((cudaStream_t)0);
   delete e;
 }
 

@@ -588,7 +588,7 @@ template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS 
 __device__ __forceinline__ void drain_entries(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh,
                                               const int* qn_node, const int* qn_state, const float* qn_age,
                                               const float* qn_press, int lane, int cnt, float& lmax,
-                                              uint32_t* mask_nxt, IT* inf_nxt) {
+                                              uint32_t* mask_nxt, IT* inf_nxt, int prep = -1) {
   __syncwarp();
   const bool ok = lane < cnt;
   int push = 0;  // +1 / -1: this node's infectious status changed
@@ -617,7 +617,51 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
       }
     }
   }
-  if (compute) rate = nodal_rate(sh.kind[s], sh.p0[s], sh.p1[s], age, p.hprec);
+  // cohort-table preparation rides in lane 31 of a warp's final drain
+  // (never a queued lane there: a final queue holds < 32 entries), through the
+  // same hazard call, so it adds no latency.  Pair `prep` = (slot sl, cohort
+  // idx) of step k+1's table (see cohort_prep).
+  const bool prep_lane = prep >= 0 && lane == 31;
+  int hk = 0;
+  double hp0 = 0.0, hp1 = 0.0;
+  float ha = 0.0f;
+  unsigned long long prep_age = ~0ull;
+  if (compute) {
+    hk = sh.kind[s];
+    hp0 = sh.p0[s];
+    hp1 = sh.p1[s];
+    ha = age;
+  }
+  if (prep_lane) {
+    const int idx = prep & (kCohortW - 1), sl = prep / kCohortW;
+    const int par_c = (int)(k.step & 1);
+    const int64_t j = (k.step + 1) - (((k.step + 1) - idx) & (kCohortW - 1));
+    if (j == k.step) {
+      prep_age = ((unsigned long long)(uint32_t)(k.step + 1) << 32) | __float_as_uint(0.0f);
+    } else if (j < k.step) {
+      const unsigned long long cur = p.cage[par_c * kCohortW + idx];
+      if ((uint32_t)(cur >> 32) == (uint32_t)k.step)
+        prep_age = ((unsigned long long)(uint32_t)(k.step + 1) << 32) |
+                   __float_as_uint(to_f32<AT>(from_f32<AT>(__fadd_rn(__uint_as_float((uint32_t)cur), k.tau_f))));
+    }
+    if (prep_age != ~0ull) {
+      const fs_compartment& cc = p.model.comp[p.cslot_comp[sl]];
+      hk = cc.hazard;
+      hp0 = cc.p0;
+      hp1 = cc.p1;
+      ha = __uint_as_float((uint32_t)prep_age);
+    }
+  }
+  float hr = 0.0f;
+  if (compute || prep_age != ~0ull) hr = nodal_rate(hk, hp0, hp1, ha, p.hprec);
+  if (compute) rate = hr;
+  if (prep_lane) {
+    const int idx = prep & (kCohortW - 1), sl = prep / kCohortW;
+    const int par_n = (int)(k.step & 1) ^ 1;
+    p.ctab[((size_t)par_n * kCohortSlots + sl) * kCohortW + idx] =
+        prep_age != ~0ull ? ((prep_age >> 32) << 32) | __float_as_uint(hr) : ~0ull;
+    if (sl == 0) p.cage[par_n * kCohortW + idx] = prep_age;
+  }
   lmax = fmaxf(lmax, rate);
   bool fire = false;
   if (rate > 0.0f) {
@@ -1015,7 +1059,15 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     pr_drains += qn < q0;
 #endif
   }
-  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS, HUBS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
+  {
+    // the final drain also prepares one (slot, cohort) pair of step k+1's
+    // cohort table in its idle lane 31 (qn < 32 here)
+    const int gw = (int)blockIdx.x * WARPS + warp;
+    const int prep = (MEMO && gw < kCohortW * p.ncslots) ? gw : -1;
+    if (qn > 0 || prep >= 0)
+      drain_entries<ST, AT, float, MAT, WARPS, HUBS>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
+                                                      sh.q_press[warp], lane, qn, lmax, mask_nxt, nullptr, prep);
+  }
 #if FS_STEP_PROBE  // per-warp [phase end, deferred << 20 | mid-loop drains] after the per-CTA block
   if (p.dbg && lane == 0) {
     unsigned long long now;
@@ -1026,9 +1078,6 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     w[1] = ((unsigned long long)pr_def << 20) | (unsigned long long)(pr_drains + (qn > 0 ? 1 : 0));
   }
 #endif
-  // next step's cohort hazards: lane 0 of each warp prepares at most one slot
-  if constexpr (MEMO)
-    if (lane == 0) cohort_prep<AT>(p, k, warp, WARPS);
 #if FS_STEP_PROBE
   if (p.dbg && lane == 0) {
     unsigned long long now;
