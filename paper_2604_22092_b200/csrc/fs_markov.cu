@@ -373,9 +373,11 @@ namespace {
     if (err__ != cudaSuccess) return set_error(FS_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(err__), __FILE__, __LINE__); \
   } while (0)
 
+// scratch from the device's stream-ordered pool, kept between engines (the
+// renewal engine sets the pool's release threshold; fs_engine.cu)
 template <typename T>
 int mk_alloc(T** p, size_t n) {
-  if (cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess)
+  if (cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T), (cudaStream_t)0) != cudaSuccess)
     return set_error(FS_ENOMEM, "cudaMalloc(%zu)", n * sizeof(T));
   return 0;
 }
@@ -398,6 +400,12 @@ int fs_markov_create(const fs_graph* g, const fs_model* m, const fs_markov_confi
                      const fs_scalars* scal, int device, fs_markov** out) {
   if (!g || !m || !c || !states || !rates || !scal || !out) return set_error(FS_EINVAL, "null argument");
   *out = nullptr;
+  {
+    cudaMemPool_t pool;
+    unsigned long long keep = ~0ull;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess)
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   if (g->num_nodes < 1) return set_error(FS_EINVAL, "empty graph");
   if (!g->out_row_offsets || !g->out_col_indices) return set_error(FS_EINVAL, "the Markov engine needs the outgoing CSR");
   if (g->d_max >= 32768) return set_error(FS_EINVAL, "in-degree %d beyond the count encoding", g->d_max);
@@ -564,7 +572,9 @@ void fs_markov_destroy(fs_markov* e) {
   void* ptrs[] = {e->S, e->vals, e->leaf_lo, e->leaf_len, e->tl, e->tr, e->tout, e->lend, e->loc_l, e->loc_r,
                   e->loc_out, e->blk_lvl, e->cnt, e->pend[0],
                   e->pend[1], e->log_clock, e->log_tau, e->log_counts};
-  for (void* q : ptrs) if (q) cudaFree(q);
+  cudaDeviceSynchronize();  // nothing of this engine still in flight on any stream
+  for (void* q : ptrs) if (q) cudaFreeAsync(q, (cudaStream_t)0);
+  cudaStreamSynchronize((cudaStream_t)0);
   delete e;
 }
 
