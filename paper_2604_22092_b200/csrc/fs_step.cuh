@@ -536,36 +536,8 @@ __device__ __forceinline__ float inf_value(const StepParams& p, const StepConst&
 // the node's entry step instead of evaluating the hazard.  Tags make stale or
 // never-prepared slots (engine start, host edits, other kernels) fall back to
 // direct evaluation; a cohort's age chain restarts only from a fresh cohort.
-// Results are bit-identical with or without the table.
-template <typename AT>
-__device__ __forceinline__ void cohort_prep(const StepParams& p, const StepConst& k, int tid, int nthreads_cta) {
-  const int par_c = (int)(k.step & 1), par_n = par_c ^ 1;
-  const uint32_t tag_c = (uint32_t)k.step, tag_n = (uint32_t)(k.step + 1);
-  for (int idx = (int)blockIdx.x + tid * (int)gridDim.x; idx < kCohortW; idx += nthreads_cta * (int)gridDim.x) {
-    const int64_t j = (k.step + 1) - (((k.step + 1) - idx) & (kCohortW - 1));  // cohort of slot idx at k+1
-    unsigned long long age_word = ~0ull;  // invalid
-    if (j == k.step) {
-      age_word = ((unsigned long long)tag_n << 32) | __float_as_uint(0.0f);  // fired this step: age 0
-    } else if (j < k.step) {
-      const unsigned long long cur = p.cage[par_c * kCohortW + idx];
-      if ((uint32_t)(cur >> 32) == tag_c) {  // its age at step k is known: advance it
-        const float a = to_f32<AT>(from_f32<AT>(__fadd_rn(__uint_as_float((uint32_t)cur), k.tau_f)));
-        age_word = ((unsigned long long)tag_n << 32) | __float_as_uint(a);
-      }
-    }
-    p.cage[par_n * kCohortW + idx] = age_word;
-    for (int sl = 0; sl < p.ncslots; ++sl) {
-      unsigned long long w = ~0ull;
-      if (age_word != ~0ull) {
-        const int c = p.cslot_comp[sl];
-        const fs_compartment& cc = p.model.comp[c];
-        const float r = nodal_rate(cc.hazard, cc.p0, cc.p1, __uint_as_float((uint32_t)age_word), p.hprec);
-        w = ((unsigned long long)tag_n << 32) | __float_as_uint(r);
-      }
-      p.ctab[((size_t)par_n * kCohortSlots + sl) * kCohortW + idx] = w;
-    }
-  }
-}
+// Results are bit-identical with or without the table.  The preparation runs
+// in lane 31 of each warp's final drain (drain_entries, argument `prep`).
 
 // incremental counts: +-1 on node j's pending delta (buffer `nxt`), in this
 // device's memory or, node-partitioned, the owner's — possibly a peer GPU's
@@ -620,7 +592,7 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
   // cohort-table preparation rides in lane 31 of a warp's final drain
   // (never a queued lane there: a final queue holds < 32 entries), through the
   // same hazard call, so it adds no latency.  Pair `prep` = (slot sl, cohort
-  // idx) of step k+1's table (see cohort_prep).
+  // idx) of step k+1's table (see the cohort-table comment above).
   const bool prep_lane = prep >= 0 && lane == 31;
   int hk = 0;
   double hp0 = 0.0, hp1 = 0.0;
