@@ -693,7 +693,7 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
       wides &= wides - 1;
       const int64_t a0 = __shfl_sync(kFull, e0, src), a1 = __shfl_sync(kFull, e1, src);
       const bool up = __shfl_sync(kFull, push, src) > 0;
-      constexpr int kHB = 4;  // 4 x 32 edges of the hub row in flight per round
+      constexpr int kHB = 8;  // 8 x 32 edges of the hub row in flight per round
       for (int64_t b = a0 + lane; b < a1; b += 32 * kHB) {
         int32_t cj[kHB];
 #pragma unroll
