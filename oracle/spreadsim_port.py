@@ -197,19 +197,58 @@ def nodal_hazard(holding, age64: np.ndarray) -> np.ndarray:
 # ----------------------------------------------------------------------
 
 
+try:  # the reference's optional compiled fold (R/renewal.py:57-68), same per-node order
+    import numba
+
+    @numba.njit("void(float32[::1], float32[::1], int64[::1], int64[::1], int64[::1])", cache=False)
+    def _fold_seq(out, contrib, nodes, starts, degs):  # pragma: no cover
+        for k in range(nodes.size):
+            acc = np.float32(0.0)
+            base = starts[k]
+            for e in range(degs[k]):
+                acc += contrib[base + e]
+            out[nodes[k]] += acc
+
+    _HAVE_NUMBA = True
+except Exception:  # pragma: no cover
+    _HAVE_NUMBA = False
+
+_FOLD_SETS: dict = {}
+
+
+def _fold_set(row_offsets: np.ndarray):
+    """Degree-sorted node order, slice starts and degrees, built once per
+    row_offsets array as the reference's plan does (R/renewal.py:177-195)."""
+    key = (id(row_offsets), row_offsets.size, int(row_offsets[-1]) if row_offsets.size else 0)
+    fs = _FOLD_SETS.get(key)
+    if fs is None or fs[0] is not row_offsets:
+        deg = np.diff(row_offsets)
+        order = np.argsort(-deg, kind="stable")
+        fs = (row_offsets, order, np.ascontiguousarray(row_offsets[:-1][order]), np.ascontiguousarray(deg[order]))
+        if len(_FOLD_SETS) > 8:
+            _FOLD_SETS.clear()
+        _FOLD_SETS[key] = fs
+    return fs[1:]
+
+
 def fold_pressure(row_offsets: np.ndarray, col: np.ndarray, w32: np.ndarray, inf32: np.ndarray) -> np.ndarray:
-    """p_i = f32 sequential sum over the slice of f32(inf[col]*w), slice
-    position by slice position across all nodes (same per-node order as
-    R/renewal.py:60-68, 198-218)."""
+    """p_i = f32 sequential sum over the slice of f32(inf[col]*w), in CSR
+    order per node (R/renewal.py:60-68, 198-218): the reference's compiled
+    fold when numba is importable, else its numpy position-major fold —
+    bit-identical (T/test_renewal.py:74-87)."""
     n = row_offsets.size - 1
     out = np.zeros(n, dtype=np.float32)
     if col.size == 0:
         return out
-    contrib = inf32.astype(np.float32)[col] * w32.astype(np.float32)
-    deg = np.diff(row_offsets)
-    order = np.argsort(-deg, kind="stable")
-    sdeg = deg[order]
-    start = row_offsets[:-1][order]
+    contrib = inf32.astype(np.float32, copy=False)[col]
+    w = w32.astype(np.float32, copy=False)
+    if not (w.size and w[0] == 1.0 and (w == 1.0).all()):
+        contrib = contrib * w
+    order, start, sdeg = _fold_set(row_offsets)
+    if _HAVE_NUMBA:
+        _fold_seq(out, np.ascontiguousarray(contrib, dtype=np.float32), order.astype(np.int64, copy=False),
+                  start.astype(np.int64, copy=False), sdeg.astype(np.int64, copy=False))
+        return out
     live = n
     for p in range(int(sdeg[0]) if n else 0):
         while live and sdeg[live - 1] <= p:

@@ -306,6 +306,7 @@ struct fs_engine {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t batch_exec[2][2][6] = {};  // [materialise][scalar slot][step % 6]: parity and exchange slot are baked in
   bool compaction_ready = false;
+  bool tiles_valid = false;  // active tile list matches the states (set by begin_batch / refresh_tiles)
   int stream_evict_first = 0;
   // incremental count mode
   int32_t* entry = nullptr;           // cohort table: per-node entry step
@@ -510,17 +511,14 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
   return 0;
 }
 
-int launch_begin_batch(fs_engine* e, cudaStream_t st) {
-  k_begin_batch<<<1, 32, 0, st>>>(e->dstate + e->s_cur, e->acc, e->log_counts, e->log_cap, e->m.num_compartments,
-                                  e->c.epsilon, e->c.tau_max, e->c.delta, e->c.carry_tau);
-  if (e->c.compaction) {
+// compaction: rebuild the active tile list from the current states
+// (refresh_active, renewal.py:426-432, at 32-node tile granularity)
+int refresh_tiles(fs_engine* e, cudaStream_t st) {
+  {
     uint32_t term_bits = 0;
     for (int i = 0; i < e->m.num_compartments; ++i)
       if (e->m.comp[i].terminal) term_bits |= 1u << i;
     const int64_t n = e->g.num_nodes;
-    // rates are zeroed once per batch under compaction (renewal.py:594)
-    if (e->b.rates) k_fill<float><<<e->sms * 4, 256, 0, st>>>(e->b.rates, n, 0.0f);
-    if (e->b.pressure) k_fill<float><<<e->sms * 4, 256, 0, st>>>(e->b.pressure, n, 0.0f);
     k_zero_i64<<<1, 1, 0, st>>>(e->num_active);
     const int blocks = (int)std::min<int64_t>((e->ntiles + 255) / 256 + 1, (int64_t)e->sms * 8);
     if (e->mixed)
@@ -540,7 +538,22 @@ int launch_begin_batch(fs_engine* e, cudaStream_t st) {
       k_sync_buffers<float><<<blocks2, 256, 0, st>>>(e->dstate + e->s_cur, (float*)e->b.infectivity[0], (float*)e->b.infectivity[1], n);
   }
   FS_CUDA(cudaGetLastError());
+  e->tiles_valid = true;
   return 0;
+}
+
+int launch_begin_batch(fs_engine* e, cudaStream_t st) {
+  k_begin_batch<<<1, 32, 0, st>>>(e->dstate + e->s_cur, e->acc, e->log_counts, e->log_cap, e->m.num_compartments,
+                                  e->c.epsilon, e->c.tau_max, e->c.delta, e->c.carry_tau);
+  if (!e->c.compaction) {
+    FS_CUDA(cudaGetLastError());
+    return 0;
+  }
+  const int64_t n = e->g.num_nodes;
+  // rates are zeroed once per batch under compaction (renewal.py:594)
+  if (e->b.rates) k_fill<float><<<e->sms * 4, 256, 0, st>>>(e->b.rates, n, 0.0f);
+  if (e->b.pressure) k_fill<float><<<e->sms * 4, 256, 0, st>>>(e->b.pressure, n, 0.0f);
+  return refresh_tiles(e, st);
 }
 
 // hazard memo: every node's cohort unknown, every slot's tag stale
@@ -898,6 +911,10 @@ int fs_engine_step(fs_engine* e, int32_t nsteps, int32_t materialize, int32_t us
   if (materialize && (!e->b.pressure || !e->b.rates)) return set_error(FS_EINVAL, "materialize needs pressure/rates buffers");
   FS_CUDA(cudaSetDevice(e->device));
   if (use_active && !e->c.compaction) return set_error(FS_EINVAL, "engine built without compaction");
+  if (use_active && !e->tiles_valid) {  // no batch boundary yet, or host-edited states
+    const int rc = refresh_tiles(e, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
   return launch_steps(e, nsteps, materialize != 0, use_active != 0, (cudaStream_t)stream);
 }
 
@@ -1088,7 +1105,11 @@ int fs_engine_states_edited(fs_engine* e, void* stream) {
   FS_CUDA(cudaSetDevice(e->device));
   cudaStream_t st = (cudaStream_t)stream;
   int rc = reset_memo(e, st);  // edited nodes no longer follow their age cohorts
+  e->tiles_valid = false;       // an edit can revive nodes of an inactive tile
   if (rc || !e->incr) return rc;
+  // under compaction, inactive tiles never fold their pending deltas: start
+  // the edit from exact counts of the current mask (both delta buffers clean)
+  if (e->c.compaction && (rc = recount(e, e->h_step, st))) return rc;
   if (e->world > 1) return set_error(FS_ESTATE, "host state edits are not supported on partitioned engines");
   const int cur = (int)(e->h_step & 1);
   const int64_t n = e->g.num_nodes;

@@ -43,6 +43,7 @@ from .renewal import (
     _STRATEGY_CODE,
     RenewalConfig,
     _check_conservation,
+    as_config,
     _DeviceGraph,
     _node_buffer,
     _pick_seed_nodes,
@@ -97,6 +98,7 @@ def partition_plan(num_nodes: int, world: int, align: int = ALIGN) -> PartitionP
 
 
 def _config(cfg: RenewalConfig, strategy, incremental: int) -> _lib.FsConfig:
+    cfg = as_config(cfg)
     return _lib.FsConfig(
         epsilon=cfg.epsilon, tau_max=cfg.tau_max, delta=cfg.delta, steps_per_batch=cfg.steps_per_batch,
         strategy=_STRATEGY_CODE[strategy], compaction=int(cfg.compaction), mixed_precision=int(cfg.mixed_precision),
@@ -121,6 +123,7 @@ class _Partition:
 
     def __init__(self, g_local, m, cfg: RenewalConfig, seed: int, plan: PartitionPlan, rank: int,
                  seed_ids: torch.Tensor, masks: list, comm, dev):
+        cfg = as_config(cfg)
         if m.transmission.kind != "constant":
             raise InvalidConfigError("partitioned runs need constant transmission (count gather)")
         lo, hi = plan.ranges[rank]

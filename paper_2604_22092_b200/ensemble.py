@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _device
-from .renewal import RenewalConfig, _build_plan, _check_conservation, init_renewal_state
+from .renewal import RenewalConfig, _build_plan, as_config, _check_conservation, init_renewal_state
 from .rng import derive_seed
 from .analysis import make_records
 from .trajectory import DEFAULT_GRID_POINTS, TrajectoryRecord
@@ -73,7 +73,7 @@ def run_ensemble(engine: str, g, m, cfg, seed: int, t_final: float, runs: int,
     bounds the trials in flight).  Records are ordered by trial index."""
     if engine != "renewal":
         raise ValueError(f"the B200 ensemble runs the renewal engine only (got {engine!r})")
-    cfg = cfg or RenewalConfig()
+    cfg = as_config(cfg)
     _device.device()
     b = cfg.steps_per_batch
     free = [torch.cuda.Stream() for _ in range(max(1, min(concurrency, runs)))]

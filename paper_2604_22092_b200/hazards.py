@@ -193,17 +193,24 @@ def _hazard(tau, kind: int, p0: float, p1: float, precision: int = _lib.HAZ_F64)
     )
 
 
-def lognormal_hazard(tau, p: LogNormalParams):
-    """h(tau) = sqrt(2/pi) / (tau sigma erfcx(z)), h(0) = 0 (hazards.py:135-146)."""
-    return _hazard(tau, _lib.HZ_LOGNORMAL, p.mu, p.sigma)
+_HAZ_PRECISION = {"f64": _lib.HAZ_F64, "f32": _lib.HAZ_F32}
 
 
-def weibull_hazard(tau, p: WeibullParams):
-    return _hazard(tau, _lib.HZ_WEIBULL, p.k, p.lam)
+def lognormal_hazard(tau, p: LogNormalParams, precision: str = "f64"):
+    """h(tau) = sqrt(2/pi) / (tau sigma erfcx(z)), h(0) = 0 (hazards.py:135-146).
+
+    `precision` selects the engine's evaluation: "f64" is the reference's
+    float64 arithmetic, "f32" the kernel's `hazard_precision="f32"` path
+    (both returned as float64 arrays)."""
+    return _hazard(tau, _lib.HZ_LOGNORMAL, p.mu, p.sigma, _HAZ_PRECISION[precision])
 
 
-def erlang_hazard(tau, p: ErlangParams):
-    return _hazard(tau, _lib.HZ_ERLANG, float(p.k), p.rate)
+def weibull_hazard(tau, p: WeibullParams, precision: str = "f64"):
+    return _hazard(tau, _lib.HZ_WEIBULL, p.k, p.lam, _HAZ_PRECISION[precision])
+
+
+def erlang_hazard(tau, p: ErlangParams, precision: str = "f64"):
+    return _hazard(tau, _lib.HZ_ERLANG, float(p.k), p.rate, _HAZ_PRECISION[precision])
 
 
 def shedding(s: Shedding, tau):

@@ -27,14 +27,14 @@ import ctypes
 import os
 import time
 import weakref
-from dataclasses import dataclass
+from dataclasses import dataclass, fields
 
 import numpy as np
 import torch
 
 from . import _device, _lib
 from .errors import InvalidConfigError, ReconfigureAfterStartError
-from .graph import CsrGraph, Strategy, resolve_strategy
+from .graph import CsrGraph, Strategy, as_strategy, resolve_strategy
 from .models import ModelSpec, model_descriptor
 from .rng import RNG_KINDS, derive_seed, uniform_array
 from .trajectory import DEFAULT_GRID_POINTS, TrajectoryRecord, make_record
@@ -51,6 +51,7 @@ __all__ = [
     "run_batch",
     "run_renewal",
     "default_seed_count",
+    "as_config",
 ]
 
 _SEED_PICK_SALT = 0x5EEDC0DE  # renewal.py:55
@@ -104,6 +105,26 @@ class RenewalConfig:
             raise ValueError("hazard_precision must be 'f64' or 'f32'")
         if self.gather not in _GATHER:
             raise ValueError("gather must be 'auto', 'f32', 'count' or 'incremental'")
+
+
+def as_config(cfg) -> RenewalConfig:
+    """This package's RenewalConfig for `cfg`.
+
+    Accepts None (defaults), a RenewalConfig, or the reference's own
+    `spreadsim.renewal.RenewalConfig` (R/renewal.py:75-99) or any object with
+    its fields: the reference fields are copied by name, its `Strategy`
+    member is mapped by value, and the three B200 fields the reference does
+    not have (`rng`, `hazard_precision`, `gather`) take their defaults —
+    the reference's own arithmetic (splitmix, f64 hazards) with the exact
+    gather encodings chosen automatically."""
+    if cfg is None:
+        return RenewalConfig()
+    if isinstance(cfg, RenewalConfig):
+        return cfg
+    kw = {f.name: getattr(cfg, f.name) for f in fields(RenewalConfig) if hasattr(cfg, f.name)}
+    if "strategy" in kw:
+        kw["strategy"] = as_strategy(kw["strategy"])
+    return RenewalConfig(**kw)
 
 
 @dataclass
@@ -313,6 +334,7 @@ class _EnginePlan:
 
 
 def _build_plan(g, m, cfg: RenewalConfig, mixed: bool) -> _EnginePlan:
+    cfg = as_config(cfg)
     strategy = resolve_strategy(g, cfg.strategy)
     dg = device_graph(g, mixed)
     count_mode = m.transmission.kind == "constant" and dg.uniform and cfg.gather != "f32"
@@ -738,6 +760,7 @@ def init_renewal_state(g, m, cfg: RenewalConfig, seed: int, seed_count: int | No
     """Fresh device state: all nodes in S at age 0, `seed_count` nodes in
     `seed_compartment` (default the first infected successor), infectivity
     consistent with the seeded state (renewal.py:370-410)."""
+    cfg = as_config(cfg)
     n = int(g.num_nodes)
     if seed_count is None:
         seed_count = default_seed_count(n)
@@ -811,6 +834,7 @@ def pressure_gather(g, infectivity, strategy: Strategy, cfg: RenewalConfig, acti
 
     numpy in -> numpy out; a CUDA tensor in -> CUDA tensor out.
     """
+    cfg = as_config(cfg)
     lib = _lib.load()
     dev = _device.device()
     strategy = resolve_strategy(g, strategy)
@@ -841,13 +865,33 @@ def _check_conservation(counts: np.ndarray, n: int) -> None:
         raise AssertionError(f"compartment counts no longer sum to N={n} (renewal.py:554)")
 
 
+def _check_active(state: RenewalState, plan: _EnginePlan, active: ActiveSet) -> None:
+    """The reference steps exactly `active.ids` (renewal.py:509-520); its
+    callers pass the set `_begin_batch` returned — the nodes not absorbed at
+    the batch start, `refresh_active(states, terminal)`, a superset of the
+    nodes live now — and absorbed nodes do not change in a step, so
+    processing that set is processing every node.  The fused
+    kernel works on whole 32-node tiles of that set (rebuilt from the
+    current states when the engine's list is stale, fs_engine_step); a
+    different subset (which would freeze the ages of the left-out live
+    nodes) is refused instead of being silently widened."""
+    live = refresh_active(state._t["states"], plan.terminal, pad=0).ids.astype(np.int64)
+    if not np.isin(live, np.asarray(active.ids, dtype=np.int64), assume_unique=True).all():
+        raise InvalidConfigError(
+            "renewal_step(active=...) must contain every live node (the set _begin_batch / refresh_active(states, "
+            "terminal) returns); a subset that leaves live nodes out is not supported")
+
+
 def renewal_step(state: RenewalState, g, m, cfg: RenewalConfig, seed: int, *, plan: _EnginePlan | None = None,
                  active: ActiveSet | None = None) -> tuple[RenewalState, float]:
     """One fused tau-leap (renewal.py:483-580): one kernel launch (two under
     EDGE_MERGE), pressure / rates materialised for inspection."""
+    cfg = as_config(cfg)
     if plan is None:
         plan = state._plan_for(g, m, cfg)
     eng = state._bind(plan, seed, materialize=True)
+    if active is not None:
+        _check_active(state, plan, active)
     before = eng.scalars()
     eng.step(1, materialize=True, use_active=active is not None and bool(cfg.compaction))
     state._after_device()
@@ -858,6 +902,7 @@ def renewal_step(state: RenewalState, g, m, cfg: RenewalConfig, seed: int, *, pl
 def _begin_batch(state: RenewalState, g, cfg: RenewalConfig, plan: _EnginePlan) -> ActiveSet | None:
     """Batch boundary (renewal.py:583-597): tau reset unless carry_tau;
     under compaction rates are zeroed and the active list refreshed."""
+    cfg = as_config(cfg)
     eng = state._bind(plan, state._scal().seed, materialize=True)
     eng.begin_batch()
     state._after_device()
@@ -869,6 +914,7 @@ def _begin_batch(state: RenewalState, g, cfg: RenewalConfig, plan: _EnginePlan) 
 def run_batch(state: RenewalState, g, m, cfg: RenewalConfig, seed: int, *, plan: _EnginePlan | None = None,
               recorder: list | None = None) -> tuple[RenewalState, float]:
     """steps_per_batch fused steps as one CUDA-graph replay (renewal.py:600-629)."""
+    cfg = as_config(cfg)
     if plan is None:
         plan = state._plan_for(g, m, cfg)
     eng = state._bind(plan, seed, materialize=True)
@@ -891,6 +937,7 @@ def run_renewal(g, m, cfg: RenewalConfig, seed: int, t_final: float, grid_points
                 seed_count: int | None = None, seed_compartment: int | None = None) -> TrajectoryRecord:
     """Whole batches until clock >= t_final, sampled onto the grid
     (renewal.py:632-663).  One graph replay and one log read per batch."""
+    cfg = as_config(cfg)
     t0 = time.perf_counter()
     state = init_renewal_state(g, m, cfg, seed, seed_count, seed_compartment)
     plan = _build_plan(g, m, cfg, state.mixed_precision)

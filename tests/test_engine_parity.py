@@ -184,9 +184,11 @@ def test_weibull_erlang_and_philox_vs_oracle(mname, gname, rng):
         fs.run_batch(st, g, m, cfg, 21)
     assert np.array_equal(st.counts, ref.counts)
     assert np.array_equal(st.states.astype(np.int32), ref.states.astype(np.int32))
-    assert np.allclose(st.ages, ref.ages, rtol=RATE_RTOL, atol=0)
+    # f64 hazards: equal after the f32 store unless a libm ulp straddles an
+    # f32 rounding boundary (p ~ 2^-28 per evaluation), so ages and clock exact
+    assert np.array_equal(st.ages, ref.ages)
     assert np.allclose(st.rates, ref.rates, rtol=RATE_RTOL, atol=0)
-    assert st.clock == pytest.approx(ref.clock, rel=1e-12)
+    assert st.clock == ref.clock and st.tau_prev == ref.tau_prev
 
 
 def test_host_edits_between_steps_are_seen():
