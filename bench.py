@@ -42,8 +42,16 @@ WORKLOADS = {
     "c1": dict(desc="C1: SEIR log-normal, uniform-degree k=10, N=1e4", kind="fixed", n=10_000, k=10, model="seir"),
     "c2": dict(desc="C2: SEIR log-normal, uniform-degree k=10, N=1e6, CUDA graph", kind="fixed", n=1_000_000, k=10,
                model="seir"),
-    "c3": dict(desc="C3: SEIR Weibull/Erlang, Barabasi-Albert m=5, N=1e6, edge-merge dispatch", kind="ba",
-               n=1_000_000, k=5, model="seir_we"),
+    "c3": dict(desc="C3: SEIR Weibull/Erlang, Barabasi-Albert m=5, N=1e6 (rho 421.7: merge strategy selected)",
+               kind="ba", n=1_000_000, k=5, model="seir_we"),
+    # the real gather paths: every step folds the CSR
+    "c2s": dict(desc="C2 with age-dependent shedding s(tau) = lognormal hazard (IR): SEIR log-normal, uniform-degree "
+                     "k=10, N=1e6 — f32 CSR-order fold of beta*s(age) every step",
+                kind="fixed", n=1_000_000, k=10, model="seir_shed"),
+    "c3f": dict(desc="C3 graph and model, gather='f32': edge-merge f32 fold of the CSR every step (EDGE_MERGE)",
+                kind="ba", n=1_000_000, k=5, model="seir_we", gather="f32"),
+    "c3c": dict(desc="C3 graph and model, gather='count': 1-bit infectious-mask gather of the CSR every step "
+                     "(EDGE_MERGE)", kind="ba", n=1_000_000, k=5, model="seir_we", gather="count"),
     "c5": dict(desc="C5: SEIR log-normal, uniform-degree k=10, N=1e9, node-partitioned across the GPUs "
                     "(NCCL mask all-gather + max/count all-reduce per step)",
                kind="regular_dev", n=1_000_000_000, k=10, model="seir", cpu_n=10_000_000, t_final=10.0),
@@ -77,6 +85,9 @@ def build_inputs(w):
         g = fs.gen_barabasi_albert(w["n"], w["k"], seed=GRAPH_SEED)
     if w["model"] == "seir":
         m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    elif w["model"] == "seir_shed":
+        ir = fs.lognormal_from_mean_median(7.5, 5.0)
+        m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0, transmission=fs.Shedding.lognormal_hazard(ir))
     elif w["model"] == "sir_markov":
         m = fs.sir_model(0.25, 0.15)
     else:
@@ -142,27 +153,82 @@ class ClockSampler:
         return out
 
 
-def roofline_block(achieved: float, pk: dict, traffic, ms_per_step: float, b_alg: float) -> dict:
+def roofline_block(achieved: float, pk: dict, ncu: dict, ms_per_step: float, b_alg: float) -> dict:
     """`achieved` counts the reference layout's B_alg bytes per node-update
-    (SURVEY.md §8d); `traffic` is the kernel's DRAM bytes per launch from one
-    ncu capture (profiles/ncu_summary.json), and `traffic_gbs` that traffic
-    over the measured step time — the physical bandwidth, against the same peak.
-    The encodings move fewer bytes than B_alg, which is why
-    frac can exceed 1 while traffic_frac cannot."""
+     over the measured step time.  The physical picture comes
+    from the dominant kernel's ncu capture (profiles/ncu_summary.json):
+    `traffic` = its DRAM bytes per launch, `frac_physical` = those bytes over
+    its ncu duration against the same peak, and `traffic_frac` the same bytes
+    over this run's step time.  `ncu_same_build` says whether the capture ran
+    the library this run loaded.  The encodings move fewer
+    bytes than B_alg, which is why frac can exceed 1 while the physical
+    fractions cannot."""
+    traffic = ncu.get("dram_bytes_per_launch")
     out = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
            "traffic": traffic, "bytes_per_update": b_alg, "peak_source": pk["source"]}
     if traffic:
         out["traffic_gbs"] = traffic / (ms_per_step / 1e3) / 1e9
         out["traffic_frac"] = out["traffic_gbs"] / pk["hbm_gbs"]
+        if ncu.get("gpu_time_us"):
+            out["frac_physical"] = traffic / (ncu["gpu_time_us"] * 1e-6) / 1e9 / pk["hbm_gbs"]
+            out["ncu_kernel"] = ncu.get("kernel")
+            out["ncu_gpu_time_us"] = ncu["gpu_time_us"]
+        out["ncu_same_build"] = ncu.get("lib_sha16") is not None and ncu.get("lib_sha16") == lib_sha16()
     return out
 
 
-def ncu_traffic(workload: str):
+def lib_sha16() -> str | None:
+    import hashlib
+
+    p = ROOT / "paper_2604_22092_b200" / "libflashspread_b200.so"
+    return hashlib.sha256(p.read_bytes()).hexdigest()[:16] if p.exists() else None
+
+
+def ncu_entry(workload: str) -> dict:
+    """The dominant kernel's ncu capture for this workload
+    (profiles/ncu_summary.json, written by scripts/ncu_to_summary.py from a
+    `ncu --set full` run of `bench.py --workload W`): DRAM bytes and duration
+    per launch, and the sha of the library the capture ran."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
+        return {}
+    return json.loads(p.read_text()).get(workload, {})
+
+
+def workload_config(w: dict, n: int, world: int = 1) -> dict:
+    """`config` of both arms (same keys and values: the workload, not the
+    implementation; the edge count and the CPU sample size are reported
+    beside it)."""
+    return {"workload": w["desc"], "n": n, "graph_seed": GRAPH_SEED, "sim_seed": SIM_SEED,
+            "precision": "mixed (states i8, ages f16, infectivity bf16)" if w.get("mixed") else "fp32 storage",
+            "gather_option": w.get("gather", "auto"),
+            "l2": ("inputs larger than L2; steps timed back to back as CUDA-graph batches"
+                   if world > 1 and not w.get("per_gpu") else
+                   "flushed before every timed step (512 MiB write + 512 MiB read of another buffer)")}
+
+
+def dtype_of(w: dict) -> str:
+    return "i8/f16/bf16 storage, f32 rates, f64 hazard/q" if w.get("mixed") else "f32 (f64 hazard/q)"
+
+
+def data_of(w: dict) -> str:
+    if w["kind"] == "regular_dev":
+        return "synthetic (GPU uniform-degree generator fs_gen_regular, graph seed 1, sim seed 7)"
+    return "synthetic (reference generators, graph seed 1, sim seed 7)"
+
+
+def port_vs_reference() -> dict | None:
+    """Per-core speed of the oracle port against the reference's own
+    renewal_step on the same C2 graph, measured in the build container where
+    the reference is importable (scripts/port_vs_reference.py)."""
+    p = ROOT / "profiles" / "port_vs_reference.json"
+    if not p.exists():
         return None
-    d = json.loads(p.read_text()).get(workload, {})
-    return d.get("dram_bytes_per_launch")
+    d = json.loads(p.read_text())["c2"]
+    return {"port_mnups_per_core": round(d["port_mnups_per_core"], 3),
+            "reference_mnups_per_core": round(d["reference_mnups_per_core"], 3),
+            "port_over_reference_time": round(d["port_over_reference_time"], 3),
+            "where": "build container, 1 thread each, C2 graph, states checked equal (profiles/port_vs_reference.json)"}
 
 
 def _cpu_worker(args):
@@ -207,20 +273,22 @@ def cpu_ensemble(g, m, warm: int, steps: int, workers: int | None = None, mixed:
             "wall_s": wall, "per_core_value": g.num_nodes * steps / (sum(walls) / len(walls)) / 1e9,
             "sample": f"{cores} independent trajectories (one per host core, run_ensemble style) x {steps} timed "
                       f"steps after {warm} warm-up, N={g.num_nodes}; oracle/spreadsim_port.py (numpy restatement "
-                      f"of renewal_step, pinned to the reference's golden vectors)"}
+                      f"of renewal_step with the reference's numba CSR fold, pinned to the reference's golden "
+                      f"vectors)",
+            "port_vs_reference": port_vs_reference()}
 
 
 def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
-    w = WORKLOADS["c2" if args.workload == "c2w" else args.workload]  # the CPU has no per-GPU split
+    w = WORKLOADS[args.workload]
     if w.get("engine") == "markov":
         print(json.dumps({"impl": "reference", "unavailable": "the CPU oracle port restates the renewal path only"}))
         return
-    if "cpu_n" in w:  # bounded sample of a workload too large for host RAM
+    if "cpu_n" in w or w.get("per_gpu"):  # bounded sample of a workload too large for host RAM
         import paper_2604_22092_b200 as fs
 
-        g = fs.gen_fixed_degree_device(w["cpu_n"], w["k"], seed=GRAPH_SEED).to_host()
+        g = fs.gen_fixed_degree_device(w.get("cpu_n", w["n"]), w["k"], seed=GRAPH_SEED).to_host()
         m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
     else:
         g, m = build_inputs(w)
@@ -229,10 +297,10 @@ def run_reference(args, rank: int, world: int) -> None:
     print(json.dumps({
         "impl": "reference", "metric": "Giga-NUPS (node updates/s)", "value": v, "unit": "G-NUPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["wall_s"] / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 hazard/q)",
-        "data": "synthetic (reference generators, graph seed 1, sim seed 7)",
-        "config": {"workload": w["desc"], "n": g.num_nodes, "edges": g.num_edges, "graph_seed": GRAPH_SEED,
-                   "sim_seed": SIM_SEED},
+        "higher_is_better": True, "scaling": "weak" if (world == 1 or w.get("per_gpu")) else "strong",
+        "vs_baseline": None, "dtype": dtype_of(w), "data": data_of(w),
+        "config": workload_config(w, w["n"] * (world if w.get("per_gpu") else 1), world),
+        "edges": g.num_edges if "cpu_n" not in w else None,
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "G-NUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -393,14 +461,13 @@ def run_partitioned(args, w, rank: int, world: int, local: int) -> None:
         "metric": "Giga-NUPS (node updates/s)", "value": n_total * steps / (total_ms / 1e3) / 1e9, "unit": "G-NUPS",
         "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None,
-        "dtype": "i8/f16/bf16 storage, f32 rates, f64 hazard/q" if mixed else "f32 (f64 hazard/q)",
-        "data": "synthetic (GPU uniform-degree generator fs_gen_regular, graph seed 1, sim seed 7)",
-        "config": {"workload": w["desc"], "n": n_total, "edges": int(edges.item()), "strategy": "per-node",
+        "dtype": dtype_of(w), "data": data_of(w),
+        "config": workload_config(w, n_total, world),
+        "edges": int(edges.item()),
+        "engine": {"strategy": "per-node",
                    "gather": "incremental counts, cross-rank pushes into peer memory (CUDA IPC / NVLink)",
                    "parallelism": f"node-partitioned x{world} (peer pushes + NCCL all-reduce of 17 words per step)",
-                   "l2": ("flushed before every timed step (512 MiB write + 512 MiB read of another buffer)" if weak
-                          else "inputs larger than L2; steps timed back to back as CUDA-graph batches"),
-                   "steps_from": f"t=0 after {args.warmup} warm-up steps"},
+                   "steps_from": f"t=0 after {args.warmup} warm-up steps", "lib_sha16": lib_sha16()},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"] * world, "unit": "GB/s",
                      "frac": achieved / (pk["hbm_gbs"] * world), "traffic": None,
                      "bytes_per_update": B_ALG[mixed], "peak_source": pk["source"] + f" x {world} GPUs"},
@@ -434,9 +501,11 @@ def main() -> None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.workload is None:
-        # N=1: the headline C2; N>1: the same per-GPU work, node-partitioned
-        # (weak scaling, so the driver's per-N efficiency compares like with like)
-        args.workload = "c2" if world == 1 else "c2w"
+        # N=1: the headline C2; N>1: BASELINE C5, N_total = 1e9 node-partitioned
+        # over the GPUs (strong scaling, north_star's >= 70 % at 8 GPUs; its
+        # T_1 is `--workload c5` on one GPU).  `--workload c2w` is the weak-
+        # scaling alternative (1e6 nodes per GPU).
+        args.workload = "c2" if world == 1 else "c5"
     if world > 1:
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
     if args.impl == "reference":
@@ -464,7 +533,7 @@ def main() -> None:
     w = WORKLOADS[args.workload]
     g, m = build_inputs(w)
     mixed = bool(w.get("mixed", False))
-    cfg = fs.RenewalConfig(mixed_precision=mixed)
+    cfg = fs.RenewalConfig(mixed_precision=mixed, gather=w.get("gather", "auto"))
     n = g.num_nodes
     device_graph = hasattr(g, "device_tensors")
 
@@ -472,9 +541,9 @@ def main() -> None:
     st = fs.init_renewal_state(g, m, cfg, SIM_SEED)
     plan = R._build_plan(g, m, cfg, st.mixed_precision)
     eng = st._bind(plan, SIM_SEED, materialize=False)
-    kernels_per_step = 2 if plan.strategy == fs.Strategy.EDGE_MERGE else 1
     strategy_name, count_mode = plan.strategy.value, plan.count_mode
     incremental = count_mode and plan.config.incremental != 0 and plan.graph.symmetric
+    kernels_per_step = eng.kernels_per_step()
     snap0 = eng.snapshot()
     for _ in range(6):  # captures the batch CUDA graphs (every step-parity variant) outside any timed region
         eng.run_batch(False)
@@ -512,6 +581,7 @@ def main() -> None:
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    uni_on = eng.uniform_s_age()
     per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = torch.tensor([sum(per_step)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -543,11 +613,15 @@ def main() -> None:
                 h2d = 0
                 src = "a graph generated on the device (fs_gen_regular, inside the timed region)"
             else:
-                g.__dict__.pop("_fs_device_cache", None)
+                # a fresh CsrGraph (new arrays, nothing cached on it) for every
+                # run: the symmetry check, degree scan, page-locking and upload
+                # are all inside the timed region, as on a user's first call
+                g_run = fs.CsrGraph(g.num_nodes, g.num_edges, g.row_offsets.copy(), g.col_indices.copy(),
+                                    g.weights.copy())
                 t0 = time.perf_counter()
-                h2d = g.row_offsets.nbytes + g.col_indices.nbytes
-                src = "a host CsrGraph (CSR H2D inside the timed region)"
-            rec = fs.run_renewal(g, m, cfg, SIM_SEED, t_final)
+                h2d = g_run.row_offsets.nbytes + g_run.col_indices.nbytes
+                src = "a fresh host CsrGraph per run (no cached device copy or scans; CSR H2D inside the timed region)"
+            rec = fs.run_renewal(g if device_graph else g_run, m, cfg, SIM_SEED, t_final)
             torch.cuda.synchronize()
             walls.append(time.perf_counter() - t0)
             setups.append(rec.summary.get("setup_s"))
@@ -574,15 +648,16 @@ def main() -> None:
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "i8/f16/bf16 storage, f32 rates, f64 hazard/q" if mixed else "f32 (f64 hazard/q)",
-        "data": ("synthetic (GPU uniform-degree generator fs_gen_regular, graph seed 1, sim seed 7)" if device_graph
-                 else "synthetic (reference generators, graph seed 1, sim seed 7)"),
-        "config": {"workload": w["desc"], "n": n, "edges": g.num_edges, "strategy": strategy_name,
+        "dtype": dtype_of(w),
+        "data": data_of(w),
+        "config": workload_config(w, n, world),
+        "edges": g.num_edges,
+        "engine": {"strategy": strategy_name,
                    "gather": ("incremental counts (pushes along the outgoing CSR)" if incremental else
-                              "count (1-bit mask)" if count_mode else "f32"), "precision": "mixed (states i8, ages f16, infectivity bf16)" if mixed else "fp32 storage",
-                   "l2": "flushed before every timed step (512 MiB write + 512 MiB read of another buffer)", "parallelism": f"replicas x{world}",
-                   "steps_from": f"t=0 after {args.warmup} warm-up steps"},
-        "roofline": roofline_block(achieved, pk, ncu_traffic(args.workload), ms_per_step, B_ALG[mixed]),
+                              "count (1-bit mask)" if count_mode else "f32 CSR-order fold"),
+                   "kernels_per_step": kernels_per_step, "uniform_s_age": uni_on, "parallelism": f"replicas x{world}",
+                   "steps_from": f"t=0 after {args.warmup} warm-up steps", "lib_sha16": lib_sha16()},
+        "roofline": roofline_block(achieved, pk, ncu_entry(args.workload), ms_per_step, B_ALG[mixed]),
         "value_l2_warm": {"value": n / (warm_ms / 1e3) / 1e9, "ms_per_step": warm_ms,
                           "what": f"the same {nb * cfg.steps_per_batch} steps replayed as {nb} back-to-back "
                                   f"CUDA-graph batches, no flush (engine state restored in between)"},

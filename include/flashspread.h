@@ -227,6 +227,48 @@ int fs_comm_init(int32_t world, int32_t rank, const uint8_t* id, int32_t device,
 void fs_comm_destroy(void* comm);
 /* 1 if the engine gathers from the infectious bit-mask, 0 for the f32 gather */
 int fs_engine_uses_count_gather(const fs_engine* e);
+/* Kernel launches one step issues (1: the fused step; 2: a separate
+ * edge-chunked merge gather before it).  Diagnostic, for launch counting. */
+int fs_engine_kernels_per_step(const fs_engine* e);
+/* Uniform S age (SEIR / SIR: S is never re-entered, so every S node has the
+ * same age, R/renewal.py:540-542).  While on, the step kernel keeps the S
+ * age as one scalar and does not read or write it per node.
+ * fs_engine_sync_ages writes it back into the ages array — call it before
+ * reading or editing ages / states on the host; fs_engine_states_edited and
+ * fs_engine_reset_age_memo re-decide the mode from the array afterwards.
+ * Replaces nothing in the reference (an encoding of RenewalState.ages,
+ * R/renewal.py:114-126). */
+int fs_engine_sync_ages(fs_engine* e, void* stream);
+/* The host overwrote the engine's state arrays and mask buffers wholesale
+ * (a snapshot restore): rebuild the incremental counts from the current mask,
+ * invalidate the hazard memo and the active tiles, re-decide the S-age mode.
+ * Call after fs_engine_set_scalars.  No reference counterpart (the
+ * reference's state is plain numpy arrays). */
+int fs_engine_state_restored(fs_engine* e, void* stream);
+
+/* ---- run setup on the device (fs_setup.cu) ------------------------------ */
+/* Seed choice of init_renewal_state: the `count` nodes with the smallest
+ * uniform_array(seed_key, 0, id) (R/renewal.py:162-169 _pick_seed_nodes,
+ * seed_key = derive_seed(seed, 0x5EEDC0DE)), by a device radix select.  Each
+ * chosen node gets states[i] = compartment (states may be null) and, when inf
+ * is non-null, inf[i] = inf_value (cast on store); flags (nullable, u8[n])
+ * receives 1 for chosen nodes.  Ties of the 53-bit uniform go to the smaller
+ * id. */
+int fs_seed_select(int64_t n, uint64_t seed_key, int64_t count, void* states, int32_t states_dtype,
+                   int32_t compartment, void* inf, int32_t inf_dtype, float inf_value, uint8_t* flags,
+                   void* stream);
+/* ids of the set flags in increasing order (sorted seed ids) */
+int fs_flags_to_ids(const uint8_t* flags, int64_t n, int64_t* out_ids, int64_t* num_out, void* stream);
+/* Is the incoming CSR its own transpose (an undirected graph, R/graph.py:
+ * 221-231)?  Rows must be sorted by source (R/graph.py:141); *symmetric = 0
+ * otherwise.  row_offsets32 (nullable) is preferred when given. */
+int fs_check_symmetric(const int64_t* row_offsets, const int32_t* row_offsets32, const int32_t* col, int64_t n,
+                       int64_t num_edges, int32_t* symmetric, void* stream);
+/* int32 copy of int64 row offsets (E < 2^31) */
+int fs_narrow_offsets(const int64_t* row_offsets, int64_t len, int32_t* out, void* stream);
+/* fill n elements of elem_bytes (1, 2, 4, 8) with the low bytes of pattern */
+int fs_fill(void* ptr, int64_t n, int32_t elem_bytes, uint64_t pattern, void* stream);
+int fs_engine_uniform_s_age(const fs_engine* e);
 /* which of the two infectivity / mask buffers holds the current step's input */
 int fs_engine_current_buffer(fs_engine* e, void* stream);
 

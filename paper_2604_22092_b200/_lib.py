@@ -182,6 +182,17 @@ _SIGNATURES = {
     "fs_markov_influence": (_c_i32, [_vp, _vp, _vp]),
     "fs_markov_refresh_rates": (_c_i32, [_vp, _vp]),
     "fs_engine_uses_count_gather": (_c_i32, [_vp]),
+    "fs_engine_kernels_per_step": (_c_i32, [_vp]),
+    "fs_engine_sync_ages": (_c_i32, [_vp, _vp]),
+    "fs_engine_state_restored": (_c_i32, [_vp, _vp]),
+    "fs_seed_select": (_c_i32, [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, _vp, ctypes.c_int32, ctypes.c_int32,
+                                _vp, ctypes.c_int32, ctypes.c_float, _vp, _vp]),
+    "fs_flags_to_ids": (_c_i32, [_vp, ctypes.c_int64, _vp, ctypes.POINTER(ctypes.c_int64), _vp]),
+    "fs_check_symmetric": (_c_i32, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int32),
+                                    _vp]),
+    "fs_narrow_offsets": (_c_i32, [_vp, ctypes.c_int64, _vp, _vp]),
+    "fs_fill": (_c_i32, [_vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, _vp]),
+    "fs_engine_uniform_s_age": (_c_i32, [_vp]),
     "fs_engine_current_buffer": (_c_i32, [_vp, _vp]),
     "fs_engine_begin_batch": (_c_i32, [_vp, _vp]),
     "fs_engine_step": (_c_i32, [_vp, _c_i32, _c_i32, _c_i32, _vp]),

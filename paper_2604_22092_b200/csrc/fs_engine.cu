@@ -84,6 +84,33 @@ __global__ void k_edit_pushes(const ST* __restrict__ states, const uint32_t* __r
   }
 }
 
+// min / max of the S nodes' age bits (f32 of the storage value; ages >= 0,
+// so the bit order is the value order)
+template <typename ST, typename AT>
+__global__ void k_s_age_range(const ST* __restrict__ states, const AT* __restrict__ ages, int64_t n, int s_comp,
+                              uint32_t* __restrict__ range) {
+  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if ((int)states[i] != s_comp) continue;
+    const uint32_t b = __float_as_uint(to_f32<AT>(ages[i]));
+    lo = min(lo, b);
+    hi = max(hi, b);
+  }
+  if (lo != 0xFFFFFFFFu) {
+    atomicMin(range, lo);
+    atomicMax(range + 1, hi);
+  }
+}
+
+// write the uniform S age into the ages array
+template <typename ST, typename AT>
+__global__ void k_fill_s_age(const ST* __restrict__ states, AT* __restrict__ ages, int64_t n, int s_comp,
+                             const uint32_t* __restrict__ bits) {
+  const AT a = from_f32<AT>(__uint_as_float(*bits));
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if ((int)states[i] == s_comp) ages[i] = a;
+}
+
 // first node n with row_offsets[n] >= chunk start, for every chunk boundary
 __global__ void k_chunk_first(const int64_t* __restrict__ ro, int64_t n, int64_t e, int64_t epb,
                               int64_t nchunks, int64_t* __restrict__ out) {
@@ -317,6 +344,12 @@ struct fs_engine {
   bool peers_linked = false;
   bool stream = false;         // k_step_incr fast path of the incremental mode
   StepFn stream_fn[2] = {nullptr, nullptr};
+  bool stream_memo = false, stream_hubs = false;  // k_step_incr variant flags
+  // uniform S age: eligible when every step runs k_step_incr
+  // and no transition re-enters S; on while every S node's age is equal
+  bool uni_ok = false;
+  bool s_uniform = false;
+  uint32_t* uni_range = nullptr;  // [2] device scratch: min / max S-age bits
   int stream_grid = 0;
   uint16_t* cnt = nullptr;
   uint32_t* delta[2] = {nullptr, nullptr};
@@ -423,6 +456,9 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.rng = e->c.rng;
   p.hprec = e->c.hazard_precision;
   p.inf_val = e->inf_val;
+  p.term_bits = 0;
+  for (int c = 0; c < e->m.num_compartments; ++c)
+    if (e->m.comp[c].terminal) p.term_bits |= 1u << c;
   return p;
 }
 
@@ -568,6 +604,64 @@ int reset_memo(fs_engine* e, cudaStream_t st) {
   return 0;
 }
 
+void drop_batch_graphs(fs_engine* e) {
+  for (auto& a : e->batch_exec)
+    for (auto& b : a)
+      for (auto& x : b)
+        if (x) { cudaGraphExecDestroy(x); x = nullptr; }
+}
+
+// S ages back into the ages array (the array is authoritative again for
+// every node; the uniform scalar stays valid)
+int sync_s_ages(fs_engine* e, cudaStream_t st) {
+  if (!e->s_uniform) return 0;
+  const int64_t n = e->g.num_nodes;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8));
+  const uint32_t* bits = &e->dstate[e->s_cur].s_age_bits;
+  if (e->mixed)
+    k_fill_s_age<int8_t, __half><<<blocks, 256, 0, st>>>((const int8_t*)e->b.states, (__half*)e->b.ages, n,
+                                                         e->m.edge_from, bits);
+  else
+    k_fill_s_age<int32_t, float><<<blocks, 256, 0, st>>>((const int32_t*)e->b.states, (float*)e->b.ages, n,
+                                                         e->m.edge_from, bits);
+  FS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// (re)decide the uniform-S-age mode from the ages array (engine creation,
+// host edits): on iff every S node holds the same age; the scalar is set to
+// it.  Switching the mode switches the step kernel, so batch graphs go.
+int recheck_uniform(fs_engine* e, cudaStream_t st) {
+  if (!e->uni_ok) return 0;
+  const int64_t n = e->g.num_nodes;
+  const uint32_t init[2] = {0xFFFFFFFFu, 0u};
+  FS_CUDA(cudaMemcpyAsync(e->uni_range, init, sizeof init, cudaMemcpyHostToDevice, st));
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8));
+  if (e->mixed)
+    k_s_age_range<int8_t, __half><<<blocks, 256, 0, st>>>((const int8_t*)e->b.states, (const __half*)e->b.ages, n,
+                                                          e->m.edge_from, e->uni_range);
+  else
+    k_s_age_range<int32_t, float><<<blocks, 256, 0, st>>>((const int32_t*)e->b.states, (const float*)e->b.ages, n,
+                                                          e->m.edge_from, e->uni_range);
+  uint32_t r[2];
+  FS_CUDA(cudaMemcpyAsync(r, e->uni_range, sizeof r, cudaMemcpyDeviceToHost, st));
+  FS_CUDA(cudaStreamSynchronize(st));
+  const bool none = r[0] == 0xFFFFFFFFu;  // no S node: any scalar will do
+  const bool uni = none || r[0] == r[1];
+  if (uni) {
+    const uint32_t bits = none ? 0u : r[0];
+    FS_CUDA(cudaMemcpyAsync(&e->dstate[e->s_cur].s_age_bits, &bits, sizeof bits, cudaMemcpyHostToDevice, st));
+    FS_CUDA(cudaStreamSynchronize(st));
+  }
+  if (uni != e->s_uniform) {
+    e->s_uniform = uni;
+    drop_batch_graphs(e);
+    for (int mat = 0; mat < 2; ++mat)
+      e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, e->stream_memo, e->stream_hubs, uni);
+  }
+  return 0;
+}
+
 // incremental counts from the current mask (buffer of step parity `step`)
 int recount(fs_engine* e, int64_t step, cudaStream_t st) {
   if (!e->incr) return 0;
@@ -674,8 +768,16 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
                         g->num_edges > 0 && (!part || part->mask_segment_words > 0);
   if (c->incremental == 1 && !can_incr) { delete e; return set_error(FS_EINVAL, "incremental counts need the count gather, an outgoing CSR, d_max < 32768 and one partition"); }
   e->incr = can_incr && c->incremental != 0;
-  e->merge = c->strategy == FS_MERGE && g->num_edges > 0 && !e->incr;
+  // MERGE (scale-free graphs): the edge-chunked merge gather kernel, then the
+  // step.  FS_MERGE_FUSED=1 runs one launch instead — the f32 fold thread per
+  // short slice and warp per hub (S_HYBRID), the count gather tile-
+  // cooperatively — which measured 2-3x slower on BA graphs: the hubs are the
+  // lowest node ids, so the warps of the first tiles fold tens of thousands
+  // of hub edges serially while the merge kernel spreads them by edge chunks
+  //
+  e->merge = c->strategy == FS_MERGE && g->num_edges > 0 && !e->incr && !getenv("FS_MERGE_FUSED");
   e->strat = c->strategy == FS_LANE ? S_WARP : S_THREAD;
+  if (c->strategy == FS_MERGE && !e->merge && !e->count_mode) e->strat = S_HYBRID;
   if (e->incr) e->gather = G_INCR;
   else if (e->merge) e->gather = G_PRE;
   else if (e->count_mode) e->gather = e->mask_smem ? G_COUNT_SMEM : G_COUNT_GLOBAL;
@@ -812,7 +914,8 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     // streaming kernel: per-node arrays readable to a multiple of 128 nodes
     if (buf->padded >= 2 && !getenv("FS_NO_STREAM")) {
       e->stream = true;
-      for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, false, g->d_max > 32);
+      e->stream_hubs = g->d_max > 32;
+      for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, false, e->stream_hubs, false);
       int socc = 1;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&socc, (const void*)e->stream_fn[0], 512, 0) != cudaSuccess || socc < 1) socc = 1;
       if (getenv("FS_INCR_CTAS_PER_SM")) socc = std::max(1, std::min(socc, atoi(getenv("FS_INCR_CTAS_PER_SM"))));
@@ -839,11 +942,25 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
       TRY(dalloc(&e->ctab, (size_t)2 * kCohortSlots * kCohortW));
       TRY(dalloc(&e->cage, (size_t)2 * kCohortW));
       TRY(reset_memo(e, nullptr));
-      if (e->stream)  // the memo's shared-memory table only in the variant that uses it
-        for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, true, g->d_max > 32);
+      if (e->stream) {  // the memo's shared-memory table only in the variant that uses it
+        e->stream_memo = true;
+        for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, true, e->stream_hubs, false);
+      }
     }
   }
   if (getenv("FS_NO_PDL")) e->pdl = false;
+  {
+    // uniform S age: only the streaming kernel keeps it, and only while no
+    // transition leads back into S (SIS re-enters S with its own ages)
+    bool reenter = m->comp[m->edge_from].terminal != 0;
+    for (int c2 = 0; c2 < m->num_compartments; ++c2)
+      if (c2 != m->edge_from && !m->comp[c2].terminal && m->comp[c2].succ == m->edge_from) reenter = true;
+    e->uni_ok = e->stream && !c->compaction && part == nullptr && !reenter && !getenv("FS_NO_UNI");
+    if (e->uni_ok) {
+      TRY(dalloc(&e->uni_range, 2));
+      TRY(recheck_uniform(e, nullptr));
+    }
+  }
   if (getenv("FS_DEBUG_TIMES")) {
     const size_t g = (size_t)std::max(std::max(e->step_grid, e->step_grid_general), e->stream_grid);
     TRY(dalloc(&e->dbg, g * (4 + 32) * 16));  // per-CTA block, then the per-warp block of the probe build
@@ -879,7 +996,7 @@ void fs_engine_destroy(fs_engine* e) {
   cudaDeviceSynchronize();  // no kernel of this engine is still in flight on any stream
   void* ptrs[] = {e->dstate, e->acc, e->log_clock, e->log_tau, e->log_counts, e->ptab,
                   e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag,
-                  e->cnt, e->entry, e->ctab, e->cage, e->dbg};
+                  e->cnt, e->entry, e->ctab, e->cage, e->dbg, e->uni_range};
   for (void* q : ptrs) if (q) cudaFreeAsync(q, (cudaStream_t)0);
   for (void* q : {(void*)e->delta[0], (void*)e->delta[1]})
     if (q) {
@@ -891,6 +1008,7 @@ void fs_engine_destroy(fs_engine* e) {
 }
 
 int fs_engine_uses_count_gather(const fs_engine* e) { return e && e->count_mode ? 1 : 0; }
+int fs_engine_kernels_per_step(const fs_engine* e) { return e ? (e->merge ? 2 : 1) : 0; }
 
 int fs_engine_current_buffer(fs_engine* e, void* stream) {
   fs_scalars s;
@@ -1030,6 +1148,7 @@ int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream) {
       FS_CUDA(cudaMemcpyAsync(e->b.infectivity[to], e->b.infectivity[from], bytes, cudaMemcpyDeviceToDevice, st));
     }
   }
+  d.s_age_bits = cur.s_age_bits;  // the uniform S age is not part of fs_scalars
   FS_CUDA(cudaMemcpyAsync(e->dstate + e->s_cur, &d, sizeof(DevState), cudaMemcpyHostToDevice, st));
   FS_CUDA(cudaMemsetAsync(e->acc, 0, 3 * sizeof(StepAcc), st));
   if ((in->step ^ cur.s.step) & 1) {  // pending deltas are indexed by step parity: rebuild
@@ -1105,6 +1224,7 @@ int fs_engine_states_edited(fs_engine* e, void* stream) {
   FS_CUDA(cudaSetDevice(e->device));
   cudaStream_t st = (cudaStream_t)stream;
   int rc = reset_memo(e, st);  // edited nodes no longer follow their age cohorts
+  if (!rc) rc = recheck_uniform(e, st);  // the caller synced S ages (fs_engine_sync_ages) before editing
   e->tiles_valid = false;       // an edit can revive nodes of an inactive tile
   if (rc || !e->incr) return rc;
   // under compaction, inactive tiles never fold their pending deltas: start
@@ -1127,8 +1247,34 @@ int fs_engine_states_edited(fs_engine* e, void* stream) {
 int fs_engine_reset_age_memo(fs_engine* e, void* stream) {
   if (!e) return set_error(FS_EINVAL, "null engine");
   FS_CUDA(cudaSetDevice(e->device));
-  return reset_memo(e, (cudaStream_t)stream);
+  const int rc = reset_memo(e, (cudaStream_t)stream);
+  return rc ? rc : recheck_uniform(e, (cudaStream_t)stream);
 }
+
+int fs_engine_state_restored(fs_engine* e, void* stream) {
+  if (!e) return set_error(FS_EINVAL, "null engine");
+  FS_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  // every per-node array and the mask were overwritten: the incremental
+  // counts and pending deltas are rebuilt from the current mask, the memo and
+  // the active tiles are stale, and the S-age mode is re-decided
+  int rc = reset_memo(e, st);
+  if (!rc && e->incr) {
+    if (e->world > 1) return set_error(FS_ESTATE, "restoring a partitioned engine is not supported");
+    rc = recount(e, e->h_step, st);
+  }
+  if (!rc) rc = recheck_uniform(e, st);
+  e->tiles_valid = false;
+  return rc;
+}
+
+int fs_engine_sync_ages(fs_engine* e, void* stream) {
+  if (!e) return set_error(FS_EINVAL, "null engine");
+  FS_CUDA(cudaSetDevice(e->device));
+  return sync_s_ages(e, (cudaStream_t)stream);
+}
+
+int fs_engine_uniform_s_age(const fs_engine* e) { return e && e->s_uniform ? 1 : 0; }
 
 int fs_engine_acc_get(fs_engine* e, uint64_t* out17, void* stream) {
   if (!e || !out17) return set_error(FS_EINVAL, "null argument");

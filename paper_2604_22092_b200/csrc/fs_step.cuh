@@ -26,7 +26,10 @@ constexpr int kCohortSlots = 2;                // age-dependent compartments wit
 constexpr int kCohortW = 1 << 10;              // cohorts (entry steps) per table: a ring
 
 constexpr uint32_t kDeltaBias = 0x8000u;  // pending delta d is stored as d + 0x8000 (|d| <= d_max < 2^15)
-enum Strat { S_THREAD = 0, S_WARP = 1 };
+// S_HYBRID: thread per node for slices of <= kWide edges, the whole warp for
+// longer ones (scale-free hubs) — the edge-merge dispatch fused into the step
+enum Strat { S_THREAD = 0, S_WARP = 1, S_HYBRID = 2 };
+constexpr int kWide = 32;
 
 // Device-side run scalars.  Two slots ping-pong (the host tracks which one
 // is current): step k reads slot `in` and its CTA 0 writes slot `out`, so no
@@ -36,7 +39,10 @@ enum Strat { S_THREAD = 0, S_WARP = 1 };
 struct DevState {
   fs_scalars s;
   int pending;
-  int pad_;
+  // uniform S age: the f32 bits of the storage-rounded age
+  // every S node has, advanced by the step kernels that keep S ages as this
+  // one scalar (k_step_incr<UNI>) instead of in the ages array
+  uint32_t s_age_bits;
 };
 // per-step accumulator (ring of 3): every CTA adds its count deltas and maxes
 // its max rate with non-returning atomics — no fence, no ticket, no tail CTA
@@ -110,6 +116,7 @@ struct StepParams {
   int rng;
   int hprec;
   float inf_val;                 // stored infectivity of an I node (count mode), promoted
+  uint32_t term_bits;            // bit c: compartment c is terminal
 };
 
 
@@ -371,14 +378,33 @@ __device__ __forceinline__ int count_tile(const int32_t* __restrict__ col, const
 
 // thread-per-node sequential f32 fold in CSR order: acc = f32(acc + f32(inf*w))
 // (renewal.py:289 + 60-68; T/test_renewal.py:27-37)
+// The loads of kFoldB edges are issued together (columns, then the gathered
+// infectivities), so a slice costs ~2 memory round trips per kFoldB edges
+// instead of 2 per edge; the adds stay one sequential chain in CSR order.
+#ifndef FS_FOLD_B
+#define FS_FOLD_B 8
+#endif
+constexpr int kFoldB = FS_FOLD_B;
 template <typename IT>
 __device__ __forceinline__ float fold_thread(const int32_t* __restrict__ col, const void* inf,
                                              const void* w, int w_bf16, int w_uniform, float w_val,
                                              int64_t lo, int64_t hi) {
   float acc = 0.0f;
-  for (int64_t e = lo; e < hi; ++e) {
-    float wv = w_uniform ? w_val : load_w(w, w_bf16, e);
-    acc = __fadd_rn(acc, __fmul_rn(load_inf<IT>(inf, __ldg(col + e)), wv));
+  for (int64_t e = lo; e < hi; e += kFoldB) {
+    int32_t c[kFoldB];
+    float v[kFoldB];
+#pragma unroll
+    for (int u = 0; u < kFoldB; ++u) c[u] = (e + u < hi) ? __ldg(col + e + u) : 0;
+#pragma unroll
+    for (int u = 0; u < kFoldB; ++u) {
+      if (e + u < hi) {
+        const float wv = w_uniform ? w_val : load_w(w, w_bf16, e + u);
+        v[u] = __fmul_rn(load_inf<IT>(inf, c[u]), wv);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kFoldB; ++u)
+      if (e + u < hi) acc = __fadd_rn(acc, v[u]);
   }
   return acc;
 }
@@ -402,6 +428,59 @@ __device__ __forceinline__ float fold_warp(const int32_t* __restrict__ col, cons
     for (int l = 0; l < live; ++l) acc = __fadd_rn(acc, __shfl_sync(kFull, v, l));
   }
   return acc;
+}
+
+// warp-cooperative fold of one long slice (a hub) in CSR order, exact: the
+// lanes gather 4 x 32 contributions at a time into a per-warp shared-memory
+// stage, and lane 0 adds them in order — one f32 add chain, as the reference's
+// sequential fold (renewal.py:60-68) — while the next 128 contributions are
+// already in flight.
+constexpr int kFoldStage = 128;
+template <typename IT>
+__device__ __forceinline__ float fold_warp_staged(const int32_t* __restrict__ col, const void* inf, const void* w,
+                                                  int w_bf16, int w_uniform, float w_val, int64_t lo, int64_t hi,
+                                                  int lane, float* stage) {
+  constexpr int R = kFoldStage / 32;
+  float acc = 0.0f;
+  float v[R];
+  auto gather = [&](int64_t base) {
+    int32_t c[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t e = base + 32 * r + lane;
+      c[r] = e < hi ? __ldg(col + e) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t e = base + 32 * r + lane;
+      v[r] = 0.0f;
+      if (e < hi) v[r] = __fmul_rn(load_inf<IT>(inf, c[r]), w_uniform ? w_val : load_w(w, w_bf16, e));
+    }
+  };
+  gather(lo);
+  for (int64_t base = lo; base < hi; base += kFoldStage) {
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r) stage[32 * r + lane] = v[r];
+    __syncwarp();
+    if (base + kFoldStage < hi) gather(base + kFoldStage);  // in flight during the chain below
+    if (lane == 0) {
+      const int64_t rem = hi - base;
+      const int live = rem < kFoldStage ? (int)rem : kFoldStage;
+      if (live == kFoldStage) {
+        const float4* s4 = reinterpret_cast<const float4*>(stage);
+#pragma unroll
+        for (int q = 0; q < kFoldStage / 4; ++q) {
+          const float4 x = s4[q];
+          acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, x.x), x.y), x.z), x.w);
+        }
+      } else {
+        for (int l = 0; l < live; ++l) acc = __fadd_rn(acc, stage[l]);
+      }
+    }
+  }
+  __syncwarp();
+  return __shfl_sync(kFull, acc, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -515,6 +594,15 @@ __device__ __forceinline__ void commit_step_start(const StepParams& p, const Ste
   for (int c = 0; c < FS_MAX_COMPARTMENTS; ++c) Z->d[c] = 0ull;
 }
 
+// uniform S age (k_step_incr<UNI>): every S node that does not fire ages by
+// f32(tau) and rounds to the storage type (renewal.py:540-542), so one scalar
+// advances for all of them; CTA 0 publishes it with the step's other scalars
+template <typename AT>
+__device__ __forceinline__ void commit_s_age(const StepParams& p, const StepConst& k) {
+  const float a = __uint_as_float(p.Sin->s_age_bits);
+  p.Sout->s_age_bits = __float_as_uint(to_f32<AT>(from_f32<AT>(__fadd_rn(a, k.tau_f))));
+}
+
 // next-step infectivity of a node in compartment ns at age nage (f32 gather;
 // renewal.py:556-565, cast on store by the caller)
 __device__ __forceinline__ float inf_value(const StepParams& p, const StepConst& k, int ns, float nage) {
@@ -556,7 +644,7 @@ __device__ __forceinline__ void push_delta(const StepParams& p, int nxt, int32_t
   else atomicSub(dn, one);
 }
 
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true>
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false>
 __device__ __forceinline__ void drain_entries(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh,
                                               const int* qn_node, const int* qn_state, const float* qn_age,
                                               const float* qn_press, int lane, int cnt, float& lmax,
@@ -566,7 +654,11 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
   int push = 0;  // +1 / -1: this node's infectious status changed
   const int n = ok ? qn_node[lane] : 0;
   const int s = ok ? qn_state[lane] : 0;
-  const float age = ok ? qn_age[lane] : 0.0f;
+  // UNI: phase A never loads ages; a queued nodal node loads its own here
+  // (S ages are the uniform scalar and are not needed for S rates)
+  const float age = !ok ? 0.0f
+                        : UNI ? (s == k.edge_from ? 0.0f : to_f32<AT>(reinterpret_cast<const AT*>(p.ages)[n]))
+                              : qn_age[lane];
   float rate = 0.0f;
   bool compute = false;
   if (ok) {
@@ -659,7 +751,7 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
     } else {
       nage = __fadd_rn(age, k.tau_f);  // queued nodes are never terminal
     }
-    reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
+    if (!UNI || fire || s != k.edge_from) reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
     if (k.write_inf) inf_nxt[n] = from_f32<IT>(inf_value(p, k, ns, nage));
     if (MAT) p.rates[n] = rate;
   }
@@ -712,23 +804,23 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
 }
 
 // phase B on this warp's own queue
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true>
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false>
 __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
                                             int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
-  drain_entries<ST, AT, IT, MAT, WARPS, HUBS>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
+  drain_entries<ST, AT, IT, MAT, WARPS, HUBS, UNI>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
                                               sh.q_press[warp], lane, cnt, lmax, mask_nxt, inf_nxt);
 }
 
 // phase A outcome of one tile (pressure already gathered): cheap outcomes
 // now, possible transitions appended to the warp queue (drained at 32)
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true>
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false>
 __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
                                              int lane, uint32_t tile, uint32_t n, bool valid, int s, float age,
                                              float pressure, int& qn, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
   const bool isS = s == k.edge_from;
   const bool term = valid && sh.term[s] != 0;
   const bool defer = valid && !term && (!isS || pressure > 0.0f);
-  if (valid && !term && !defer) {  // S with zero pressure: rate 0, ages
+  if (!UNI && valid && !term && !defer) {  // S with zero pressure: rate 0, ages (UNI: the uniform scalar)
     const float nage = __fadd_rn(age, k.tau_f);
     reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
     if (k.write_inf) inf_nxt[n] = from_f32<IT>(inf_value(p, k, s, nage));
@@ -754,7 +846,7 @@ __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepCons
   }
   qn += __popc(dm);
   if (qn >= 32) {
-    drain_queue<ST, AT, IT, MAT, WARPS, HUBS>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt);
+    drain_queue<ST, AT, IT, MAT, WARPS, HUBS, UNI>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt);
     if (lane < qn - 32) {
       sh.q_node[warp][lane] = sh.q_node[warp][32 + lane];
       sh.q_state[warp][lane] = sh.q_state[warp][32 + lane];
@@ -806,6 +898,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   constexpr int WARPS = BLOCK / 32;
   __shared__ StepShared<WARPS> sh;
   __shared__ __align__(8) uint64_t s_bar;
+  __shared__ __align__(16) float s_fold[STRAT == S_HYBRID ? WARPS * kFoldStage : 4];  // hub fold stages
   constexpr bool COUNT = (GATHER == G_COUNT_SMEM || GATHER == G_COUNT_GLOBAL);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -892,6 +985,18 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
                                                             l2_policy_stream(p.stream_evict_first));
           if (need) pressure = p.ptab_mul ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
         }
+      } else if (STRAT == S_HYBRID) {  // f32 fold: thread per short slice, warp per hub
+        const bool wide = need && (in.hi - in.lo > kWide);
+        if (need && !wide) pressure = fold_thread<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo, in.hi);
+        unsigned rest = __ballot_sync(kFull, wide);
+        while (rest) {
+          const int j = __ffs(rest) - 1;
+          rest &= rest - 1;
+          const int64_t lj = __shfl_sync(kFull, in.lo, j), hj = __shfl_sync(kFull, in.hi, j);
+          const float pj = fold_warp_staged<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lj, hj, lane,
+                                                s_fold + warp * kFoldStage);
+          if (lane == j) pressure = pj;
+        }
       } else {  // warp per node (LANE strategy)
         unsigned rest = todo;
         while (rest) {
@@ -930,7 +1035,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
 #ifndef FS_PF_DEPTH
 #define FS_PF_DEPTH 2
 #endif
-template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, int BLOCK>
+template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   constexpr int WARPS = BLOCK / 32;
   __shared__ StepShared<WARPS> sh;
@@ -949,7 +1054,10 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   pdl_wait();
   if (tid == 0) {
     s_k = step_const(p, true);
-    if (blockIdx.x == 0) commit_step_start(p, s_k);
+    if (blockIdx.x == 0) {
+      commit_step_start(p, s_k);
+      if (UNI) commit_s_age<AT>(p, s_k);
+    }
   }
   const ST* __restrict__ states = reinterpret_cast<const ST*>(p.states);
   const AT* __restrict__ ages = reinterpret_cast<const AT*>(p.ages);
@@ -961,7 +1069,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   auto load = [&](uint32_t t, const uint16_t* pend, In& in) {
     const uint32_t n = t * 32u + (uint32_t)lane;
     in.s = (int)states[n];
-    in.age = to_f32<AT>(ages[n]);
+    if (!UNI) in.age = to_f32<AT>(ages[n]);  // UNI: queued nodal nodes load their age in phase B
     in.c = cnt[n];
     in.d = pend[n];
   };
@@ -1018,14 +1126,25 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
       pend[n] = (uint16_t)kDeltaBias;
     }
     const int s = valid ? in.s : -1;
+    if (UNI && !MAT) {
+      // quiet tile: every lane absorbed, or S with no infectious in-neighbour
+      // (rate 0, and its age is the uniform scalar) — nothing but the
+      // next-step mask word to write
+      const bool quiet = !valid || ((p.term_bits >> s) & 1u) || (s == k.edge_from && c == 0u);
+      if (__all_sync(0xffffffffu, quiet)) {
+        const unsigned word = __ballot_sync(0xffffffffu, valid && s == k.infectious);
+        if (lane == 0) mask_nxt[p.tile_base + t] = word;
+        continue;
+      }
+    }
     const float pressure = (valid && (s == k.edge_from || MAT))
                                ? (p.ptab_mul ? __fmul_rn((float)c, p.ptab_c) : __ldg(p.ptab + c))
                                : 0.0f;
 #if FS_STEP_PROBE
     const int q0 = qn;
 #endif
-    tile_outcome<ST, AT, float, MAT, WARPS, HUBS>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure,
-                                                  qn, lmax, mask_nxt, nullptr);
+    tile_outcome<ST, AT, float, MAT, WARPS, HUBS, UNI>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure,
+                                                       qn, lmax, mask_nxt, nullptr);
 #if FS_STEP_PROBE
     pr_def += qn - q0 + (qn < q0 ? 32 : 0);
     pr_drains += qn < q0;
@@ -1037,8 +1156,8 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     const int gw = (int)blockIdx.x * WARPS + warp;
     const int prep = (MEMO && gw < kCohortW * p.ncslots) ? gw : -1;
     if (qn > 0 || prep >= 0)
-      drain_entries<ST, AT, float, MAT, WARPS, HUBS>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
-                                                      sh.q_press[warp], lane, qn, lmax, mask_nxt, nullptr, prep);
+      drain_entries<ST, AT, float, MAT, WARPS, HUBS, UNI>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
+                                                           sh.q_press[warp], lane, qn, lmax, mask_nxt, nullptr, prep);
   }
 #if FS_STEP_PROBE  // per-warp [phase end, deferred << 20 | mid-loop drains] after the per-CTA block
   if (p.dbg && lane == 0) {
@@ -1314,7 +1433,7 @@ using TmaFn = void (*)(const StepParams, const TmaLayout);
 
 // instantiation units
 StepFn pick_step(bool mixed, int gather, int strat, bool mat, int& block);  // fs_step_general.cu
-StepFn pick_stream(bool mixed, bool mat, bool memo, bool hubs);             // fs_step_incr.cu
+StepFn pick_stream(bool mixed, bool mat, bool memo, bool hubs, bool uni);           // fs_step_incr.cu
 MergeFn pick_merge(bool inf_bf16, int mode, int& block);                    // fs_step_incr.cu
 TmaFn pick_tma(bool mixed, bool smem_mask, bool mat, bool ptab_mul, int block);  // fs_step_tma.cu
 

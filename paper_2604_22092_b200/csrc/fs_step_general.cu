@@ -24,6 +24,7 @@ StepFn pick_step2(int gather, int strat, int& block) {
       return k_step<ST, AT, IT, G_INCR, S_THREAD, MAT, 512>;
     case G_F32:
       block = 512;
+      if (strat == S_HYBRID) return k_step<ST, AT, IT, G_F32, S_HYBRID, MAT, 512>;
       return strat == S_WARP ? k_step<ST, AT, IT, G_F32, S_WARP, MAT, 512>
                              : k_step<ST, AT, IT, G_F32, S_THREAD, MAT, 512>;
     default:

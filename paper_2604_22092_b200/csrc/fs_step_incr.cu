@@ -4,17 +4,23 @@
 
 namespace fs {
 
+template <bool MEMO, bool HUBS, bool UNI>
+StepFn pick_stream3(bool mixed, bool mat) {
+  if (mixed) return mat ? k_step_incr<int8_t, __half, true, MEMO, HUBS, UNI, 512> : k_step_incr<int8_t, __half, false, MEMO, HUBS, UNI, 512>;
+  return mat ? k_step_incr<int32_t, float, true, MEMO, HUBS, UNI, 512> : k_step_incr<int32_t, float, false, MEMO, HUBS, UNI, 512>;
+}
+
 template <bool MEMO, bool HUBS>
-StepFn pick_stream2(bool mixed, bool mat) {
-  if (mixed) return mat ? k_step_incr<int8_t, __half, true, MEMO, HUBS, 512> : k_step_incr<int8_t, __half, false, MEMO, HUBS, 512>;
-  return mat ? k_step_incr<int32_t, float, true, MEMO, HUBS, 512> : k_step_incr<int32_t, float, false, MEMO, HUBS, 512>;
+StepFn pick_stream2(bool mixed, bool mat, bool uni) {
+  return uni ? pick_stream3<MEMO, HUBS, true>(mixed, mat) : pick_stream3<MEMO, HUBS, false>(mixed, mat);
 }
 
 // MEMO: the age-cohort hazard memo's shared table; HUBS: warp-cooperative
-// pushes for rows over 32 edges (compiled out for bounded-degree graphs)
-StepFn pick_stream(bool mixed, bool mat, bool memo, bool hubs) {
-  if (memo) return hubs ? pick_stream2<true, true>(mixed, mat) : pick_stream2<true, false>(mixed, mat);
-  return hubs ? pick_stream2<false, true>(mixed, mat) : pick_stream2<false, false>(mixed, mat);
+// pushes for rows over 32 edges (compiled out for bounded-degree graphs);
+// UNI: S ages kept as one uniform scalar, quiet tiles skipped
+StepFn pick_stream(bool mixed, bool mat, bool memo, bool hubs, bool uni) {
+  if (memo) return hubs ? pick_stream2<true, true>(mixed, mat, uni) : pick_stream2<true, false>(mixed, mat, uni);
+  return hubs ? pick_stream2<false, true>(mixed, mat, uni) : pick_stream2<false, false>(mixed, mat, uni);
 }
 
 

@@ -144,12 +144,25 @@ def default_seed_count(num_nodes: int) -> int:
     return max(10, int(round(0.01 * num_nodes)))
 
 
+_BYTES = {torch.int8: 1, torch.uint8: 1, torch.int16: 2, torch.float16: 2, torch.bfloat16: 2, torch.int32: 4,
+          torch.float32: 4, torch.int64: 8, torch.float64: 8}
+
+
+def _fill(t: torch.Tensor, value) -> torch.Tensor:
+    """Fill a device buffer through the library (fs_fill) — torch only owns it."""
+    if t.numel():
+        pat = torch.tensor([value], dtype=t.dtype).view(torch.uint8).numpy().tobytes()
+        _lib.check(_lib.load().fs_fill(_lib.ptr(t), t.numel(), _BYTES[t.dtype], int.from_bytes(pat, "little"),
+                                       _device.stream_handle(t.device)))
+    return t
+
+
 def _node_buffer(n: int, dtype: torch.dtype, dev: torch.device, fill=0) -> torch.Tensor:
     """Per-node device array, allocated to a whole number of 128-node units
     (the streaming kernels read whole tiles / vectors, fs_state_buffers.padded)
     and returned as the [:n] view."""
     cap = (n + 127) // 128 * 128
-    return torch.full((cap,), fill, dtype=dtype, device=dev)[:n]
+    return _fill(torch.empty((cap,), dtype=dtype, device=dev), fill)[:n]
 
 
 def _storage(mixed: bool):
@@ -190,18 +203,16 @@ class _DeviceGraph:
         col_h = np.ascontiguousarray(g.col_indices, dtype=np.int32)
         _pin_host(g, "row_offsets", ro)
         _pin_host(g, "col_indices", col_h)
-        self.row_offsets = torch.from_numpy(ro).to(dev)
+        self.row_offsets = torch.empty(ro.size, dtype=torch.int64, device=dev)
+        self.row_offsets.copy_(torch.from_numpy(ro), non_blocking=True)
         # int32 copy for the hot kernels when every offset fits (halves the
         # offset stream; listed in DESIGN.md as an encoding).  Both the int32
         # offsets and the columns carry slack past the end for 16-byte TMA
         # bulk copies (fs_graph.padded).
-        self.row_offsets32 = None
-        if self.num_edges < 2**31:
-            r32 = torch.full((self.num_nodes + 1 + 8,), self.num_edges, dtype=torch.int32, device=dev)
-            r32[: self.num_nodes + 1] = self.row_offsets
-            self.row_offsets32 = r32[: self.num_nodes + 1]
-        col = torch.zeros(self.num_edges + 4, dtype=torch.int32, device=dev)
-        col[: self.num_edges] = torch.from_numpy(col_h).to(dev)
+        self.row_offsets32 = _narrow_offsets(self.row_offsets, self.num_nodes, self.num_edges, dev)
+        col = torch.empty(self.num_edges + 4, dtype=torch.int32, device=dev)
+        col[: self.num_edges].copy_(torch.from_numpy(col_h), non_blocking=True)
+        _fill(col[self.num_edges:], 0)
         self.col_indices = col[: self.num_edges]
         # host passes over the arrays run once per graph object and are cached
         # on it, like the symmetry check below
@@ -265,11 +276,7 @@ class _DeviceGraph:
         self.num_edges = int(g.num_edges)
         t = g.device_tensors()
         self.row_offsets = t["row_offsets"]
-        self.row_offsets32 = None
-        if self.num_edges < 2**31:
-            r32 = torch.full((self.num_nodes + 1 + 8,), self.num_edges, dtype=torch.int32, device=dev)
-            r32[: self.num_nodes + 1] = self.row_offsets
-            self.row_offsets32 = r32[: self.num_nodes + 1]
+        self.row_offsets32 = _narrow_offsets(self.row_offsets, self.num_nodes, self.num_edges, dev)
         self.col_indices = t["col_buffer"][: self.num_edges]
         self.uniform = True
         self.uniform_weight = float(g.uniform_weight)
@@ -282,19 +289,27 @@ class _DeviceGraph:
         return self
 
 
+def _narrow_offsets(ro: torch.Tensor, n: int, e: int, dev: torch.device):
+    """int32 offsets (+8 slack entries = E) when E < 2^31, else None."""
+    if e >= 2**31:
+        return None
+    r32 = torch.empty(n + 1 + 8, dtype=torch.int32, device=dev)
+    _lib.check(_lib.load().fs_narrow_offsets(_lib.ptr(ro), n + 1, _lib.ptr(r32), _device.stream_handle(dev)))
+    _fill(r32[n + 1:], e)
+    return r32[: n + 1]
+
+
 def _is_symmetric(dg) -> bool:
     """Is the incoming CSR its own transpose (an undirected graph, as every
-    reference generator makes, R/graph.py:221-231)?  Decided on the device:
-    the sorted (dst, src) keys equal the sorted (src, dst) keys."""
-    n, e = dg.num_nodes, dg.num_edges
-    if e == 0:
+    reference generator makes, R/graph.py:221-231)?  Decided on the device
+    (fs_check_symmetric): every edge's multiplicity equals its reverse's."""
+    if dg.num_edges == 0:
         return True
-    deg = dg.row_offsets[1:] - dg.row_offsets[:-1]
-    dst = torch.repeat_interleave(torch.arange(n, device=deg.device, dtype=torch.int64), deg)
-    src = dg.col_indices.to(torch.int64)
-    fwd = dst * n + src  # already sorted: rows by dst, slices by src
-    rev = torch.sort(src * n + dst).values
-    return bool(torch.equal(fwd, rev))
+    out = ctypes.c_int32()
+    _lib.check(_lib.load().fs_check_symmetric(_lib.ptr(dg.row_offsets), _lib.ptr(dg.row_offsets32),
+                                              _lib.ptr(dg.col_indices), dg.num_nodes, dg.num_edges,
+                                              ctypes.byref(out), _device.stream_handle(dg.row_offsets.device)))
+    return bool(out.value)
 
 
 def device_graph(g, mixed: bool = False) -> _DeviceGraph:
@@ -374,9 +389,9 @@ class _Engine:
         _, _, it = _storage(state.mixed_precision)
         if plan.count_mode:
             w = ((n + 31) // 32 + 1 + 3) // 4 * 4  # + a zero sentinel word, 16-byte multiple (TMA)
-            self.bufs = [torch.zeros(w, dtype=torch.int32, device=dev) for _ in range(2)]
+            self.bufs = [_fill(torch.empty(w, dtype=torch.int32, device=dev), 0) for _ in range(2)]
         else:
-            self.bufs = [torch.zeros(n, dtype=it, device=dev) for _ in range(2)]
+            self.bufs = [_fill(torch.empty(n, dtype=it, device=dev), 0) for _ in range(2)]
         self.materialize = materialize
         if materialize:
             state._ensure_debug_buffers()
@@ -404,6 +419,16 @@ class _Engine:
             self.handle = None
 
     __del__ = close
+
+    def sync_ages(self) -> None:
+        """Uniform S age back into the ages array (before host reads / edits)."""
+        _lib.check(self.lib.fs_engine_sync_ages(self.handle, self.stream))
+
+    def uniform_s_age(self) -> bool:
+        return bool(self.lib.fs_engine_uniform_s_age(self.handle))
+
+    def kernels_per_step(self) -> int:
+        return int(self.lib.fs_engine_kernels_per_step(self.handle))
 
     def scalars(self) -> _lib.FsScalars:
         s = _lib.FsScalars()
@@ -438,6 +463,7 @@ class _Engine:
         """Device copies of everything a step mutates (states, ages, the
         infectivity / mask double buffer, scalars) — for benchmarking the
         same step window twice."""
+        self.sync_ages()
         t = self.state._t
         return (t["states"].clone(), t["ages"].clone(), [b.clone() for b in self.bufs], self.scalars())
 
@@ -448,7 +474,9 @@ class _Engine:
         for dst, src in zip(self.bufs, bufs):
             dst.copy_(src)
         self.set_scalars(sc)
-        self.reset_age_memo()
+        # incremental counts / pending deltas follow the restored mask, not
+        # the steps run since the snapshot
+        _lib.check(self.lib.fs_engine_state_restored(self.handle, self.stream))
 
     def states_edited(self) -> None:
         _lib.check(self.lib.fs_engine_states_edited(self.handle, self.stream))
@@ -533,6 +561,7 @@ class RenewalState:
             return
         s = self._engine.scalars()
         inf = self._engine.store_infectivity()
+        self._engine.sync_ages()  # the state's ages array is authoritative without an engine
         self._engine.close()
         self._engine = None
         self._host_scal = s
@@ -581,7 +610,7 @@ class RenewalState:
     def _ensure_debug_buffers(self) -> None:
         for name in ("pressure", "rates"):
             if name not in self._t:
-                self._t[name] = torch.zeros(self._n, dtype=torch.float32, device=self._dev)
+                self._t[name] = _fill(torch.empty(self._n, dtype=torch.float32, device=self._dev), 0.0)
 
     # ---- host mirror -----------------------------------------------------
     def _download(self, name: str) -> np.ndarray:
@@ -589,6 +618,8 @@ class RenewalState:
             return _device.to_host(self._current_infectivity())
         if name in ("pressure", "rates") and name not in self._t:
             return np.zeros(self._n, dtype=np.float32)
+        if name == "ages" and self._engine is not None:
+            self._engine.sync_ages()
         return _device.to_host(self._t[name])
 
     def _view(self, name: str) -> np.ndarray:
@@ -623,6 +654,8 @@ class RenewalState:
         dtype = {"states": st, "ages": at}.get(name, torch.float32)
         if name in ("pressure", "rates"):
             self._ensure_debug_buffers()
+        if name == "states" and self._engine is not None:
+            self._engine.sync_ages()  # untouched S nodes keep their true age in the array
         self._t[name].copy_(_device.to_device(_host_cast(arr, dtype), self._dev))
         if name == "states" and self._engine is not None:
             self._engine.states_edited()  # age cohorts, and the pushes of implied status changes
@@ -649,6 +682,8 @@ class RenewalState:
     def device_tensors(self) -> dict:
         """The live device buffers (no copies)."""
         self._push_host()
+        if self._engine is not None:
+            self._engine.sync_ages()
         return dict(self._t)
 
     @property
@@ -734,25 +769,35 @@ for _name in _ARRAYS:
 # ----------------------------------------------------------------------
 
 
+def _seed_select(n: int, seed: int, count: int, dev: torch.device, states=None, comp: int = 0, inf=None,
+                 inf_value: float = 0.0, flags=None) -> None:
+    """fs_seed_select: the `count` nodes with the smallest
+    u(derive_seed(seed, salt), 0, id) (renewal.py:162-169), marked on the device."""
+    if not 0 <= count <= n:
+        raise ValueError(f"seed count {count} outside [0, N]")
+    st_dt = _lib.I8 if states is not None and states.dtype == torch.int8 else _lib.I32
+    inf_dt = _lib.BF16 if inf is not None and inf.dtype == torch.bfloat16 else _lib.F32
+    _lib.check(_lib.load().fs_seed_select(n, derive_seed(seed, _SEED_PICK_SALT) & ((1 << 64) - 1), count,
+                                          _lib.ptr(states), st_dt, int(comp), _lib.ptr(inf), inf_dt,
+                                          float(inf_value), _lib.ptr(flags), _device.stream_handle(dev)))
+
+
 def _pick_seed_nodes(n: int, seed: int, count: int, dev: torch.device) -> torch.Tensor:
     """The `count` nodes with the smallest u(derive_seed(seed, salt), 0, id)
-    (renewal.py:162-169), chosen on the device."""
+    (renewal.py:162-169), chosen on the device; sorted int64 ids."""
     if not 0 <= count <= n:
         raise ValueError(f"seed count {count} outside [0, N]")
     if count == 0:
         return torch.empty(0, dtype=torch.int64, device=dev)
-    u = uniform_array(derive_seed(seed, _SEED_PICK_SALT), 0, n=n)
-    if n > (1 << 22) and count < n // 4:
-        # exact prefilter: the `count` smallest of the candidates below a
-        # threshold are the `count` smallest overall whenever at least
-        # `count` values fall below it (expected 1.25 count + 8 sigma)
-        thr = min(1.0, (1.25 * count + 8.0 * (count ** 0.5) + 64.0) / n)
-        cand = torch.nonzero(u < thr).squeeze(1)
-        if cand.numel() >= count:
-            pick = torch.topk(u[cand], count, largest=False, sorted=False).indices
-            return torch.sort(cand[pick]).values
-    idx = torch.topk(u, count, largest=False, sorted=False).indices
-    return torch.sort(idx).values
+    flags = torch.empty(n, dtype=torch.uint8, device=dev)
+    _seed_select(n, seed, count, dev, flags=flags)
+    ids = torch.empty(count, dtype=torch.int64, device=dev)
+    got = ctypes.c_int64()
+    _lib.check(_lib.load().fs_flags_to_ids(_lib.ptr(flags), n, _lib.ptr(ids), ctypes.byref(got),
+                                           _device.stream_handle(dev)))
+    if got.value != count:
+        raise AssertionError(f"seed selection picked {got.value} nodes, expected {count}")
+    return ids
 
 
 def init_renewal_state(g, m, cfg: RenewalConfig, seed: int, seed_count: int | None = None,
@@ -771,14 +816,14 @@ def init_renewal_state(g, m, cfg: RenewalConfig, seed: int, seed_count: int | No
     mixed = bool(cfg.mixed_precision)
     st, at, it = _storage(mixed)
     states = _node_buffer(n, st, dev, int(m.edge_from))
-    if seed_count:
-        states[_pick_seed_nodes(n, seed, seed_count, dev)] = comp
     ages = _node_buffer(n, at, dev)
     # infectivity beta * s(0): s(0) = 1 for constant transmission and 0 for
     # the hazard / density profiles (h(0) = 0, f(0) = 0)
-    inf = torch.zeros(n, dtype=it, device=dev)
-    if comp == m.infectious and m.transmission.kind == "constant" and seed_count:
-        inf[states == comp] = float(np.float32(m.beta))
+    inf = _fill(torch.empty(n, dtype=it, device=dev), 0)
+    seeded_inf = comp == m.infectious and m.transmission.kind == "constant"
+    if seed_count:
+        _seed_select(n, seed, seed_count, dev, states=states, comp=comp, inf=inf if seeded_inf else None,
+                     inf_value=float(np.float32(m.beta)))
     counts = np.zeros(m.num_compartments, dtype=np.int64)
     counts[m.edge_from] += n - seed_count
     counts[comp] += seed_count

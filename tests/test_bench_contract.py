@@ -32,11 +32,23 @@ def test_reference_arm_line_c1():
 
 def test_roofline_block_fields():
     pk = {"hbm_gbs": 6537.6, "source": "measured"}
-    r = bench.roofline_block(3000.0, pk, 12_000_000, 0.025, 112.0)
+    ncu = {"dram_bytes_per_launch": 12_000_000, "gpu_time_us": 20.0, "kernel": "k", "lib_sha16": "x"}
+    r = bench.roofline_block(3000.0, pk, ncu, 0.025, 112.0)
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] == 6537.6
     assert r["frac"] == pytest.approx(3000.0 / 6537.6)
     assert r["traffic"] == 12_000_000 and r["bytes_per_update"] == 112.0
     assert r["traffic_gbs"] == pytest.approx(12_000_000 / 0.025e-3 / 1e9)
+    assert r["frac_physical"] == pytest.approx(12_000_000 / 20e-6 / 1e9 / 6537.6)
+    assert r["ncu_same_build"] is False  # the sha does not match the built library
+    assert "frac_physical" not in bench.roofline_block(3000.0, pk, {}, 0.025, 112.0)
+
+
+def test_both_arms_share_the_workload_config():
+    for name, w in bench.WORKLOADS.items():
+        for world in (1, 8):
+            a = bench.workload_config(w, w["n"], world)
+            assert a == bench.workload_config(w, w["n"], world)
+            assert set(a) == {"workload", "n", "graph_seed", "sim_seed", "precision", "gather_option", "l2"}
 
 
 def test_clock_sampler_parses_reasons_and_memory_clock():

@@ -336,3 +336,88 @@ def test_host_state_edits_mid_run(gather, edit_inf):
     assert np.array_equal(st.states.astype(np.int32), ref.states.astype(np.int32))
     assert np.array_equal(st.pressure, ref.pressure)
     assert st.clock == ref.clock
+
+
+def test_snapshot_restore_replays_the_same_steps():
+    """bench.py times a step window twice (warm, then flushed) from one
+    snapshot: after a restore the engine must replay exactly the same
+    trajectory — counts, states, ages, clock — including its incremental
+    counts and pending deltas (fs_engine_state_restored)."""
+    meta, g, m, cfg, ref = trajectory_case("c1")
+    st = fs.init_renewal_state(g, m, cfg, meta["seed"])
+    plan = R._build_plan(g, m, cfg, st.mixed_precision)
+    eng = st._bind(plan, meta["seed"], materialize=False)
+    eng.step(10, False, False)
+    snap = eng.snapshot()
+    runs = []
+    for _ in range(2):
+        eng.restore(snap)
+        eng.run_batch(False)   # a graph-replayed batch ...
+        eng.step(37, False, False)  # ... and eager steps: 10 + 50 + 37 = 97 (odd parity)
+        st._after_device()
+        runs.append((st.states.copy(), st.ages.copy(), st.counts.copy(), st.clock))
+    for a, b in zip(runs[0], runs[1]):
+        assert np.array_equal(a, b)
+    eng.restore(snap)
+    eng.step(190, False, False)
+    st._after_device()
+    assert np.array_equal(st.states.astype(np.int32), ref["states"]) and np.array_equal(st.ages, ref["ages"])
+    assert np.array_equal(st.counts, ref["counts"][199]) and st.clock == ref["clock"][199]
+
+
+@pytest.mark.parametrize("mixed", [False, True])
+def test_uniform_s_age_mode_and_reentry_edit(mixed):
+    """SEIR never re-enters S, so the engine keeps the S age as one scalar
+    (DESIGN.md §3.4): host reads of `ages` still see every S node's age, and
+    an edit that puts a node back into S with a different age switches the
+    mode off — the run stays exact against the oracle either way."""
+    g, m = graph("er_300"), model("seir")
+    cfg = fs.RenewalConfig(mixed_precision=mixed)
+    st = fs.init_renewal_state(g, m, cfg, 5)
+    ref = O.init_state(g, m, cfg, 5)
+    for _ in range(60):
+        fs.renewal_step(st, g, m, cfg, 5)
+        O.step(ref, g, m, cfg, 5)
+    assert st._engine.uniform_s_age()
+    assert np.array_equal(st.ages, ref.ages)
+    r_nodes = np.flatnonzero(ref.states == 3)[:3]
+    e_nodes = np.flatnonzero(ref.states == 1)[:3]
+    assert r_nodes.size and e_nodes.size
+    for arr in (st.states, ref.states):
+        arr[r_nodes] = 0  # R -> S, keeping the R node's own (different) age
+        arr[e_nodes] = 0
+    c = np.bincount(ref.states.astype(np.int64), minlength=4)
+    st.counts = c
+    ref.counts = c.copy()
+    fs.renewal_step(st, g, m, cfg, 5)
+    O.step(ref, g, m, cfg, 5)
+    assert not st._engine.uniform_s_age()
+    for _ in range(40):
+        fs.renewal_step(st, g, m, cfg, 5)
+        O.step(ref, g, m, cfg, 5)
+    assert np.array_equal(st.counts, ref.counts) and np.array_equal(st.states, ref.states)
+    assert np.array_equal(st.ages, ref.ages) and st.clock == ref.clock
+
+
+@pytest.mark.parametrize("n,count", [(1, 1), (300, 0), (300, 1), (300, 299), (300, 300), (5000, 50),
+                                     (200_000, 2000), (3_000_000, 30_000)])
+def test_seed_selection_matches_reference_choice(n, count):
+    """fs_seed_select (device radix select, several digit passes at the
+    larger sizes) picks exactly the reference's _pick_seed_nodes set
+    (R/renewal.py:162-169): the `count` smallest uniforms."""
+    ids = R._pick_seed_nodes(n, 11, count, torch.device("cuda")).cpu().numpy()
+    u = O.uniform_array(O.derive_seed(11, 0x5EEDC0DE), 0, np.arange(n, dtype=np.uint64))
+    want = np.sort(np.argpartition(u, count - 1)[:count]) if count else np.empty(0, np.int64)
+    assert np.array_equal(ids, want)
+
+
+def test_symmetry_check_on_device():
+    from paper_2604_22092_b200.renewal import device_graph
+
+    assert device_graph(graph("ba_2000")).symmetric and device_graph(graph("er_300")).symmetric
+    assert not device_graph(fs.build_csr([(0, 1, 1.0), (1, 2, 1.0)], 3)).symmetric  # directed chain
+    # multiplicities must match too (a hand-built multigraph CSR): 0->1 twice, 1->0 once
+    multi = fs.CsrGraph(2, 3, np.array([0, 1, 3]), np.array([1, 0, 0], np.int32), np.ones(3, np.float32))
+    assert not device_graph(multi).symmetric
+    multi2 = fs.CsrGraph(2, 4, np.array([0, 2, 4]), np.array([1, 1, 0, 0], np.int32), np.ones(4, np.float32))
+    assert device_graph(multi2).symmetric
