@@ -246,6 +246,23 @@ int fs_engine_sync_ages(fs_engine* e, void* stream);
  * reference's state is plain numpy arrays). */
 int fs_engine_state_restored(fs_engine* e, void* stream);
 
+/* Log of the replayed batch that ended at step first_step + n (a batch
+ * launched by fs_engine_run_batch; the engine keeps the last 8): waits for
+ * that batch only and copies its per-step clocks / taus / counts on a side
+ * stream, so the next batch can already be running — the pipelined
+ * run_renewal loop (R/renewal.py:632-663 reads the recorder after each
+ * batch).  Every replayed batch ends by folding its last step's counts. */
+int fs_engine_wait_log(fs_engine* e, int64_t first_step, int32_t n, double* clocks, double* taus, int64_t* counts);
+
+/* ---- host side of the upload (fs_hostio.cpp) --------------------------- */
+/* host -> device copy of a pageable array through the library's page-locked
+ * staging slots, host threads filling one slot while the next is in flight */
+int fs_h2d_staged(void* dst, const void* src, int64_t bytes, void* stream);
+/* max in-degree of an int64 CSR (R/graph.py:194-201) and whether every f32
+ * weight is equal (the uniform-weight scalar), with host threads */
+int fs_host_csr_scan(const int64_t* row_offsets, int64_t n, const float* weights, int64_t num_edges, int64_t* d_max,
+                     int32_t* uniform, float* w0);
+
 /* ---- run setup on the device (fs_setup.cu) ------------------------------ */
 /* Seed choice of init_renewal_state: the `count` nodes with the smallest
  * uniform_array(seed_key, 0, id) (R/renewal.py:162-169 _pick_seed_nodes,

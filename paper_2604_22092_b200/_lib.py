@@ -192,6 +192,10 @@ _SIGNATURES = {
                                     _vp]),
     "fs_narrow_offsets": (_c_i32, [_vp, ctypes.c_int64, _vp, _vp]),
     "fs_fill": (_c_i32, [_vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, _vp]),
+    "fs_engine_wait_log": (_c_i32, [_vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp, _vp]),
+    "fs_h2d_staged": (_c_i32, [_vp, _vp, ctypes.c_int64, _vp]),
+    "fs_host_csr_scan": (_c_i32, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                                  ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_float)]),
     "fs_engine_uniform_s_age": (_c_i32, [_vp]),
     "fs_engine_current_buffer": (_c_i32, [_vp, _vp]),
     "fs_engine_begin_batch": (_c_i32, [_vp, _vp]),

@@ -331,6 +331,13 @@ struct fs_engine {
   int* bad_flag = nullptr;
   // CUDA graphs of one batch (index: materialise last step)
   cudaStream_t cap_stream = nullptr;
+  // pipelined batches: each replay records an event after its steps and the
+  // final fold, so the host can read one batch's log while the next runs
+  static constexpr int kBatchEv = 8;
+  cudaEvent_t batch_ev[kBatchEv] = {};
+  int64_t batch_ev_end[kBatchEv] = {};  // step count after the batch (-1: unused)
+  int batch_ev_next = 0;
+  cudaStream_t copy_stream = nullptr;
   cudaGraphExec_t batch_exec[2][2][6] = {};  // [materialise][scalar slot][step % 6]: parity and exchange slot are baked in
   bool compaction_ready = false;
   bool tiles_valid = false;  // active tile list matches the states (set by begin_batch / refresh_tiles)
@@ -967,6 +974,11 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * g * (4 + 32) * 16));
   }
   FS_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+  FS_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < fs_engine::kBatchEv; ++i) {
+    FS_CUDA(cudaEventCreateWithFlags(&e->batch_ev[i], cudaEventDisableTiming));
+    e->batch_ev_end[i] = -1;
+  }
   FS_CUDA(cudaGetLastError());
   FS_CUDA(cudaDeviceSynchronize());
 #undef TRY
@@ -993,6 +1005,8 @@ void fs_engine_destroy(fs_engine* e) {
     for (auto& b : a)
       for (auto& x : b) if (x) cudaGraphExecDestroy(x);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+  if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
+  for (auto& ev : e->batch_ev) if (ev) cudaEventDestroy(ev);
   cudaDeviceSynchronize();  // no kernel of this engine is still in flight on any stream
   void* ptrs[] = {e->dstate, e->acc, e->log_clock, e->log_tau, e->log_counts, e->ptab,
                   e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag,
@@ -1053,6 +1067,13 @@ int fs_engine_run_batch(fs_engine* e, int32_t materialize, void* stream) {
     FS_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = launch_begin_batch(e, e->cap_stream);
     if (!rc) rc = launch_steps(e, e->c.steps_per_batch, materialize != 0, e->c.compaction != 0, e->cap_stream);
+    if (!rc) {
+      // fold the last step's counts into the scalars and the log at the end
+      // of the batch (what the next batch's prologue would do first), so the
+      // batch's whole log is final when its graph completes
+      k_begin_batch<<<1, 32, 0, e->cap_stream>>>(e->dstate + e->s_cur, e->acc, e->log_counts, e->log_cap,
+                                                 e->m.num_compartments, e->c.epsilon, e->c.tau_max, e->c.delta, 1);
+    }
     cudaError_t err = cudaStreamEndCapture(e->cap_stream, &graph);
     e->s_cur = s0;  // capture does not execute
     e->h_step = h0;
@@ -1065,6 +1086,42 @@ int fs_engine_run_batch(fs_engine* e, int32_t materialize, void* stream) {
   FS_CUDA(cudaGraphLaunch(exec, (cudaStream_t)stream));
   e->s_cur = s0 ^ (e->c.steps_per_batch & 1);
   e->h_step = h0 + e->c.steps_per_batch;
+  const int slot = e->batch_ev_next;
+  e->batch_ev_next = (slot + 1) % fs_engine::kBatchEv;
+  FS_CUDA(cudaEventRecord(e->batch_ev[slot], (cudaStream_t)stream));
+  e->batch_ev_end[slot] = e->h_step;
+  return 0;
+}
+
+int fs_engine_wait_log(fs_engine* e, int64_t first_step, int32_t n, double* clocks, double* taus, int64_t* counts) {
+  if (!e || n < 0) return set_error(FS_EINVAL, "bad log request");
+  if (n > e->log_cap) return set_error(FS_EINVAL, "log request of %d steps exceeds capacity %lld", n, (long long)e->log_cap);
+  FS_CUDA(cudaSetDevice(e->device));
+  const int64_t end = first_step + n;
+  int slot = -1;
+  for (int i = 0; i < fs_engine::kBatchEv; ++i)
+    if (e->batch_ev_end[i] == end) slot = i;
+  if (slot < 0) return set_error(FS_EINVAL, "no replayed batch ends at step %lld", (long long)end);
+  if (e->h_step - first_step > e->log_cap)
+    return set_error(FS_EINVAL, "steps %lld.. were overwritten in the log ring", (long long)first_step);
+  FS_CUDA(cudaEventSynchronize(e->batch_ev[slot]));
+  const int M = e->m.num_compartments;
+  cudaStream_t cs = e->copy_stream;
+  // the batch's slots of the ring, in at most two contiguous pieces
+  std::vector<int64_t> lk((size_t)n * kCntStride);
+  for (int64_t done = 0; done < n;) {
+    const int64_t s0 = (first_step + done) % e->log_cap;
+    const int64_t len = std::min<int64_t>(n - done, e->log_cap - s0);
+    if (clocks) FS_CUDA(cudaMemcpyAsync(clocks + done, e->log_clock + s0, len * sizeof(double), cudaMemcpyDeviceToHost, cs));
+    if (taus) FS_CUDA(cudaMemcpyAsync(taus + done, e->log_tau + s0, len * sizeof(double), cudaMemcpyDeviceToHost, cs));
+    FS_CUDA(cudaMemcpyAsync(lk.data() + done * kCntStride, e->log_counts + s0 * kCntStride,
+                            len * kCntStride * sizeof(int64_t), cudaMemcpyDeviceToHost, cs));
+    done += len;
+  }
+  FS_CUDA(cudaStreamSynchronize(cs));
+  if (counts)
+    for (int i = 0; i < n; ++i)
+      for (int c2 = 0; c2 < M; ++c2) counts[(size_t)i * M + c2] = lk[(size_t)i * kCntStride + c2];
   return 0;
 }
 

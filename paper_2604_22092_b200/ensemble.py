@@ -7,7 +7,8 @@ seeds `derive_seed(seed, trial)` and results ordered by trial
 GPU at the same time: every trial owns an engine on its own CUDA stream,
 the graph's device copy is shared, and the host loop keeps `concurrency`
 trials in flight, launching one CUDA-graph batch per trial per round and
-reading each trial's per-batch log as it lands; the trajectory records
+reading each trial's per-batch log as it lands (one batch queued ahead of the one read, so the
+GPU never waits for the host); the trajectory records
 of all trials are built by one device launch (analysis.make_records).  Each trial is exactly
 `run_renewal(g, m, cfg, derive_seed(seed, trial), ...)` (same kernels, same
 per-trial RNG keys), so the ensemble is bit-identical to the sequential one
@@ -46,7 +47,7 @@ class _Trial:
         self.eng.run_batch(materialize=False)
 
     def collect(self, b: int, n: int) -> None:
-        clocks, _, counts = self.eng.read_log(self.done, b)
+        clocks, _, counts = self.eng.wait_log(self.done, b)  # this batch only; the next may be running
         _check_conservation(counts, n)
         self.times.extend(clocks.tolist())
         self.rows.extend(counts)
@@ -84,7 +85,9 @@ def run_ensemble(engine: str, g, m, cfg, seed: int, t_final: float, runs: int,
     torch.cuda.current_stream().synchronize()  # the graph upload precedes the trial streams
     while pending or live:
         while pending and free:
-            live.append(_Trial(pending.pop(0), g, m, cfg, seed, seed_count, seed_compartment, free.pop(), plan))
+            tr = _Trial(pending.pop(0), g, m, cfg, seed, seed_count, seed_compartment, free.pop(), plan)
+            tr.launch()  # pipelined: every live trial keeps one batch queued ahead of the one collected
+            live.append(tr)
         for tr in live:
             tr.launch()
         still = []

@@ -26,7 +26,6 @@ from __future__ import annotations
 import ctypes
 import os
 import time
-import weakref
 from dataclasses import dataclass, fields
 
 import numpy as np
@@ -177,20 +176,6 @@ def _storage(mixed: bool):
 # ----------------------------------------------------------------------
 
 
-def _pin_host(g, name: str, arr: np.ndarray) -> None:
-    """Page-lock a large host CSR array once per graph object (released with
-    the array): later uploads are direct DMA, and the pages cannot be
-    reclaimed by the OS between runs (which made repeated end-to-end runs
-    stall for 0.1-0.8 s on pageable memory)."""
-    pinned = g.__dict__.setdefault("_fs_pinned", {})
-    if arr.nbytes < (1 << 22) or pinned.get(name) is arr or arr is not getattr(g, name, None):
-        return  # small, already pinned, or a converted temporary
-    lib = _lib.load()
-    if lib.fs_host_register(arr.ctypes.data, arr.nbytes) == 0:
-        pinned[name] = arr
-        weakref.finalize(arr, lib.fs_host_unregister, ctypes.c_void_p(arr.ctypes.data))
-
-
 class _DeviceGraph:
     """CSR on the device, uploaded once per (graph, precision) and cached on
     the graph object.  Uniform weights (every generator's 1.0,
@@ -201,26 +186,33 @@ class _DeviceGraph:
         self.num_edges = int(g.num_edges)
         ro = np.ascontiguousarray(g.row_offsets, dtype=np.int64)
         col_h = np.ascontiguousarray(g.col_indices, dtype=np.int32)
-        _pin_host(g, "row_offsets", ro)
-        _pin_host(g, "col_indices", col_h)
+        lib = _lib.load()
+        stream = _device.stream_handle(dev)
+        # uploads through the library's page-locked staging slots (host
+        # threads copy one slot while the previous one is in flight)
         self.row_offsets = torch.empty(ro.size, dtype=torch.int64, device=dev)
-        self.row_offsets.copy_(torch.from_numpy(ro), non_blocking=True)
+        _lib.check(lib.fs_h2d_staged(_lib.ptr(self.row_offsets), ro.ctypes.data, ro.nbytes, stream))
         # int32 copy for the hot kernels when every offset fits (halves the
         # offset stream; listed in DESIGN.md as an encoding).  Both the int32
         # offsets and the columns carry slack past the end for 16-byte TMA
         # bulk copies (fs_graph.padded).
         self.row_offsets32 = _narrow_offsets(self.row_offsets, self.num_nodes, self.num_edges, dev)
         col = torch.empty(self.num_edges + 4, dtype=torch.int32, device=dev)
-        col[: self.num_edges].copy_(torch.from_numpy(col_h), non_blocking=True)
+        _lib.check(lib.fs_h2d_staged(_lib.ptr(col), col_h.ctypes.data, col_h.nbytes, stream))
         _fill(col[self.num_edges:], 0)
         self.col_indices = col[: self.num_edges]
-        # host passes over the arrays run once per graph object and are cached
-        # on it, like the symmetry check below
+        # host passes over the arrays (max degree, uniform weights) run once
+        # per graph object, in parallel host threads, and are cached on it,
+        # like the symmetry check below
         uni = g.__dict__.get("_fs_uniform")
-        if uni is None:
+        dm = g.__dict__.get("_fs_dmax")
+        if uni is None or dm is None:
             w32 = np.ascontiguousarray(g.weights, dtype=np.float32)
-            uni = g.__dict__["_fs_uniform"] = (bool(w32.size == 0 or (w32 == w32[0]).all()),
-                                               float(w32[0]) if w32.size else 1.0)
+            dmax, flag, w0 = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_float()
+            _lib.check(lib.fs_host_csr_scan(ro.ctypes.data, self.num_nodes, w32.ctypes.data, w32.size,
+                                            ctypes.byref(dmax), ctypes.byref(flag), ctypes.byref(w0)))
+            uni = g.__dict__["_fs_uniform"] = (bool(flag.value), float(w0.value) if w32.size else 1.0)
+            dm = g.__dict__["_fs_dmax"] = int(dmax.value)
         self.uniform = uni[0]
         if mixed:  # weights rounded to bf16 at plan time (renewal.py:330-331)
             import ml_dtypes
@@ -237,9 +229,6 @@ class _DeviceGraph:
                 w = w.astype(ml_dtypes.bfloat16)
             self.weights = _device.to_device(w, dev)
         self.weights_bf16 = mixed
-        dm = g.__dict__.get("_fs_dmax")
-        if dm is None:
-            dm = g.__dict__["_fs_dmax"] = int(np.diff(ro).max()) if self.num_nodes else 0
         self.d_max = dm
         # cached on the host graph like the reference caches its transpose
         # (R/graph.py:187-191 build_outgoing): a property of the arrays
@@ -485,6 +474,17 @@ class _Engine:
         fn = getattr(self.lib, "fs_engine_reset_age_memo", None)  # absent only in older A/B builds
         if fn is not None:
             _lib.check(fn(self.handle, self.stream))
+
+    def wait_log(self, first_step: int, n: int):
+        """Log of the replayed batch ending at first_step + n, waiting for that
+        batch only (later batches may be running)."""
+        M = self.plan.num_compartments
+        clocks = np.empty(n, dtype=np.float64)
+        taus = np.empty(n, dtype=np.float64)
+        counts = np.empty((n, M), dtype=np.int64)
+        _lib.check(self.lib.fs_engine_wait_log(self.handle, first_step, n, clocks.ctypes.data, taus.ctypes.data,
+                                               counts.ctypes.data))
+        return clocks, taus, counts
 
     def read_log(self, first_step: int, n: int):
         M = self.plan.num_compartments
@@ -993,10 +993,15 @@ def run_renewal(g, m, cfg: RenewalConfig, seed: int, t_final: float, grid_points
     rows = [state.counts.copy()]
     done, clock = 0, 0.0
     trace = [] if os.environ.get("FS_E2E_TRACE") else None  # per-batch wall times (diagnostics)
+    # pipelined: batch j+1 is queued before batch j's log is read, so the GPU
+    # never waits for the host; the loop stops at the first batch whose clock
+    # reaches t_final, exactly as the reference's (the one batch launched past
+    # it only advances this function's private state)
+    eng.run_batch(materialize=False)
     while clock < t_final:
         tb = time.perf_counter()
         eng.run_batch(materialize=False)
-        clocks, _, counts = eng.read_log(done, b)
+        clocks, _, counts = eng.wait_log(done, b)
         _check_conservation(counts, state._n)
         times.extend(clocks.tolist())
         rows.extend(counts)
