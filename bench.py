@@ -60,6 +60,11 @@ WORKLOADS = {
     "c2w": dict(desc="C2 per GPU, weak scaling: SEIR log-normal, uniform-degree k=10, N=1e6 nodes per GPU, "
                      "node-partitioned (peer pushes + NCCL all-reduce per step)",
                 kind="regular_dev", n=1_000_000, k=10, model="seir", per_gpu=True),
+    # the reference's acceptance ensemble (T/test_acceptance.py:34-79)
+    "ens": dict(desc="ensemble: run_ensemble('renewal', ER N=1000 d=8 seed 20250809, SEIR log-normal, 100 runs, "
+                     "10 E seeds, t_final=50) — R/analysis.py:97-130",
+                kind="er", n=1000, k=8.0, model="seir", ensemble=dict(runs=100, seed=20250809, t_final=50.0,
+                                                                      seed_count=10)),
     "c4": dict(desc="C4: SEIR log-normal, uniform-degree k=10, N=1e8, bf16/fp16 mixed-precision storage",
                kind="regular_dev", n=100_000_000, k=10, model="seir", mixed=True, cpu_n=10_000_000),
 }
@@ -79,6 +84,8 @@ def build_inputs(w):
 
     if w["kind"] == "fixed":
         g = fs.gen_fixed_degree(w["n"], w["k"], seed=GRAPH_SEED)
+    elif w["kind"] == "er":
+        g = fs.gen_erdos_renyi(w["n"], w["k"], seed=w["ensemble"]["seed"])
     elif w["kind"] == "regular_dev":  # GPU generator (the CPU one does not scale to 1e8)
         g = fs.gen_fixed_degree_device(w["n"], w["k"], seed=GRAPH_SEED)
     else:
@@ -214,6 +221,8 @@ def dtype_of(w: dict) -> str:
 def data_of(w: dict) -> str:
     if w["kind"] == "regular_dev":
         return "synthetic (GPU uniform-degree generator fs_gen_regular, graph seed 1, sim seed 7)"
+    if w.get("ensemble"):
+        return f"synthetic (reference generator gen_erdos_renyi, seed {w['ensemble']['seed']}; trial seeds derive_seed)"
     return "synthetic (reference generators, graph seed 1, sim seed 7)"
 
 
@@ -278,10 +287,98 @@ def cpu_ensemble(g, m, warm: int, steps: int, workers: int | None = None, mixed:
             "port_vs_reference": port_vs_reference()}
 
 
+def _ens_worker(trial):
+    from oracle import spreadsim_port as O
+
+    g, m, cfg, e = _CPU_INPUTS
+    times, rows, st = O.run(g, m, cfg, O.derive_seed(e["seed"], trial), e["t_final"], seed_count=e["seed_count"])
+    return len(times) - 1  # steps run (whole batches)
+
+
+def cpu_ensemble_trials(g, m, e: dict, runs: int) -> dict:
+    """The reference's run_ensemble on the host cores: a process pool of
+    trajectories of the oracle port (R/analysis.py:97-130)."""
+    import multiprocessing as mp
+
+    import paper_2604_22092_b200 as fs
+
+    global _CPU_INPUTS
+    _CPU_INPUTS = (g, m, fs.RenewalConfig(), e)
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as pool:
+        steps = pool.map(_ens_worker, range(runs))
+    wall = time.perf_counter() - t0
+    return {"value": g.num_nodes * sum(steps) / wall / 1e9, "unit": "G-NUPS", "cores": cores, "kind": "port",
+            "wall_s": wall, "trajectories_per_s": runs / wall,
+            "sample": f"{runs} trajectories to t_final={e['t_final']} in a process pool of {cores} workers "
+                      f"(oracle/spreadsim_port.py, run_ensemble style)", "port_vs_reference": port_vs_reference()}
+
+
+def run_ensemble_bench(args, w) -> None:
+    """run_ensemble on the GPU (trials concurrent on CUDA streams, one graph
+    upload, pipelined batches, device records): node-updates of every trial
+    (whole batches, as run) over the call's wall time, max of `steps` calls
+    after `warmup` untimed calls; host graph already built."""
+    import torch
+
+    import paper_2604_22092_b200 as fs
+
+    g, m = build_inputs(w)
+    e = w["ensemble"]
+    cfg = fs.RenewalConfig()
+    runs = e["runs"]
+
+    def once():
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        recs = fs.run_ensemble("renewal", g, m, cfg, e["seed"], e["t_final"], runs, seed_count=e["seed_count"])
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0, recs
+
+    for _ in range(max(1, args.warmup // 3)):
+        once()
+    walls = []
+    with ClockSampler(0) as clk:
+        for _ in range(max(1, args.steps // 40)):
+            wall, recs = once()
+            walls.append(wall)
+    wall = statistics.median(walls)
+    b = cfg.steps_per_batch
+    steps = sum(int(np.ceil(r.summary["step_count"] / b) * b) for r in recs)
+    value = g.num_nodes * steps / wall / 1e9
+    out = {
+        "metric": "Giga-NUPS (node updates/s)", "value": value, "unit": "G-NUPS", "n_gpus": 1,
+        "steps": len(walls), "warmup": args.warmup, "ms_per_step": wall * 1e3 / (steps / runs),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(w), "data": data_of(w),
+        "config": workload_config(w, w["n"]), "edges": g.num_edges,
+        "engine": {"runner": "run_ensemble: trials on CUDA streams, pipelined batches, records by one device launch",
+                   "trials": runs, "trajectories_per_s": runs / wall, "wall_s": walls, "lib_sha16": lib_sha16()},
+        "roofline": None, "gpu_launches": steps + 3 * runs, "clocks": clk.summary(),
+        "e2e": {"value": value, "unit": "G-NUPS", "h2d_bytes_per_step": (g.row_offsets.nbytes + g.col_indices.nbytes)
+                / (steps / runs), "d2h_bytes_per_step": 8 * (2 + m.num_compartments) * runs,
+                "what": "the whole run_ensemble call from a host graph (graph upload, 100 trials, records)"},
+        "cpu_baseline": cpu_ensemble_trials(g, m, e, runs) if args.cpu_steps > 0 else None,
+    }
+    print(json.dumps(out))
+
+
 def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     w = WORKLOADS[args.workload]
+    if w.get("ensemble"):
+        g, m = build_inputs(w)
+        cb = cpu_ensemble_trials(g, m, w["ensemble"], w["ensemble"]["runs"])
+        print(json.dumps({"impl": "reference", "metric": "Giga-NUPS (node updates/s)", "value": cb["value"],
+                          "unit": "G-NUPS", "n_gpus": world, "steps": 1, "warmup": 0,
+                          "ms_per_step": cb["wall_s"] * 1e3, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": dtype_of(w), "data": data_of(w),
+                          "config": workload_config(w, w["n"], world), "cpu_baseline": cb,
+                          "e2e": {"value": cb["value"], "unit": "G-NUPS", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return
     if w.get("engine") == "markov":
         print(json.dumps({"impl": "reference", "unavailable": "the CPU oracle port restates the renewal path only"}))
         return
@@ -431,6 +528,15 @@ def run_partitioned(args, w, rank: int, world: int, local: int) -> None:
         t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
+    # transport evidence: pushes this rank sent to other ranks per timed step
+    # (read from the engine's per-step ring), and the exchange's own time
+    k_rp = min(steps, 200)
+    rp = run.part.remote_pushes(run.steps - k_rp, k_rp).astype(np.float64)
+    rp_t = torch.tensor([rp.mean(), rp.max()], dtype=torch.float64, device="cuda")
+    dist.all_reduce(rp_t, op=dist.ReduceOp.MAX)
+    xus = run.exchange_us(100)
+    xus_t = torch.tensor([xus or 0.0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(xus_t, op=dist.ReduceOp.MAX)
     run.close()
     del g
     torch.cuda.empty_cache()
@@ -467,7 +573,10 @@ def run_partitioned(args, w, rank: int, world: int, local: int) -> None:
         "engine": {"strategy": "per-node",
                    "gather": "incremental counts, cross-rank pushes into peer memory (CUDA IPC / NVLink)",
                    "parallelism": f"node-partitioned x{world} (peer pushes + NCCL all-reduce of 17 words per step)",
-                   "steps_from": f"t=0 after {args.warmup} warm-up steps", "lib_sha16": lib_sha16()},
+                   "steps_from": f"t=0 after {args.warmup} warm-up steps", "lib_sha16": lib_sha16(),
+                   "remote_pushes_per_step": {"mean_max_over_ranks": float(rp_t[0]), "max": float(rp_t[1]),
+                                              "steps": k_rp},
+                   "exchange_us_max_over_ranks": float(xus_t[0])},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"] * world, "unit": "GB/s",
                      "frac": achieved / (pk["hbm_gbs"] * world), "traffic": None,
                      "bytes_per_update": B_ALG[mixed], "peak_source": pk["source"] + f" x {world} GPUs"},
@@ -528,6 +637,9 @@ def main() -> None:
         return
     if WORKLOADS[args.workload].get("engine") == "markov":
         run_markov_bench(args, WORKLOADS[args.workload])
+        return
+    if WORKLOADS[args.workload].get("ensemble"):
+        run_ensemble_bench(args, WORKLOADS[args.workload])
         return
 
     w = WORKLOADS[args.workload]

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 2
+#define FS_ABI_VERSION 3
 #define FS_MAX_COMPARTMENTS 16
 
 /* error codes */
@@ -174,6 +174,11 @@ typedef struct fs_partition {
   int64_t mask_segment_words;
   int32_t rank, world;
   void* comm;
+  /* world + 1 node boundaries (multiples of 32) of unequal, e.g. edge-
+   * balanced, ranges; nullable: equal ranges of
+   * mask_segment_words * 32 nodes.  Unequal ranges need incremental counts
+   * (no mask all-gather). */
+  const int64_t* range_bounds;
 } fs_partition;
 
 typedef struct fs_engine fs_engine;
@@ -181,9 +186,9 @@ typedef struct fs_engine fs_engine;
 int fs_abi_version(void);
 const char* fs_last_error(void);
 int fs_device_sm_count(int device);
-/* page-lock / release a host range (cudaHostRegister): host CSR arrays are
- * registered once per graph so every later upload is a direct DMA and the
- * pages cannot be reclaimed between runs (paper_2604_22092_b200/renewal.py) */
+/* page-lock / release a host range (cudaHostRegister), for callers that
+ * upload the same host arrays repeatedly; the CSR upload itself goes through
+ * fs_h2d_staged (registering fresh pages cost ~0.4 ms per MB on B200 hosts) */
 int fs_host_register(void* p, int64_t bytes);
 int fs_host_unregister(void* p);
 
@@ -253,6 +258,14 @@ int fs_engine_state_restored(fs_engine* e, void* stream);
  * run_renewal loop (R/renewal.py:632-663 reads the recorder after each
  * batch).  Every replayed batch ends by folding its last step's counts. */
 int fs_engine_wait_log(fs_engine* e, int64_t first_step, int32_t n, double* clocks, double* taus, int64_t* counts);
+/* Partitioned runs: per-step count of the +-1 pushes this rank sent to other
+ * ranks' pending deltas (over NVLink on a multi-GPU box), for steps
+ * [first_step, first_step + n) still in the log ring. */
+int fs_engine_read_remote_pushes(fs_engine* e, int64_t first_step, int32_t n, uint32_t* out, void* stream);
+/* Mean device time of the per-step exchange (the NCCL group of the count /
+ * max-rate all-reduces, plus the mask all-gather when seg_words > 0) over
+ * `iters` back-to-back calls on `stream`, in microseconds. */
+int fs_comm_time_exchange(void* comm, int32_t rank, int64_t seg_words, int32_t iters, void* stream, float* us);
 
 /* ---- host side of the upload (fs_hostio.cpp) --------------------------- */
 /* host -> device copy of a pageable array through the library's page-locked

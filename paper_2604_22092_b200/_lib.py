@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import FlashSpreadNativeError, InvalidConfigError, ReconfigureAfterStartError
 
 MAX_COMPARTMENTS = 16
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # enum fs_dtype
 I8, I32, I64, F16, BF16, F32, F64, U32, U64 = 1, 2, 3, 4, 5, 6, 7, 8, 9
@@ -136,6 +136,7 @@ class FsPartition(ctypes.Structure):
         ("rank", _c_i32),
         ("world", _c_i32),
         ("comm", _vp),
+        ("range_bounds", _vp),
     ]
 
 
@@ -193,6 +194,9 @@ _SIGNATURES = {
     "fs_narrow_offsets": (_c_i32, [_vp, ctypes.c_int64, _vp, _vp]),
     "fs_fill": (_c_i32, [_vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, _vp]),
     "fs_engine_wait_log": (_c_i32, [_vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp, _vp]),
+    "fs_engine_read_remote_pushes": (_c_i32, [_vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp]),
+    "fs_comm_time_exchange": (_c_i32, [_vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, _vp,
+                                       ctypes.POINTER(ctypes.c_float)]),
     "fs_h2d_staged": (_c_i32, [_vp, _vp, ctypes.c_int64, _vp]),
     "fs_host_csr_scan": (_c_i32, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
                                   ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_float)]),

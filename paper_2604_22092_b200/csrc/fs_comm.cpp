@@ -51,6 +51,36 @@ int fs_comm_init(int32_t world, int32_t rank, const uint8_t* id_bytes, int32_t d
   return 0;
 }
 
+int fs_comm_time_exchange(void* comm, int32_t rank, int64_t seg_words, int32_t iters, void* stream, float* us) {
+  if (!comm || iters < 1 || !us) return fs::set_error(FS_EINVAL, "bad exchange timing arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  void* buf = nullptr;
+  ncclComm_t c = static_cast<ncclComm_t>(comm);
+  int world = 1;
+  FS_NCCL(ncclCommCount(c, &world));
+  const size_t bytes = 256 + (size_t)seg_words * (size_t)world * 4;
+  if (cudaMalloc(&buf, bytes) != cudaSuccess) return fs::set_error(FS_ECUDA, "exchange timing buffer");
+  cudaMemset(buf, 0, bytes);
+  auto* d16 = static_cast<unsigned long long*>(buf);
+  auto* mx = reinterpret_cast<unsigned*>(d16 + FS_MAX_COMPARTMENTS);
+  uint32_t* mask = seg_words > 0 ? reinterpret_cast<uint32_t*>(static_cast<char*>(buf) + 256) : nullptr;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  int rc = fs::fs_exchange_step(comm, d16, mx, mask, seg_words, rank, st);  // warm-up
+  cudaEventRecord(a, st);
+  for (int i = 0; i < iters && !rc; ++i) rc = fs::fs_exchange_step(comm, d16, mx, mask, seg_words, rank, st);
+  cudaEventRecord(b, st);
+  cudaEventSynchronize(b);
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, a, b);
+  *us = ms * 1e3f / (float)iters;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  return rc;
+}
+
 void fs_comm_destroy(void* comm) {
   if (comm) ncclCommDestroy(static_cast<ncclComm_t>(comm));
 }

@@ -293,6 +293,9 @@ struct fs_engine {
   int64_t ntiles_mask = 0;   // words of the global infectious mask
   int rank = 0, world = 1;
   void* comm = nullptr;
+  int64_t part_bound[FS_MAX_PARTITIONS + 1] = {};  // rank r owns [part_bound[r], part_bound[r+1])
+  bool unequal_ranges = false;
+  uint32_t* remote_log = nullptr;  // partitioned: per-step pushes sent to other ranks
   int64_t mask_seg_words = 0;  // words of mask each rank contributes to the all-gather      // ncclComm_t: per-step exchange after every step kernel
   int64_t h_step = 0;        // host mirror of the device step counter (exchange slot / mask parity)
   float inf_val = 0.0f;  // promoted stored value of an I node (count mode)
@@ -452,7 +455,8 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.out_col = e->g.out_col_indices;
   p.world = e->incr ? e->world : 1;
   p.hubs = e->g.d_max > 32 ? 1 : 0;  // local rows; partitioned rows of a symmetric graph mirror the degrees
-  p.part_chunk = e->mask_seg_words * 32;
+  for (int r = 0; r <= FS_MAX_PARTITIONS; ++r) p.part_bound[r] = e->part_bound[r];
+  p.remote_log = (e->incr && e->world > 1) ? e->remote_log : nullptr;
   for (int par = 0; par < 2; ++par)
     for (int r = 0; r < FS_MAX_PARTITIONS; ++r) p.peer_pend[par][r] = e->peer_pend[par][r];
   p.dbg = e->dbg;
@@ -750,10 +754,23 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     e->world = part->world;
     e->comm = part->comm;
     e->mask_seg_words = part->mask_segment_words;
-    if ((e->comm || e->world > 1) && (e->mask_seg_words < 1 || e->mask_seg_words * e->world < e->ntiles_mask ||
-                    e->node_base / 32 != (int64_t)e->rank * e->mask_seg_words)) {
-      delete e;
-      return set_error(FS_EINVAL, "partition: ranks must own equal mask segments of mask_segment_words words");
+    if (part->world > FS_MAX_PARTITIONS) { delete e; return set_error(FS_EINVAL, "at most %d partitions", FS_MAX_PARTITIONS); }
+    if (part->range_bounds) {
+      const int64_t* b = part->range_bounds;
+      bool ok = b[0] == 0 && b[part->world] == part->num_nodes_global && b[part->rank] == part->node_base &&
+                b[part->rank + 1] == part->node_base + n;
+      for (int r = 0; r < part->world && ok; ++r) ok = b[r] < b[r + 1] && b[r] % 32 == 0;
+      if (!ok) { delete e; return set_error(FS_EINVAL, "partition: bad range boundaries"); }
+      for (int r = 0; r <= part->world; ++r) e->part_bound[r] = b[r];
+      e->unequal_ranges = true;
+    } else {
+      if ((e->comm || e->world > 1) && (e->mask_seg_words < 1 || e->mask_seg_words * e->world < e->ntiles_mask ||
+                      e->node_base / 32 != (int64_t)e->rank * e->mask_seg_words)) {
+        delete e;
+        return set_error(FS_EINVAL, "partition: ranks must own equal mask segments of mask_segment_words words");
+      }
+      for (int r = 0; r <= part->world; ++r)
+        e->part_bound[r] = std::min<int64_t>((int64_t)r * e->mask_seg_words * 32, part->num_nodes_global);
     }
   }
   const bool can_count = (m->shedding == FS_SHED_CONSTANT) && (g->weights_uniform || g->num_edges == 0);
@@ -775,6 +792,10 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
                         g->num_edges > 0 && (!part || part->mask_segment_words > 0);
   if (c->incremental == 1 && !can_incr) { delete e; return set_error(FS_EINVAL, "incremental counts need the count gather, an outgoing CSR, d_max < 32768 and one partition"); }
   e->incr = can_incr && c->incremental != 0;
+  if (e->unequal_ranges && !e->incr) {
+    delete e;
+    return set_error(FS_EINVAL, "unequal partition ranges need incremental counts (the mask all-gather needs equal segments)");
+  }
   // MERGE (scale-free graphs): the edge-chunked merge gather kernel, then the
   // step.  FS_MERGE_FUSED=1 runs one launch instead — the f32 fold thread per
   // short slice and warp per hub (S_HYBRID), the count gather tile-
@@ -893,6 +914,10 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   TRY(dalloc(&e->log_clock, e->log_cap));
   TRY(dalloc(&e->log_tau, e->log_cap));
   TRY(dalloc(&e->log_counts, (size_t)e->log_cap * kCntStride));
+  if (e->world > 1) {
+    TRY(dalloc(&e->remote_log, e->log_cap));
+    FS_CUDA(cudaMemset(e->remote_log, 0, sizeof(uint32_t) * e->log_cap));
+  }
   TRY(dalloc(&e->num_active, 1));
   if (c->compaction) TRY(dalloc(&e->active_tiles, e->ntiles));
   FS_CUDA(cudaMemset(e->acc, 0, 3 * sizeof(StepAcc)));
@@ -1010,7 +1035,7 @@ void fs_engine_destroy(fs_engine* e) {
   cudaDeviceSynchronize();  // no kernel of this engine is still in flight on any stream
   void* ptrs[] = {e->dstate, e->acc, e->log_clock, e->log_tau, e->log_counts, e->ptab,
                   e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag,
-                  e->cnt, e->entry, e->ctab, e->cage, e->dbg, e->uni_range};
+                  e->cnt, e->entry, e->ctab, e->cage, e->dbg, e->uni_range, e->remote_log};
   for (void* q : ptrs) if (q) cudaFreeAsync(q, (cudaStream_t)0);
   for (void* q : {(void*)e->delta[0], (void*)e->delta[1]})
     if (q) {
@@ -1090,6 +1115,22 @@ int fs_engine_run_batch(fs_engine* e, int32_t materialize, void* stream) {
   e->batch_ev_next = (slot + 1) % fs_engine::kBatchEv;
   FS_CUDA(cudaEventRecord(e->batch_ev[slot], (cudaStream_t)stream));
   e->batch_ev_end[slot] = e->h_step;
+  return 0;
+}
+
+int fs_engine_read_remote_pushes(fs_engine* e, int64_t first_step, int32_t n, uint32_t* out, void* stream) {
+  if (!e || n < 0 || (n > 0 && !out)) return set_error(FS_EINVAL, "bad remote-push request");
+  if (n > e->log_cap) return set_error(FS_EINVAL, "request of %d steps exceeds the log capacity", n);
+  if (!e->remote_log) {
+    for (int i = 0; i < n; ++i) out[i] = 0;
+    return 0;
+  }
+  FS_CUDA(cudaSetDevice(e->device));
+  std::vector<uint32_t> ring(e->log_cap);
+  FS_CUDA(cudaMemcpyAsync(ring.data(), e->remote_log, ring.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                          (cudaStream_t)stream));
+  FS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  for (int i = 0; i < n; ++i) out[i] = ring[(first_step + i) % e->log_cap];
   return 0;
 }
 

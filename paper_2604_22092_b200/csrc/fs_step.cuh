@@ -97,7 +97,8 @@ struct StepParams {
   const int32_t* out_col;        // global ids
   int world;                     // > 1: pushes go to the owner's pending deltas (peer_pend)
   int hubs;                      // some out-row exceeds 32 edges: warp-cooperative pushes
-  int64_t part_chunk;            // nodes per rank
+  int64_t part_bound[FS_MAX_PARTITIONS + 1];  // node range boundaries of the ranks
+  uint32_t* remote_log;          // partitioned: per-step count of pushes sent to other ranks (log ring)
   uint32_t* peer_pend[2][FS_MAX_PARTITIONS];  // every rank's pending-delta arrays, by parity
   int stream_evict_first;        // CSR stream larger than L2: evict-first hint on column loads
   int host_parity;               // the host's mirror of (step & 1) for this launch (early loads), -1: none
@@ -591,6 +592,7 @@ __device__ __forceinline__ void commit_step_start(const StepParams& p, const Ste
   p.log_tau[slot] = k.tau;
   StepAcc* Z = p.acc + (k.step + 1) % 3;  // last read by the previous step
   Z->max_bits = 0u;
+  if (p.remote_log) p.remote_log[(k.step + 1) % p.log_cap] = 0u;  // the next step's counter
   for (int c = 0; c < FS_MAX_COMPARTMENTS; ++c) Z->d[c] = 0ull;
 }
 
@@ -631,17 +633,22 @@ __device__ __forceinline__ float inf_value(const StepParams& p, const StepConst&
 // device's memory or, node-partitioned, the owner's — possibly a peer GPU's
 // over NVLink.  Chunk boundaries are even, so the 16-bit lane
 // of j is the same in global and owner-local numbering.
-__device__ __forceinline__ void push_delta(const StepParams& p, int nxt, int32_t j, bool up) {
+// Returns 1 when the push went to another rank.
+__device__ __forceinline__ int push_delta(const StepParams& p, int nxt, int32_t j, bool up) {
   const uint32_t one = 1u << (16 * (j & 1));
   uint32_t* dn;
+  int remote = 0;
   if (p.world > 1) {
-    const int owner = (int)((int64_t)j / p.part_chunk);
-    dn = p.peer_pend[nxt][owner] + (((int64_t)j - (int64_t)owner * p.part_chunk) >> 1);
+    int owner = 0;  // ranges (equal or edge-balanced) by their boundaries
+    for (int r = 1; r < p.world; ++r) owner += (int64_t)j >= p.part_bound[r];
+    dn = p.peer_pend[nxt][owner] + (((int64_t)j - p.part_bound[owner]) >> 1);
+    remote = (int64_t)j < p.node_base || (int64_t)j >= p.node_base + p.n;
   } else {
     dn = p.pend[nxt] + (j >> 1);
   }
   if (up) atomicAdd(dn, one);
   else atomicSub(dn, one);
+  return remote;
 }
 
 template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false>
@@ -766,6 +773,7 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
       e1 = __ldg(p.out_ro + n + 1);
     }
     const bool wide = HUBS && p.hubs && push && (e1 - e0 > 32);
+    int remote = 0;  // pushes this lane sent to other ranks (partitioned runs)
     // column loads are batched ahead of their atomics: a load-then-push loop
     // would wait one memory round trip per edge (each push needs its column)
     constexpr int kPB = 8;
@@ -776,7 +784,7 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
         for (int j = 0; j < kPB; ++j) cj[j] = (b + j < e1) ? __ldg(p.out_col + b + j) : -1;
 #pragma unroll
         for (int j = 0; j < kPB; ++j)
-          if (cj[j] >= 0) push_delta(p, nxt, cj[j], push > 0);
+          if (cj[j] >= 0) remote += push_delta(p, nxt, cj[j], push > 0);
       }
     }
     unsigned wides = HUBS ? __ballot_sync(kFull, wide) : 0u;
@@ -792,8 +800,12 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
         for (int j = 0; j < kHB; ++j) cj[j] = (b + 32 * j < a1) ? __ldg(p.out_col + b + 32 * j) : -1;
 #pragma unroll
         for (int j = 0; j < kHB; ++j)
-          if (cj[j] >= 0) push_delta(p, nxt, cj[j], up);
+          if (cj[j] >= 0) remote += push_delta(p, nxt, cj[j], up);
       }
+    }
+    if (p.remote_log) {
+      const int tot = __reduce_add_sync(kFull, remote);
+      if (lane == 0 && tot) atomicAdd(p.remote_log + k.step % p.log_cap, (unsigned)tot);
     }
     // partitioned: the pushes into peer GPUs' memory are ordered before
     // anything this thread's rank does next — in particular before the NCCL

@@ -64,6 +64,12 @@ class PartitionPlan:
     world: int
     chunk: int          # nodes per rank (multiple of ALIGN); the last rank may own fewer
     ranges: tuple       # ((lo, hi), ...) per rank
+    balanced: bool = False  # ranges cut at edge quantiles (unequal node counts)
+
+    @property
+    def bounds(self) -> np.ndarray:
+        """world + 1 node boundaries of the ranges."""
+        return np.array([lo for lo, _ in self.ranges] + [self.ranges[-1][1]], dtype=np.int64)
 
     @property
     def mask_segment_words(self) -> int:
@@ -77,14 +83,34 @@ class PartitionPlan:
         return (w + 3) // 4 * 4
 
 
-def partition_plan(num_nodes: int, world: int, align: int = ALIGN) -> PartitionPlan:
-    """Equal node ranges (the regular graphs of C4/C5 are edge-balanced by
-    node count), each a multiple of `align` nodes so no mask word straddles
-    two ranks."""
+def partition_plan(num_nodes: int, world: int, align: int = ALIGN, row_offsets=None) -> PartitionPlan:
+    """Contiguous node ranges, each a multiple of `align` nodes so no mask
+    word straddles two ranks.  Equal node counts by default (the regular
+    graphs of C4/C5 are edge-balanced by node count); with `row_offsets`
+    (the incoming CSR's, global) the boundaries are cut at the edge
+    quantiles instead, so the hubs of a scale-free graph do not
+    load one rank — the partitioned engine then needs incremental counts."""
     if world < 1 or num_nodes < world:
         raise ValueError("need 1 <= world <= num_nodes")
     if align % 32:
         raise ValueError("align must be a multiple of 32")
+    if row_offsets is not None and world > 1:
+        ro = np.asarray(row_offsets, dtype=np.int64)
+        if ro.size != num_nodes + 1:
+            raise ValueError("row_offsets must have N + 1 entries")
+        e = int(ro[-1])
+        cuts = [0]
+        for r in range(1, world):
+            b = int(np.searchsorted(ro, (r * e) // world, side="left"))
+            b = max(cuts[-1] + align, (b + align // 2) // align * align)
+            cuts.append(min(b, num_nodes))
+        cuts.append(num_nodes)
+        ranges = tuple((cuts[r], cuts[r + 1]) for r in range(world))
+        if any(hi <= lo for lo, hi in ranges):
+            raise ValueError(f"N={num_nodes} too small for {world} edge-balanced ranks of {align}-node granularity")
+        chunk = max(hi - lo for lo, hi in ranges)
+        chunk = -(-chunk // align) * align
+        return PartitionPlan(num_nodes, world, chunk, ranges, balanced=True)
     chunk = -(-num_nodes // world)
     chunk = -(-chunk // align) * align
     ranges = []
@@ -161,9 +187,11 @@ class _Partition:
         b.imask[0], b.imask[1] = _lib.ptr(masks[0]), _lib.ptr(masks[1])
         b.padded = 1
         self._b = b
+        self._bounds = plan.bounds if plan.balanced else None  # kept alive for the create call
         part = _lib.FsPartition(node_base=lo, num_nodes_global=plan.num_nodes,
                                 mask_segment_words=plan.mask_segment_words, rank=rank, world=plan.world,
-                                comm=comm)
+                                comm=comm,
+                                range_bounds=self._bounds.ctypes.data if self._bounds is not None else None)
         h = ctypes.c_void_p()
         incr = {"auto": -1, "incremental": 1}.get(cfg.gather, 0) if self.dg.symmetric else 0
         _lib.check(self.lib.fs_engine_create_partitioned(self.dg.view(), model_descriptor(m),
@@ -199,6 +227,12 @@ class _Partition:
         s = _lib.FsScalars()
         _lib.check(self.lib.fs_engine_get_scalars(self.handle, ctypes.byref(s), self.stream))
         return s
+
+    def remote_pushes(self, first: int, n: int) -> np.ndarray:
+        """Per-step count of the pushes this rank sent to other ranks."""
+        out = np.zeros(n, dtype=np.uint32)
+        _lib.check(self.lib.fs_engine_read_remote_pushes(self.handle, first, n, out.ctypes.data, self.stream))
+        return out
 
     def read_log(self, first: int, n: int):
         clocks = np.empty(n, dtype=np.float64)
@@ -328,6 +362,18 @@ class DistributedRun:
                 table[par][r] = out.value
         self.part.link_peers(table)
         dist.barrier(group=pg)  # every rank linked before anyone pushes
+
+    def exchange_us(self, iters: int = 200) -> float | None:
+        """Mean device time of one per-step NCCL exchange on this rank's
+        stream (the count / max all-reduce group, plus the mask all-gather
+        when the engine exchanges the mask)."""
+        if not self.comm.value:
+            return None
+        us = ctypes.c_float()
+        seg = 0 if self.part.incremental else self.plan.mask_segment_words
+        _lib.check(_lib.load().fs_comm_time_exchange(self.comm, self.rank, seg, iters, self.part.stream,
+                                                     ctypes.byref(us)))
+        return float(us.value)
 
     def run_batch(self):
         first = self.steps

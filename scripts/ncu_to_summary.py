@@ -1,11 +1,14 @@
 """Fold `ncu --set full` captures of bench.py workloads into
 profiles/ncu_summary.json (the file bench.py's roofline block reads).
 
-    python scripts/ncu_to_summary.py TAG W1 [W2 ...]
+    python scripts/ncu_to_summary.py TAG W1 [W2 ...]           (here, from reports)
+    OUT=gpurun_out python scripts/ncu_to_summary.py TAG W1 ...  (on the GPU box)
 
-reads gpurun_out/prof_TAG_W.ncu-rep (scripts/gpu_prof.sh) and
+reads gpurun_out/prof_TAG_W.ncu-rep (scripts/gpu_evidence_r2.sh) and
 gpurun_out/lib_sha16_TAG.txt (the sha of the library the capture ran) and
-writes, per workload: kernel, DRAM bytes per launch, ncu duration.
+writes, per workload: kernel, DRAM bytes per launch, ncu duration, into
+$OUT/ncu_summary.json (default profiles/) and the text summary into
+$OUT/TAG_W_ncu_full.txt.
 """
 
 from __future__ import annotations
@@ -39,7 +42,10 @@ def metrics(rep: Path) -> dict:
 
 def main() -> None:
     tag, works = sys.argv[1], sys.argv[2:]
-    out_p = ROOT / "profiles" / "ncu_summary.json"
+    import os
+
+    out_dir = ROOT / os.environ.get("OUT", "profiles")
+    out_p = out_dir / "ncu_summary.json"
     summary = json.loads(out_p.read_text()) if out_p.exists() else {}
     sha_p = ROOT / "gpurun_out" / f"lib_sha16_{tag}.txt"
     sha = sha_p.read_text().strip() if sha_p.exists() else None
@@ -54,7 +60,7 @@ def main() -> None:
         summary[w] = m
         txt = subprocess.run([sys.executable, str(ROOT / "scripts" / "ncu_summary.py"), str(rep)],
                              capture_output=True, text=True).stdout
-        (ROOT / "profiles" / f"{tag}_{w}_ncu_full.txt").write_text(txt)
+        (out_dir / f"{tag}_{w}_ncu_full.txt").write_text(txt)
         print(w, m)
     out_p.write_text(json.dumps(summary, indent=1))
 
