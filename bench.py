@@ -317,8 +317,9 @@ def cpu_ensemble_trials(g, m, e: dict, runs: int) -> dict:
 
 
 def run_ensemble_bench(args, w) -> None:
-    """run_ensemble on the GPU (trials concurrent on CUDA streams, one graph
-    upload, pipelined batches, device records): node-updates of every trial
+    """run_ensemble on the GPU (trials in lockstep, one launch per step for
+    all of them, one graph upload, pipelined batches, device records):
+    node-updates of every trial
     (whole batches, as run) over the call's wall time, max of `steps` calls
     after `warmup` untimed calls; host graph already built."""
     import torch
@@ -330,10 +331,11 @@ def run_ensemble_bench(args, w) -> None:
     cfg = fs.RenewalConfig()
     runs = e["runs"]
 
-    def once():
+    def once(lockstep=True):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        recs = fs.run_ensemble("renewal", g, m, cfg, e["seed"], e["t_final"], runs, seed_count=e["seed_count"])
+        recs = fs.run_ensemble("renewal", g, m, cfg, e["seed"], e["t_final"], runs, seed_count=e["seed_count"],
+                               lockstep=lockstep)
         torch.cuda.synchronize()
         return time.perf_counter() - t0, recs
 
@@ -348,14 +350,25 @@ def run_ensemble_bench(args, w) -> None:
     b = cfg.steps_per_batch
     steps = sum(int(np.ceil(r.summary["step_count"] / b) * b) for r in recs)
     value = g.num_nodes * steps / wall / 1e9
+    # lockstep: one launch per step for all trials, until the slowest trial ends
+    lock_steps = max(int(np.ceil(r.summary["step_count"] / b) * b) for r in recs) + b  # + the batch queued ahead
+    launches = lock_steps + 2 * (lock_steps // b)
+    # the per-trial-stream runner (one engine and one launch per trial per step) on the same call, for comparison
+    once(False)
+    s_walls = [once(False)[0] for _ in range(max(1, args.steps // 40))]
+    s_wall = statistics.median(s_walls)
     out = {
         "metric": "Giga-NUPS (node updates/s)", "value": value, "unit": "G-NUPS", "n_gpus": 1,
         "steps": len(walls), "warmup": args.warmup, "ms_per_step": wall * 1e3 / (steps / runs),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(w), "data": data_of(w),
         "config": workload_config(w, w["n"]), "edges": g.num_edges,
-        "engine": {"runner": "run_ensemble: trials on CUDA streams, pipelined batches, records by one device launch",
-                   "trials": runs, "trajectories_per_s": runs / wall, "wall_s": walls, "lib_sha16": lib_sha16()},
-        "roofline": None, "gpu_launches": steps + 3 * runs, "clocks": clk.summary(),
+        "engine": {"runner": "run_ensemble lockstep: every trial stepped by one grid per step (fs_ensemble, "
+                             "k_step_incr_multi), CUDA-graph batches, one 2-D log copy per batch, records by one "
+                             "device launch",
+                   "trials": runs, "trajectories_per_s": runs / wall, "wall_s": walls, "lib_sha16": lib_sha16(),
+                   "streams_runner": {"what": "run_ensemble(lockstep=False): one engine per trial on 32 CUDA streams",
+                                      "value": g.num_nodes * steps / s_wall / 1e9, "wall_s": s_walls}},
+        "roofline": None, "gpu_launches": launches, "clocks": clk.summary(),
         "e2e": {"value": value, "unit": "G-NUPS", "h2d_bytes_per_step": (g.row_offsets.nbytes + g.col_indices.nbytes)
                 / (steps / runs), "d2h_bytes_per_step": 8 * (2 + m.num_compartments) * runs,
                 "what": "the whole run_ensemble call from a host graph (graph upload, 100 trials, records)"},

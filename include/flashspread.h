@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 3
+#define FS_ABI_VERSION 4
 #define FS_MAX_COMPARTMENTS 16
 
 /* error codes */
@@ -258,6 +258,25 @@ int fs_engine_state_restored(fs_engine* e, void* stream);
  * run_renewal loop (R/renewal.py:632-663 reads the recorder after each
  * batch).  Every replayed batch ends by folding its last step's counts. */
 int fs_engine_wait_log(fs_engine* e, int64_t first_step, int32_t n, double* clocks, double* taus, int64_t* counts);
+
+/* ---- ensembles (R/analysis.py:97-130 run_ensemble, DESIGN.md §8 row 2) --- */
+/* Independent trials of one graph and model stepped in lockstep by ONE grid
+ * per step: every member is an ordinary engine (its own buffers, scalars and
+ * seed) built with the incremental streaming step, all at the same step; a
+ * member is bit-identical to its engine run alone.  Members must not be
+ * stepped or edited while they belong to the ensemble (run_batch refuses);
+ * destroy the ensemble before the engines. */
+typedef struct fs_ensemble fs_ensemble;
+int fs_ensemble_create(fs_engine* const* engines, int32_t count, fs_ensemble** out);
+void fs_ensemble_destroy(fs_ensemble* x);
+/* CTAs of one step launch (return value) and per member */
+int fs_ensemble_grid(const fs_ensemble* x, int32_t* ctas_per_member);
+/* one CUDA-graph batch of steps_per_batch lockstep steps of every member,
+ * ending with every member's count fold (fs_engine_run_batch for R trials) */
+int fs_ensemble_run_batch(fs_ensemble* x, void* stream);
+/* per-member log of the batch ending at first_step + n: clocks[R][n],
+ * taus[R][n], counts[R][n][M] (any may be NULL); waits for that batch only */
+int fs_ensemble_wait_log(fs_ensemble* x, int64_t first_step, int32_t n, double* clocks, double* taus, int64_t* counts);
 /* Partitioned runs: per-step count of the +-1 pushes this rank sent to other
  * ranks' pending deltas (over NVLink on a multi-GPU box), for steps
  * [first_step, first_step + n) still in the log ring. */

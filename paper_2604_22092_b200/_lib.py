@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import FlashSpreadNativeError, InvalidConfigError, ReconfigureAfterStartError
 
 MAX_COMPARTMENTS = 16
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # enum fs_dtype
 I8, I32, I64, F16, BF16, F32, F64, U32, U64 = 1, 2, 3, 4, 5, 6, 7, 8, 9
@@ -201,6 +201,11 @@ _SIGNATURES = {
     "fs_host_csr_scan": (_c_i32, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
                                   ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_float)]),
     "fs_engine_uniform_s_age": (_c_i32, [_vp]),
+    "fs_ensemble_create": (_c_i32, [_vp, _c_i32, ctypes.POINTER(_vp)]),
+    "fs_ensemble_destroy": (None, [_vp]),
+    "fs_ensemble_grid": (_c_i32, [_vp, ctypes.POINTER(_c_i32)]),
+    "fs_ensemble_run_batch": (_c_i32, [_vp, _vp]),
+    "fs_ensemble_wait_log": (_c_i32, [_vp, _c_i64, _c_i32, _vp, _vp, _vp]),
     "fs_engine_current_buffer": (_c_i32, [_vp, _vp]),
     "fs_engine_begin_batch": (_c_i32, [_vp, _vp]),
     "fs_engine_step": (_c_i32, [_vp, _c_i32, _c_i32, _c_i32, _vp]),

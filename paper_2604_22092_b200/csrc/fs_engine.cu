@@ -144,9 +144,8 @@ __global__ void k_ptab(float* ptab, int64_t len, float c, int* exact_mul) {
 
 // batch prologue (renewal.py:583-597): fold a pending step into the
 // scalars, then reset tau unless carry_tau
-__global__ void k_begin_batch(DevState* D, StepAcc* acc, int64_t* log_counts, int64_t log_cap,
-                              int M, double eps, double tau_max, double delta, int carry_tau) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ __forceinline__ void begin_batch_one(DevState* D, StepAcc* acc, int64_t* log_counts, int64_t log_cap,
+                                                int M, double eps, double tau_max, double delta, int carry_tau) {
   if (D->pending) {
     const int64_t last = D->s.step - 1;
     const StepAcc* A = acc + last % 3;
@@ -165,6 +164,25 @@ __global__ void k_begin_batch(DevState* D, StepAcc* acc, int64_t* log_counts, in
     acc[j].max_bits = 0u;
     for (int c = 0; c < FS_MAX_COMPARTMENTS; ++c) acc[j].d[c] = 0ull;
   }
+}
+
+__global__ void k_begin_batch(DevState* D, StepAcc* acc, int64_t* log_counts, int64_t log_cap,
+                              int M, double eps, double tau_max, double delta, int carry_tau) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  begin_batch_one(D, acc, log_counts, log_cap, M, eps, tau_max, delta, carry_tau);
+}
+
+// the same for every member of an ensemble (thread m: member m)
+struct MemberBatch {
+  DevState* D[2];      // the member's two scalar slots
+  StepAcc* acc;        // its accumulator ring
+  int64_t* log_counts; // its row of the ensemble's count log
+};
+__global__ void k_begin_batch_multi(const MemberBatch* __restrict__ mb, int count, int slot, int64_t log_cap, int M,
+                                    double eps, double tau_max, double delta, int carry_tau) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= count) return;
+  begin_batch_one(mb[m].D[slot], mb[m].acc, mb[m].log_counts, log_cap, M, eps, tau_max, delta, carry_tau);
 }
 
 // compaction refresh at tile granularity: a 32-node tile is active if any of
@@ -1568,3 +1586,256 @@ extern "C" int fs_engine_debug_times(fs_engine* e, unsigned long long* out, int3
   FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * (4 + 32) * 16 * n));
   return n;
 }
+
+// ---------------------------------------------------------------------------
+// Ensembles (R/analysis.py:97-130 `run_ensemble`): independent trials of one
+// graph and model, stepped in lockstep by ONE grid per step.  Each member is
+// an ordinary engine (its own states, ages, counts, scalars, seed); the
+// ensemble launches k_step_incr_multi over a device array of the members'
+// StepParams, so a step of R trials costs one launch instead of R, and a
+// batch is one CUDA graph of steps_per_batch such launches between two
+// batched count folds.  The members' per-step logs go to one [R][cap] ring
+// owned by the ensemble, read back with three 2-D copies per batch.
+// ---------------------------------------------------------------------------
+struct fs_ensemble {
+  int device = 0;
+  int count = 0;
+  std::vector<fs_engine*> members;
+  MultiFn fn = nullptr;
+  StepFn member_fn = nullptr;     // the members' k_step_incr variant at creation
+  uint32_t ctas_per = 1;
+  int grid = 1;
+  bool pdl = true;
+  int M = 0, steps_per_batch = 0;
+  double eps = 0, tau_max = 0, delta = 0;
+  int carry_tau = 1;
+  StepParams* dparams = nullptr;  // [2 scalar slot][2 step parity][count]
+  MemberBatch* dbatch = nullptr;  // [count]
+  double* log_clock = nullptr;    // [count][cap]
+  double* log_tau = nullptr;      // [count][cap]
+  int64_t* log_counts = nullptr;  // [count][cap][kCntStride]
+  int64_t log_cap = 0;
+  int s_cur = 0;
+  int64_t h_step = 0;
+  cudaStream_t cap_stream = nullptr, copy_stream = nullptr;
+  cudaGraphExec_t exec[2][2] = {};  // [scalar slot][step parity] at the batch start
+  static constexpr int kBatchEv = 8;
+  cudaEvent_t ev[kBatchEv] = {};
+  int64_t ev_end[kBatchEv] = {};
+  int ev_next = 0;
+};
+
+extern "C" {
+
+void fs_ensemble_destroy(fs_ensemble* x) {
+  if (!x) return;
+  cudaSetDevice(x->device);
+  for (auto& a : x->exec)
+    for (auto& g : a) if (g) cudaGraphExecDestroy(g);
+  if (x->cap_stream) cudaStreamDestroy(x->cap_stream);
+  if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
+  for (auto& ev : x->ev) if (ev) cudaEventDestroy(ev);
+  cudaDeviceSynchronize();
+  for (void* q : {(void*)x->dparams, (void*)x->dbatch, (void*)x->log_clock, (void*)x->log_tau, (void*)x->log_counts})
+    if (q) cudaFreeAsync(q, (cudaStream_t)0);
+  cudaStreamSynchronize((cudaStream_t)0);
+  delete x;
+}
+
+int fs_ensemble_create(fs_engine* const* engines, int32_t count, fs_ensemble** out) {
+  if (!out) return set_error(FS_EINVAL, "null output");
+  *out = nullptr;
+  if (!engines || count < 1) return set_error(FS_EINVAL, "an ensemble needs at least one engine");
+  const fs_engine* e0 = engines[0];
+  for (int i = 0; i < count; ++i) {
+    const fs_engine* e = engines[i];
+    if (!e) return set_error(FS_EINVAL, "null engine %d", i);
+    if (!e->stream || e->c.compaction || e->world > 1 || e->comm || e->dbg)
+      return set_error(FS_EINVAL, "ensemble member %d: needs the incremental streaming step (single partition, no compaction)", i);
+    if (e->device != e0->device || e->g.num_nodes != e0->g.num_nodes || e->g.out_row_offsets != e0->g.out_row_offsets ||
+        e->stream_fn[0] != e0->stream_fn[0] || e->c.steps_per_batch != e0->c.steps_per_batch ||
+        e->m.num_compartments != e0->m.num_compartments || e->c.epsilon != e0->c.epsilon ||
+        e->c.tau_max != e0->c.tau_max || e->c.delta != e0->c.delta || e->c.carry_tau != e0->c.carry_tau ||
+        e->pdl != e0->pdl)
+      return set_error(FS_EINVAL, "ensemble member %d: every member needs the same device, graph, model shape, config and step kernel", i);
+    if (e->s_cur != e0->s_cur || e->h_step != e0->h_step)
+      return set_error(FS_EINVAL, "ensemble member %d: members must be at the same step", i);
+  }
+  FS_CUDA(cudaSetDevice(e0->device));
+  fs_ensemble* x = new fs_ensemble();
+  int rc = 0;
+#define TRY(v) do { rc = (v); if (rc) { fs_ensemble_destroy(x); return rc; } } while (0)
+  x->device = e0->device;
+  x->count = count;
+  x->members.assign(engines, engines + count);
+  x->member_fn = e0->stream_fn[0];
+  x->fn = pick_stream_multi(e0->mixed, false, e0->stream_memo, e0->stream_hubs, e0->s_uniform);
+  if (!x->fn) { delete x; return set_error(FS_EINVAL, "no ensemble step kernel for this engine variant"); }
+  x->pdl = e0->pdl;
+  x->M = e0->m.num_compartments;
+  x->steps_per_batch = e0->c.steps_per_batch;
+  x->eps = e0->c.epsilon;
+  x->tau_max = e0->c.tau_max;
+  x->delta = e0->c.delta;
+  x->carry_tau = e0->c.carry_tau;
+  x->s_cur = e0->s_cur;
+  x->h_step = e0->h_step;
+  // CTAs per member: enough warps for its tiles, the grid about one wave
+  {
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)x->fn, 512, 0) != cudaSuccess || occ < 1) occ = 1;
+    const int64_t need = (e0->ntiles + 15) / 16;
+    const int64_t wave = ((int64_t)e0->sms * occ + count - 1) / count;
+    x->ctas_per = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(need, wave));
+    const int64_t grid = (int64_t)x->ctas_per * count;
+    if (grid > INT32_MAX) { delete x; return set_error(FS_EINVAL, "ensemble grid too large"); }
+    x->grid = (int)grid;
+  }
+  x->log_cap = e0->log_cap;
+  TRY(dalloc(&x->log_clock, (size_t)count * x->log_cap));
+  TRY(dalloc(&x->log_tau, (size_t)count * x->log_cap));
+  TRY(dalloc(&x->log_counts, (size_t)count * x->log_cap * kCntStride));
+  TRY(dalloc(&x->dparams, (size_t)4 * count));
+  TRY(dalloc(&x->dbatch, (size_t)count));
+  {
+    std::vector<StepParams> hp((size_t)4 * count);
+    std::vector<MemberBatch> hb((size_t)count);
+    for (int i = 0; i < count; ++i) {
+      fs_engine* e = engines[i];
+      for (int s = 0; s < 2; ++s)
+        for (int par = 0; par < 2; ++par) {
+          StepParams p = make_step_params(e, false, false, s);
+          p.host_parity = par;
+          p.log_clock = x->log_clock + (size_t)i * x->log_cap;
+          p.log_tau = x->log_tau + (size_t)i * x->log_cap;
+          p.log_counts = x->log_counts + (size_t)i * x->log_cap * kCntStride;
+          p.log_cap = x->log_cap;
+          p.dbg = nullptr;
+          hp[((size_t)s * 2 + par) * count + i] = p;
+        }
+      hb[i].D[0] = e->dstate;
+      hb[i].D[1] = e->dstate + 1;
+      hb[i].acc = e->acc;
+      hb[i].log_counts = x->log_counts + (size_t)i * x->log_cap * kCntStride;
+    }
+    FS_CUDA(cudaMemcpy(x->dparams, hp.data(), hp.size() * sizeof(StepParams), cudaMemcpyHostToDevice));
+    FS_CUDA(cudaMemcpy(x->dbatch, hb.data(), hb.size() * sizeof(MemberBatch), cudaMemcpyHostToDevice));
+  }
+  FS_CUDA(cudaStreamCreateWithFlags(&x->cap_stream, cudaStreamNonBlocking));
+  FS_CUDA(cudaStreamCreateWithFlags(&x->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < fs_ensemble::kBatchEv; ++i) {
+    FS_CUDA(cudaEventCreateWithFlags(&x->ev[i], cudaEventDisableTiming));
+    x->ev_end[i] = -1;
+  }
+  FS_CUDA(cudaDeviceSynchronize());
+#undef TRY
+  *out = x;
+  return 0;
+}
+
+int fs_ensemble_grid(const fs_ensemble* x, int32_t* ctas_per_member) {
+  if (!x) return set_error(FS_EINVAL, "null ensemble");
+  if (ctas_per_member) *ctas_per_member = (int32_t)x->ctas_per;
+  return x->grid;
+}
+
+static int ensemble_launch_batch(fs_ensemble* x, cudaStream_t st) {
+  const int tb = 128, mb = (x->count + tb - 1) / tb;
+  k_begin_batch_multi<<<mb, tb, 0, st>>>(x->dbatch, x->count, x->s_cur, x->log_cap, x->M, x->eps, x->tau_max, x->delta,
+                                         x->carry_tau);
+  int s = x->s_cur;
+  int64_t h = x->h_step;
+  for (int k = 0; k < x->steps_per_batch; ++k) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(x->grid);
+    cfg.blockDim = dim3(512);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = x->pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const StepParams* P = x->dparams + ((size_t)s * 2 + (size_t)(h & 1)) * x->count;
+    FS_CUDA(cudaLaunchKernelEx(&cfg, x->fn, P, x->ctas_per));
+    s ^= 1;
+    ++h;
+  }
+  // the batch's last step folded into the scalars and the log (as the
+  // single-engine batch graph ends)
+  k_begin_batch_multi<<<mb, tb, 0, st>>>(x->dbatch, x->count, s, x->log_cap, x->M, x->eps, x->tau_max, x->delta, 1);
+  FS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int fs_ensemble_run_batch(fs_ensemble* x, void* stream) {
+  if (!x) return set_error(FS_EINVAL, "null ensemble");
+  for (fs_engine* e : x->members)
+    if (e->s_cur != x->s_cur || e->h_step != x->h_step || e->stream_fn[0] != x->member_fn)
+      return set_error(FS_ESTATE, "an ensemble member was stepped or edited outside the ensemble");
+  FS_CUDA(cudaSetDevice(x->device));
+  cudaGraphExec_t& exec = x->exec[x->s_cur][x->h_step & 1];
+  if (!exec) {
+    cudaGraph_t graph = nullptr;
+    FS_CUDA(cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = ensemble_launch_batch(x, x->cap_stream);
+    cudaError_t err = cudaStreamEndCapture(x->cap_stream, &graph);
+    if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+    if (err != cudaSuccess) return set_error(FS_ECUDA, "ensemble graph capture: %s", cudaGetErrorString(err));
+    err = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (err != cudaSuccess) return set_error(FS_ECUDA, "ensemble graph instantiate: %s", cudaGetErrorString(err));
+  }
+  FS_CUDA(cudaGraphLaunch(exec, (cudaStream_t)stream));
+  x->s_cur ^= (x->steps_per_batch & 1);
+  x->h_step += x->steps_per_batch;
+  for (fs_engine* e : x->members) {  // the members' host mirrors follow their device state
+    e->s_cur = x->s_cur;
+    e->h_step = x->h_step;
+  }
+  const int slot = x->ev_next;
+  x->ev_next = (slot + 1) % fs_ensemble::kBatchEv;
+  FS_CUDA(cudaEventRecord(x->ev[slot], (cudaStream_t)stream));
+  x->ev_end[slot] = x->h_step;
+  return 0;
+}
+
+int fs_ensemble_wait_log(fs_ensemble* x, int64_t first_step, int32_t n, double* clocks, double* taus, int64_t* counts) {
+  if (!x || n < 0) return set_error(FS_EINVAL, "bad ensemble log request");
+  if (n > x->log_cap) return set_error(FS_EINVAL, "log request of %d steps exceeds capacity %lld", n, (long long)x->log_cap);
+  FS_CUDA(cudaSetDevice(x->device));
+  const int64_t end = first_step + n;
+  int slot = -1;
+  for (int i = 0; i < fs_ensemble::kBatchEv; ++i)
+    if (x->ev_end[i] == end) slot = i;
+  if (slot < 0) return set_error(FS_EINVAL, "no ensemble batch ends at step %lld", (long long)end);
+  if (x->h_step - first_step > x->log_cap)
+    return set_error(FS_EINVAL, "steps %lld.. were overwritten in the log ring", (long long)first_step);
+  FS_CUDA(cudaEventSynchronize(x->ev[slot]));
+  const int R = x->count, M = x->M;
+  cudaStream_t cs = x->copy_stream;
+  // [R][n] clocks / taus and [R][n][kCntStride] counts, ring pieces as 2-D copies
+  std::vector<int64_t> lk((size_t)R * n * kCntStride);
+  for (int64_t done = 0; done < n;) {
+    const int64_t s0 = (first_step + done) % x->log_cap;
+    const int64_t len = std::min<int64_t>(n - done, x->log_cap - s0);
+    if (clocks)
+      FS_CUDA(cudaMemcpy2DAsync(clocks + done, (size_t)n * sizeof(double), x->log_clock + s0, (size_t)x->log_cap * sizeof(double),
+                                (size_t)len * sizeof(double), (size_t)R, cudaMemcpyDeviceToHost, cs));
+    if (taus)
+      FS_CUDA(cudaMemcpy2DAsync(taus + done, (size_t)n * sizeof(double), x->log_tau + s0, (size_t)x->log_cap * sizeof(double),
+                                (size_t)len * sizeof(double), (size_t)R, cudaMemcpyDeviceToHost, cs));
+    FS_CUDA(cudaMemcpy2DAsync(lk.data() + done * kCntStride, (size_t)n * kCntStride * sizeof(int64_t),
+                              x->log_counts + s0 * kCntStride, (size_t)x->log_cap * kCntStride * sizeof(int64_t),
+                              (size_t)len * kCntStride * sizeof(int64_t), (size_t)R, cudaMemcpyDeviceToHost, cs));
+    done += len;
+  }
+  FS_CUDA(cudaStreamSynchronize(cs));
+  if (counts)
+    for (size_t r = 0; r < (size_t)R; ++r)
+      for (int i = 0; i < n; ++i)
+        for (int c2 = 0; c2 < M; ++c2)
+          counts[(r * n + i) * M + c2] = lk[(r * n + i) * kCntStride + c2];
+  return 0;
+}
+
+}  // extern "C"

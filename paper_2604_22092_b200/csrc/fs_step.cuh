@@ -1047,8 +1047,10 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
 #ifndef FS_PF_DEPTH
 #define FS_PF_DEPTH 2
 #endif
+// `cta` / `nctas`: this CTA and the CTAs sharing the engine `p` (the whole
+// grid, or one member's CTAs of an ensemble launch)
 template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, int BLOCK>
-__global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
+__device__ __forceinline__ void step_incr_body(const StepParams& p, const uint32_t cta, const uint32_t nctas) {
   constexpr int WARPS = BLOCK / 32;
   __shared__ StepShared<WARPS> sh;
   __shared__ StepConst s_k;
@@ -1066,7 +1068,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   pdl_wait();
   if (tid == 0) {
     s_k = step_const(p, true);
-    if (blockIdx.x == 0) {
+    if (cta == 0) {
       commit_step_start(p, s_k);
       if (UNI) commit_s_age<AT>(p, s_k);
     }
@@ -1075,7 +1077,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   const AT* __restrict__ ages = reinterpret_cast<const AT*>(p.ages);
   uint16_t* __restrict__ cnt = p.cnt;
   const uint32_t N = (uint32_t)p.n, ntiles = (uint32_t)p.ntiles;
-  const uint32_t stride = gridDim.x * WARPS;
+  const uint32_t stride = nctas * WARPS;
   struct In { int s; float age; uint32_t c, d; };
   // arrays are padded to whole 128-node units: every lane loads unconditionally
   auto load = [&](uint32_t t, const uint16_t* pend, In& in) {
@@ -1087,7 +1089,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   };
   // the first two tiles' loads need only the buffer parity, which the host
   // knows: they overlap thread 0's scalar reads instead of waiting for them
-  uint32_t t = blockIdx.x * WARPS + warp;
+  uint32_t t = cta * WARPS + warp;
   constexpr int PD = FS_PF_DEPTH;  // tiles in flight per warp (register ring, compile-time indices)
   In inq[PD];
 #pragma unroll
@@ -1106,7 +1108,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
     unsigned sm;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    unsigned long long* dbg = p.dbg + ((size_t)(k.step & 15) * gridDim.x + blockIdx.x) * 4;
+    unsigned long long* dbg = p.dbg + ((size_t)(k.step & 15) * nctas + cta) * 4;
     dbg[0] = ((unsigned long long)sm << 48) | (s_entry & 0xFFFFFFFFFFFFull);
     dbg[2] = now;
   }
@@ -1165,7 +1167,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   {
     // the final drain also prepares one (slot, cohort) pair of step k+1's
     // cohort table in its idle lane 31 (qn < 32 here)
-    const int gw = (int)blockIdx.x * WARPS + warp;
+    const int gw = (int)cta * WARPS + warp;
     const int prep = (MEMO && gw < kCohortW * p.ncslots) ? gw : -1;
     if (qn > 0 || prep >= 0)
       drain_entries<ST, AT, float, MAT, WARPS, HUBS, UNI>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
@@ -1175,8 +1177,8 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   if (p.dbg && lane == 0) {
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    unsigned long long* w = p.dbg + (size_t)16 * gridDim.x * 4 +
-                            (((size_t)(k.step & 15) * gridDim.x + blockIdx.x) * 32 + (size_t)warp * 2);
+    unsigned long long* w = p.dbg + (size_t)16 * nctas * 4 +
+                            (((size_t)(k.step & 15) * nctas + cta) * 32 + (size_t)warp * 2);
     w[0] = now;
     w[1] = ((unsigned long long)pr_def << 20) | (unsigned long long)(pr_drains + (qn > 0 ? 1 : 0));
   }
@@ -1185,7 +1187,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   if (p.dbg && lane == 0) {
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    atomicMax(p.dbg + ((size_t)(k.step & 15) * gridDim.x + blockIdx.x) * 4 + 1, now);
+    atomicMax(p.dbg + ((size_t)(k.step & 15) * nctas + cta) * 4 + 1, now);
   }
 #endif
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
@@ -1193,9 +1195,26 @@ __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   if (p.dbg && tid == 0) {
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    p.dbg[((size_t)(k.step & 15) * gridDim.x + blockIdx.x) * 4 + 3] = now;
+    p.dbg[((size_t)(k.step & 15) * nctas + cta) * 4 + 3] = now;
   }
 #endif
+}
+
+
+template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
+  step_incr_body<ST, AT, MAT, MEMO, HUBS, UNI, BLOCK>(p, blockIdx.x, gridDim.x);
+}
+
+// Ensemble launch (fs_ensemble, DESIGN.md §8 row 2): one step of every member
+// engine in one grid.  Member m owns CTAs [m * ctas_per, (m + 1) * ctas_per)
+// and runs exactly the single-engine step on its own parameters — its own
+// buffers, scalars, accumulators, log and RNG seed — so every member is
+// bit-identical to its engine stepped alone.
+template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, 2) k_step_incr_multi(const StepParams* __restrict__ P, const uint32_t ctas_per) {
+  const uint32_t m = blockIdx.x / ctas_per;
+  step_incr_body<ST, AT, MAT, MEMO, HUBS, UNI, BLOCK>(P[m], blockIdx.x - m * ctas_per, ctas_per);
 }
 
 // thread-per-node count over a slice staged in shared memory: lane-private
@@ -1442,10 +1461,12 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_gather_merge
 using StepFn = void (*)(const StepParams);
 using MergeFn = void (*)(const MergeParams);
 using TmaFn = void (*)(const StepParams, const TmaLayout);
+using MultiFn = void (*)(const StepParams*, uint32_t);
 
 // instantiation units
 StepFn pick_step(bool mixed, int gather, int strat, bool mat, int& block);  // fs_step_general.cu
 StepFn pick_stream(bool mixed, bool mat, bool memo, bool hubs, bool uni);           // fs_step_incr.cu
+MultiFn pick_stream_multi(bool mixed, bool mat, bool memo, bool hubs, bool uni);    // fs_step_incr.cu
 MergeFn pick_merge(bool inf_bf16, int mode, int& block);                    // fs_step_incr.cu
 TmaFn pick_tma(bool mixed, bool smem_mask, bool mat, bool ptab_mul, int block);  // fs_step_tma.cu
 

@@ -17,12 +17,13 @@ and to the reference's CPU ensemble (tests/test_ensemble.py).
 
 from __future__ import annotations
 
+import ctypes
 import time
 
 import numpy as np
 import torch
 
-from . import _device
+from . import _device, _lib
 from .renewal import RenewalConfig, _build_plan, as_config, _check_conservation, init_renewal_state
 from .rng import derive_seed
 from .analysis import make_records
@@ -66,17 +67,111 @@ class _Trial:
         return t_arr, np.asarray(self.rows), {"step_count": steps, "wall_clock": wall, "engine": "renewal"}
 
 
+class _Lockstep:
+    """A group of trials stepped by one grid per step (fs_ensemble): every
+    trial is an ordinary engine; the ensemble launches the step of all of them
+    at once and keeps their logs in one ring, read back once per batch."""
+
+    def __init__(self, trials: list[int], g, m, cfg, seed: int, seed_count, seed_compartment, plan):
+        self.lib = _lib.load()
+        self.trials = trials
+        self.seeds = [derive_seed(seed, t) for t in trials]
+        self.states = [init_renewal_state(g, m, cfg, s, seed_count, seed_compartment) for s in self.seeds]
+        self.engines = [st._bind(plan, s, materialize=False) for st, s in zip(self.states, self.seeds)]
+        arr = (ctypes.c_void_p * len(trials))(*[e.handle.value for e in self.engines])
+        h = ctypes.c_void_p()
+        rc = self.lib.fs_ensemble_create(arr, len(trials), ctypes.byref(h))
+        self.handle = h if rc == 0 else None
+        self.rc = rc
+        self.stream = _device.stream_handle(_device.device())
+        self.M = len(m.compartments)
+        self.times = [[0.0] for _ in trials]
+        self.rows = [[st.counts.copy()] for st in self.states]
+        self.end = [None] * len(trials)  # steps a single run would have taken (whole batches)
+        self.done = 0
+
+    def run_batch(self) -> None:
+        _lib.check(self.lib.fs_ensemble_run_batch(self.handle, self.stream))
+
+    def collect(self, b: int, n: int, t_final: float) -> bool:
+        R = len(self.trials)
+        clocks = np.empty((R, b), dtype=np.float64)
+        counts = np.empty((R, b, self.M), dtype=np.int64)
+        _lib.check(self.lib.fs_ensemble_wait_log(self.handle, self.done, b, clocks.ctypes.data, None,
+                                                 counts.ctypes.data))
+        self.done += b
+        for r in range(R):
+            if self.end[r] is not None:
+                continue  # past its own stopping batch: a single run would have stopped
+            _check_conservation(counts[r], n)
+            self.times[r].extend(clocks[r].tolist())
+            self.rows[r].extend(counts[r])
+            if clocks[r, -1] >= t_final:
+                self.end[r] = self.done
+        return all(e is not None for e in self.end)
+
+    def close(self) -> None:
+        if self.handle is not None:
+            torch.cuda.current_stream().synchronize()
+            self.lib.fs_ensemble_destroy(self.handle)
+            self.handle = None
+        for e in self.engines:  # the trial states are dropped with their engines
+            e.close()
+
+
+def _run_lockstep(g, m, cfg, seed, t_final, runs, seed_count, seed_compartment, plan, group: int):
+    """Trials in lockstep groups of `group`; None when the engines cannot form
+    an ensemble (e.g. a model or graph that needs the general gather)."""
+    b = cfg.steps_per_batch
+    out = []
+    t0 = time.perf_counter()
+    for lo in range(0, runs, group):
+        ls = _Lockstep(list(range(lo, min(runs, lo + group))), g, m, cfg, seed, seed_count, seed_compartment, plan)
+        try:
+            if ls.handle is None:
+                if lo == 0:
+                    return None
+                _lib.check(ls.rc)
+            ls.run_batch()
+            finished = False
+            while not finished:
+                ls.run_batch()  # one batch queued ahead of the one read
+                finished = ls.collect(b, g.num_nodes, t_final)
+        finally:
+            ls.close()
+        wall = time.perf_counter() - t0
+        for r in range(len(ls.trials)):
+            t_arr = np.asarray(ls.times[r])
+            steps = min(int(np.searchsorted(t_arr, t_final, side="left")), ls.end[r])
+            out.append((t_arr, np.asarray(ls.rows[r]), {"step_count": steps, "wall_clock": wall, "engine": "renewal"}))
+    return out
+
+
 def run_ensemble(engine: str, g, m, cfg, seed: int, t_final: float, runs: int,
                  grid_points: int = DEFAULT_GRID_POINTS, workers: int = 1, seed_count=None, seed_compartment=None,
-                 concurrency: int = 32) -> list[TrajectoryRecord]:
-    """R/analysis.py:97-130 for the renewal engine, trials concurrent on the
-    GPU (`workers` is accepted for signature compatibility; `concurrency`
-    bounds the trials in flight).  Records are ordered by trial index."""
+                 concurrency: int = 32, lockstep: bool = True) -> list[TrajectoryRecord]:
+    """R/analysis.py:97-130 for the renewal engine, every trial on the GPU
+    (`workers` is accepted for signature compatibility).  Records are ordered
+    by trial index.
+
+    lockstep (default): groups of trials advance together, one step launch
+    for the whole group (fs_ensemble), as many trials per group as fit
+    ~2^27 nodes; trials whose engines cannot share a launch run as below.
+    lockstep=False: one engine per trial on its own CUDA stream, `concurrency`
+    trials in flight."""
     if engine != "renewal":
         raise ValueError(f"the B200 ensemble runs the renewal engine only (got {engine!r})")
     cfg = as_config(cfg)
     _device.device()
     b = cfg.steps_per_batch
+    if lockstep and runs > 0:
+        plan = _build_plan(g, m, cfg, bool(cfg.mixed_precision))
+        torch.cuda.current_stream().synchronize()
+        group = max(1, min(runs, (1 << 27) // max(1, g.num_nodes)))
+        res = _run_lockstep(g, m, cfg, seed, t_final, runs, seed_count, seed_compartment, plan, group)
+        if res is not None:
+            return make_records([(t, c) for t, c, _ in res], m.compartments, g.num_nodes, t_final, grid_points,
+                                [s for _, _, s in res])
     free = [torch.cuda.Stream() for _ in range(max(1, min(concurrency, runs)))]
     plan = _build_plan(g, m, cfg, bool(cfg.mixed_precision))  # one device copy of the graph for every trial
     out: list[tuple | None] = [None] * runs

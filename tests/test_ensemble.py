@@ -117,3 +117,65 @@ def test_weibull_erlang_ensemble_agrees_with_exact_oracle(we_golden, gname):
         b = ref[f"{gname}__{stat}"]
         se = np.sqrt(a.var(ddof=1) / a.size + b.var(ddof=1) / b.size)
         assert abs(a.mean() - b.mean()) <= 3.0 * se, (gname, stat, a.mean(), b.mean(), se)
+
+
+# ---------------------------------------------------------------------------
+# lockstep runner (fs_ensemble: one step launch for every trial) against the
+# per-trial-stream runner — the same trials bit for bit
+# ---------------------------------------------------------------------------
+
+
+def _summ(recs):
+    return [(r.summary["peak_I"], r.summary["peak_I_time"], r.summary["final_R"], r.summary["step_count"])
+            for r in recs]
+
+
+@pytest.mark.parametrize("case", ["er_seir", "ba_weibull_erlang", "er_mixed", "ba_sir"])
+def test_lockstep_equals_stream_runner(case):
+    if case.startswith("er"):
+        g = fs.gen_erdos_renyi(1500, 6.0, seed=11)
+    else:
+        g = fs.gen_barabasi_albert(3000, 3, seed=5)  # hubs > 32 edges: warp-cooperative pushes
+    m = {"er_seir": fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0), "er_mixed": fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0),
+         "ba_weibull_erlang": fs.seir_weibull_erlang(0.25), "ba_sir": fs.sir_model(0.3, 0.1)}[case]
+    cfg = fs.RenewalConfig(mixed_precision=case == "er_mixed", steps_per_batch=32)
+    plan = fs.renewal._build_plan(g, m, cfg, cfg.mixed_precision)
+    res = fs.ensemble._run_lockstep(g, m, cfg, 99, 30.0, 13, 5, None, plan, group=6)  # 3 groups
+    assert res is not None, "the trials did not form a lockstep ensemble"
+    a = fs.run_ensemble("renewal", g, m, cfg, 99, 30.0, 13, seed_count=5, lockstep=True)
+    b = fs.run_ensemble("renewal", g, m, cfg, 99, 30.0, 13, seed_count=5, lockstep=False)
+    assert _summ(a) == _summ(b)
+    for x, y in zip(a, b):
+        assert np.array_equal(x.fractions, y.fractions)
+    for (t, c, s), y in zip(res, b):
+        assert s["step_count"] == y.summary["step_count"]
+
+
+def test_lockstep_trial_equals_run_renewal():
+    g = fs.gen_erdos_renyi(1000, 8.0, seed=3)
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    cfg = fs.RenewalConfig()
+    recs = fs.run_ensemble("renewal", g, m, cfg, 7, 40.0, 40, seed_count=10)
+    for t in (0, 17, 39):
+        rec = fs.run_renewal(g, m, cfg, fs.derive_seed(7, t), 40.0, seed_count=10)
+        assert np.array_equal(rec.fractions, recs[t].fractions)
+        assert rec.summary["step_count"] == recs[t].summary["step_count"]
+
+
+def test_ensemble_abi_rejects_mismatched_members():
+    from paper_2604_22092_b200 import _lib
+    import ctypes
+
+    g1 = fs.gen_erdos_renyi(1000, 8.0, seed=3)
+    g2 = fs.gen_erdos_renyi(1000, 8.0, seed=4)
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    cfg = fs.RenewalConfig()
+    engs = []
+    for g in (g1, g2):
+        st = fs.init_renewal_state(g, m, cfg, 1)
+        engs.append((st, st._bind(fs.renewal._build_plan(g, m, cfg, False), 1, materialize=False)))
+    lib = _lib.load()
+    arr = (ctypes.c_void_p * 2)(*[e.handle.value for _, e in engs])
+    h = ctypes.c_void_p()
+    assert lib.fs_ensemble_create(arr, 2, ctypes.byref(h)) == _lib.FS_EINVAL
+    assert b"same device, graph" in lib.fs_last_error()
