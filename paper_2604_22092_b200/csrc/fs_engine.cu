@@ -239,9 +239,18 @@ __global__ void k_load_mask(const IT* __restrict__ inf, int64_t n, float c, uint
        i += (int64_t)gridDim.x * blockDim.x) {
     float v = i < n ? to_f32<IT>(inf[i]) : 0.0f;
     const bool on = v != 0.0f;
-    if (on && v != c) atomicExch(bad, 1);
+    if (bad && on && v != c) atomicExch(bad, 1);  // bad == nullptr: any nonzero value (f32 mask)
     const unsigned w = __ballot_sync(kFull, on);
     if (lane == 0) { m0[i >> 5] = w; m1[i >> 5] = w; }
+  }
+}
+
+// 1 in *bad when some weight is not finite (the f32 mask prefilter skips
+// 0 * w, which is NaN for an infinite or NaN weight)
+__global__ void k_any_nonfinite(const void* w, int bf16, int64_t e, int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(w)[i]) : reinterpret_cast<const float*>(w)[i];
+    if (!isfinite(v)) atomicExch(bad, 1);
   }
 }
 
@@ -301,6 +310,11 @@ struct fs_engine {
   fs_state_buffers b{};
   bool count_mode = false;
   bool mask_smem = false;
+  bool fmask = false;     // f32 gather with the nonzero-infectivity mask prefilter (G_F32M_*)
+  int32_t* hub_list = nullptr;  // fused edge-merge: nodes with in-degree > kWide, heaviest first
+  int64_t nhubs = 0;
+  float* hub_pre = nullptr;     // [N]
+  uint32_t* hub_flag = nullptr; // [N]
   bool mixed = false;
   int gather = G_F32;
   int strat = S_THREAD;
@@ -453,6 +467,11 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.num_active = e->num_active;
   p.pre = use_pre ? e->pre : nullptr;
   p.count_mode = e->count_mode;
+  p.f32_mask = e->fmask;
+  p.hub_list = e->hub_list;
+  p.nhubs = e->nhubs;
+  p.hub_pre = e->hub_pre;
+  p.hub_flag = e->hub_flag;
   p.stream_evict_first = e->stream_evict_first;
   p.host_parity = (int)(e->h_step & 1);
   p.entry = e->entry;
@@ -594,8 +613,10 @@ int refresh_tiles(fs_engine* e, cudaStream_t st) {
                                                        e->active_tiles, e->num_active);
     // inactive tiles are never rewritten: make both buffers agree on them
     const int blocks2 = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
-    if (e->count_mode)
+    if (e->count_mode || e->fmask)
       k_sync_buffers<uint32_t><<<blocks2, 256, 0, st>>>(e->dstate + e->s_cur, e->b.imask[0], e->b.imask[1], e->ntiles_mask);
+    if (e->count_mode)
+      ;  // the mask is the whole infectivity
     else if (e->mixed)
       k_sync_buffers<__nv_bfloat16><<<blocks2, 256, 0, st>>>(e->dstate + e->s_cur, (__nv_bfloat16*)e->b.infectivity[0],
                                                              (__nv_bfloat16*)e->b.infectivity[1], n);
@@ -734,6 +755,21 @@ int fs_host_unregister(void* p) {
   return 0;
 }
 
+// fused edge-merge: the nodes with more than kWide in-edges, heaviest first
+// (fs_setup.cu: degree flags, compaction, descending sort by degree)
+static int build_hub_list(fs_engine* e) {
+  const int64_t n = e->g.num_nodes;
+  int rc = dalloc(&e->hub_list, (size_t)n);
+  if (!rc) rc = dalloc(&e->hub_pre, (size_t)n);
+  if (!rc) rc = dalloc(&e->hub_flag, (size_t)n);
+  if (rc) return rc;
+  FS_CUDA(cudaMemset(e->hub_flag, 0, sizeof(uint32_t) * n));
+  rc = fs_hub_list(e->g.row_offsets, n, kWide, e->hub_list, &e->nhubs, nullptr);
+  if (rc) return rc;
+  FS_CUDA(cudaDeviceSynchronize());
+  return 0;
+}
+
 static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* c, const fs_state_buffers* buf,
                          const fs_scalars* scal, int device, const fs_partition* part, fs_engine** out) {
   if (!g || !m || !c || !buf || !scal || !out) return set_error(FS_EINVAL, "null argument");
@@ -814,25 +850,54 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     delete e;
     return set_error(FS_EINVAL, "unequal partition ranges need incremental counts (the mask all-gather needs equal segments)");
   }
-  // MERGE (scale-free graphs): the edge-chunked merge gather kernel, then the
-  // step.  FS_MERGE_FUSED=1 runs one launch instead — the f32 fold thread per
-  // short slice and warp per hub (S_HYBRID), the count gather tile-
-  // cooperatively — which measured 2-3x slower on BA graphs: the hubs are the
-  // lowest node ids, so the warps of the first tiles fold tens of thousands
-  // of hub edges serially while the merge kernel spreads them by edge chunks
-  //
-  e->merge = c->strategy == FS_MERGE && g->num_edges > 0 && !e->incr && !getenv("FS_MERGE_FUSED");
+  // (The first fused MERGE form — hubs folded by the warp of their tile —
+  // measured 2-3x slower than the 2-launch merge on BA graphs: the hubs are
+  // the lowest node ids, so the first tiles' warps folded tens of thousands
+  // of hub edges serially.  The hub pre-pass below spreads them over the grid.)
+  int rc = 0;
+#define TRY(x) do { rc = (x); if (rc) { fs_engine_destroy(e); return rc; } } while (0)
+  TRY(dalloc(&e->bad_flag, 1));
   e->strat = c->strategy == FS_LANE ? S_WARP : S_THREAD;
+  // f32 gather: keep a bitmap of the nodes with nonzero infectivity next to
+  // the infectivity buffers and gather only those (fold_*_masked) — exact
+  // for finite weights; one partition; not the warp-per-node LANE fold
+  if (!e->count_mode && buf->imask[0] && buf->imask[1] && !part && e->strat != S_WARP && !getenv("FS_NO_F32_MASK")) {
+    bool finite = true;
+    if (g->num_edges > 0) {
+      if (g->weights_uniform) {
+        finite = std::isfinite(g->uniform_weight);
+      } else {
+        TRY(cudaMemset(e->bad_flag, 0, sizeof(int)) == cudaSuccess ? 0 : set_error(FS_ECUDA, "memset"));
+        k_any_nonfinite<<<(int)std::min<int64_t>((g->num_edges + 255) / 256, (int64_t)e->sms * 8), 256>>>(
+            g->weights, g->weights_dtype == FS_BF16, g->num_edges, e->bad_flag);
+        int bad = 0;
+        TRY(cudaMemcpy(&bad, e->bad_flag, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : set_error(FS_ECUDA, "nonfinite check"));
+        finite = bad == 0;
+      }
+    }
+    e->fmask = finite;
+  }
+  // EDGE_MERGE (scale-free graphs), f32 gather with the mask: ONE launch —
+  // the grid's warps first fold the hub rows (in-degree > kWide), heaviest
+  // first, round robin, then sweep the tiles, reading the hubs' results
+  // (S_HYBRID).  Count gather without incremental counts:
+  // the edge-chunked merge gather kernel, then the step (2 launches).
+  e->merge = c->strategy == FS_MERGE && g->num_edges > 0 && !e->incr && (!e->fmask || getenv("FS_MERGE_UNFUSED"));
   if (c->strategy == FS_MERGE && !e->merge && !e->count_mode) e->strat = S_HYBRID;
+  if (e->merge) e->fmask = false;
   if (e->incr) e->gather = G_INCR;
   else if (e->merge) e->gather = G_PRE;
   else if (e->count_mode) e->gather = e->mask_smem ? G_COUNT_SMEM : G_COUNT_GLOBAL;
+  else if (e->fmask)  // (+ the hub fold stages of 32 warps behind the mask)
+    e->gather = (size_t)e->ntiles_mask * 4 + (e->strat == S_HYBRID ? 32u * kHubPass * 4u : 0u) <= kMaxSmemMaskBytes
+                    ? G_F32M_SMEM : G_F32M_GLOBAL;
   else e->gather = G_F32;
 
-  int rc = 0;
-#define TRY(x) do { rc = (x); if (rc) { fs_engine_destroy(e); return rc; } } while (0)
   for (int mat = 0; mat < 2; ++mat) e->step_fn[mat] = pick_step(e->mixed, e->gather, e->strat, mat != 0, e->step_block);
-  e->step_smem = (e->gather == G_COUNT_SMEM) ? (size_t)((e->ntiles_mask + 3) & ~3LL) * 4 : 0;
+  e->step_smem = (e->gather == G_COUNT_SMEM || e->gather == G_F32M_SMEM) ? (size_t)((e->ntiles_mask + 3) & ~3LL) * 4 : 0;
+  if (e->gather == G_F32M_SMEM && e->strat == S_HYBRID)
+    e->step_smem += (size_t)(e->step_block / 32) * kHubPass * sizeof(float);  // the hub fold stages behind the mask
+  if (e->strat == S_HYBRID && e->fmask) TRY(build_hub_list(e));
   int occ = 1;
   for (int mat = 0; mat < 2; ++mat) {
     if (e->step_smem > 0)
@@ -845,7 +910,6 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     const int64_t ctas_needed = (warps_needed + e->step_block / 32 - 1) / (e->step_block / 32);
     e->step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sms * occ, ctas_needed));
   }
-  TRY(dalloc(&e->bad_flag, 1));
   if (e->count_mode) {
     e->ptab_len = (int64_t)g->d_max + 1;
     TRY(dalloc(&e->ptab, e->ptab_len));
@@ -1053,7 +1117,8 @@ void fs_engine_destroy(fs_engine* e) {
   cudaDeviceSynchronize();  // no kernel of this engine is still in flight on any stream
   void* ptrs[] = {e->dstate, e->acc, e->log_clock, e->log_tau, e->log_counts, e->ptab,
                   e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag,
-                  e->cnt, e->entry, e->ctab, e->cage, e->dbg, e->uni_range, e->remote_log};
+                  e->cnt, e->entry, e->ctab, e->cage, e->dbg, e->uni_range, e->remote_log,
+                  e->hub_list, e->hub_pre, e->hub_flag};
   for (void* q : ptrs) if (q) cudaFreeAsync(q, (cudaStream_t)0);
   for (void* q : {(void*)e->delta[0], (void*)e->delta[1]})
     if (q) {
@@ -1256,10 +1321,11 @@ int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream) {
   if ((in->step ^ cur.s.step) & 1) {
     // the step parity selects the current infectivity / mask buffer: move it
     const int from = (int)(cur.s.step & 1), to = from ^ 1;
-    if (e->count_mode) {
+    if (e->count_mode || e->fmask) {
       const size_t bytes = (size_t)((e->ntiles_mask + 1 + 3) & ~3LL) * 4;
       FS_CUDA(cudaMemcpyAsync(e->b.imask[to], e->b.imask[from], bytes, cudaMemcpyDeviceToDevice, st));
-    } else {
+    }
+    if (!e->count_mode) {
       const size_t bytes = (size_t)e->g.num_nodes * (e->mixed ? 2 : 4);
       FS_CUDA(cudaMemcpyAsync(e->b.infectivity[to], e->b.infectivity[from], bytes, cudaMemcpyDeviceToDevice, st));
     }
@@ -1271,6 +1337,8 @@ int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream) {
     rc = recount(e, in->step, st);
     if (rc) return rc;
   }
+  if (e->hub_flag && in->step != cur.s.step)  // hub tags are step numbers
+    FS_CUDA(cudaMemsetAsync(e->hub_flag, 0, sizeof(uint32_t) * e->g.num_nodes, st));
   if (in->step != cur.s.step) {  // memo tags and cohorts are relative to the step counter
     rc = reset_memo(e, st);
     if (rc) return rc;
@@ -1310,6 +1378,14 @@ int fs_engine_load_infectivity(fs_engine* e, const void* inf, void* stream) {
   const size_t bytes = (size_t)n * (e->mixed ? 2 : 4);
   FS_CUDA(cudaMemcpyAsync(e->b.infectivity[0], inf, bytes, cudaMemcpyDeviceToDevice, st));
   FS_CUDA(cudaMemcpyAsync(e->b.infectivity[1], inf, bytes, cudaMemcpyDeviceToDevice, st));
+  if (e->fmask) {  // the nonzero bitmap of the loaded values, both parities
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8));
+    if (e->mixed)
+      k_load_mask<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)inf, n, 0.0f, e->b.imask[0], e->b.imask[1], nullptr);
+    else
+      k_load_mask<float><<<blocks, 256, 0, st>>>((const float*)inf, n, 0.0f, e->b.imask[0], e->b.imask[1], nullptr);
+    FS_CUDA(cudaGetLastError());
+  }
   return 0;
 }
 

@@ -330,3 +330,65 @@ int fs_narrow_offsets(const int64_t* row_offsets, int64_t len, int32_t* out, voi
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// hub list of the fused edge-merge step (fs_engine.cu build_hub_list): the
+// nodes with more than `wide` in-edges, sorted by in-degree, heaviest first
+// (ties by node id), so the step's round-robin pre-pass hands the longest
+// folds out first
+// ---------------------------------------------------------------------------
+namespace fs {
+namespace {
+__global__ void k_hub_flags(const int64_t* __restrict__ ro, int64_t n, int64_t wide, uint8_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (ro[i + 1] - ro[i]) > wide ? 1 : 0;
+}
+__global__ void k_hub_degrees(const int64_t* __restrict__ ro, const int32_t* __restrict__ ids, const long long* num,
+                              int32_t* __restrict__ deg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < *num; i += (int64_t)gridDim.x * blockDim.x)
+    deg[i] = (int32_t)(ro[ids[i] + 1] - ro[ids[i]]);
+}
+}  // namespace
+
+int fs_hub_list(const int64_t* row_offsets, int64_t n, int wide, int32_t* out, int64_t* num_out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  *num_out = 0;
+  if (n <= 0) return 0;
+  uint8_t* flags = nullptr;
+  int32_t *ids = nullptr, *deg = nullptr, *deg2 = nullptr;
+  long long* d_num = nullptr;
+  void* tmp = nullptr;
+  size_t tb1 = 0, tb2 = 0;
+  FS_CUDA(cudaMallocAsync(&flags, n, st));
+  FS_CUDA(cudaMallocAsync(&ids, sizeof(int32_t) * n, st));
+  FS_CUDA(cudaMallocAsync(&d_num, sizeof(long long), st));
+  const int g = grid_of(n);
+  k_hub_flags<<<g, 256, 0, st>>>(row_offsets, n, wide, flags);
+  cub::CountingInputIterator<int32_t> it(0);
+  cub::DeviceSelect::Flagged(nullptr, tb1, it, flags, ids, d_num, (int)n, st);
+  FS_CUDA(cudaMallocAsync(&tmp, tb1 + 16, st));
+  cub::DeviceSelect::Flagged(tmp, tb1, it, flags, ids, d_num, (int)n, st);
+  long long hn = 0;
+  FS_CUDA(cudaMemcpyAsync(&hn, d_num, sizeof hn, cudaMemcpyDeviceToHost, st));
+  FS_CUDA(cudaStreamSynchronize(st));
+  cudaFreeAsync(tmp, st);
+  tmp = nullptr;
+  int rc = 0;
+  if (hn > 0) {
+    FS_CUDA(cudaMallocAsync(&deg, sizeof(int32_t) * hn, st));
+    FS_CUDA(cudaMallocAsync(&deg2, sizeof(int32_t) * hn, st));
+    k_hub_degrees<<<grid_of(hn), 256, 0, st>>>(row_offsets, ids, d_num, deg);
+    cub::DoubleBuffer<int32_t> keys(deg, deg2), vals(ids, out);
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tb2, keys, vals, (int)hn, 0, 32, st);
+    FS_CUDA(cudaMallocAsync(&tmp, tb2 + 16, st));
+    cub::DeviceRadixSort::SortPairsDescending(tmp, tb2, keys, vals, (int)hn, 0, 32, st);
+    if (vals.Current() != out) FS_CUDA(cudaMemcpyAsync(out, vals.Current(), sizeof(int32_t) * hn, cudaMemcpyDeviceToDevice, st));
+    FS_CUDA(cudaGetLastError());
+  }
+  FS_CUDA(cudaStreamSynchronize(st));
+  for (void* q : {(void*)flags, (void*)ids, (void*)deg, (void*)deg2, (void*)d_num, tmp})
+    if (q) cudaFreeAsync(q, st);
+  *num_out = hn;
+  return rc;
+}
+}  // namespace fs

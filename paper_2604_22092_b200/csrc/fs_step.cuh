@@ -20,7 +20,10 @@ constexpr int kCntStride = FS_MAX_COMPARTMENTS;
 // tables on a 227 KB CTA
 constexpr size_t kMaxSmemMaskBytes = 188u * 1024u;  // + ~34 KB static (queues) <= 227 KB
 
-enum Gather { G_COUNT_SMEM = 0, G_COUNT_GLOBAL = 1, G_F32 = 2, G_PRE = 3, G_INCR = 4 };
+// G_F32M_*: the f32 fold with a nonzero-infectivity bitmap prefilter — the
+// mask (staged in shared memory, or read from L2) says which in-neighbours
+// carry infectivity; only those are gathered and folded
+enum Gather { G_COUNT_SMEM = 0, G_COUNT_GLOBAL = 1, G_F32 = 2, G_PRE = 3, G_INCR = 4, G_F32M_SMEM = 5, G_F32M_GLOBAL = 6 };
 constexpr int32_t kEntryInvalid = INT32_MIN;  // age not known to follow its cohort (init, host edits)
 constexpr int kCohortSlots = 2;                // age-dependent compartments with a cohort table
 constexpr int kCohortW = 1 << 10;              // cohorts (entry steps) per table: a ring
@@ -88,6 +91,14 @@ struct StepParams {
   const int64_t* num_active;
   const float* pre;              // G_PRE: gathered pressure
   int count_mode;
+  int f32_mask;                  // f32 gather keeps the nonzero-infectivity mask (G_F32M_*)
+  // fused edge-merge (S_HYBRID + G_F32M_*): the nodes with more than kWide
+  // in-edges, heaviest first, are folded by the grid's warps round robin
+  // before the tile sweep; a tile lane of such a node waits for its flag
+  const int32_t* hub_list;
+  int64_t nhubs;
+  float* hub_pre;                // [N] pressure of the hubs (entries of hubs only)
+  uint32_t* hub_flag;            // [N] step tag (step + 1) once hub_pre[n] holds this step's value
   // incremental count mode (G_INCR): per-node infectious in-neighbour count,
   // kept current by +-1 pushes along the outgoing edges of every node whose
   // infectious status changes
@@ -410,6 +421,106 @@ __device__ __forceinline__ float fold_thread(const int32_t* __restrict__ col, co
   return acc;
 }
 
+// the same fold with the nonzero-infectivity bitmap as a prefilter: a column
+// whose mask bit is clear has infectivity exactly 0, so its contribution
+// f32(0 * w) = +-0 leaves the accumulator unchanged (it is never -0: it starts
+// at +0 and x + (-x) rounds to +0) — only the set bits are gathered and
+// folded, still in CSR order.  Needs finite weights (0 * inf = NaN), which
+// the engine checks before it selects this gather.
+template <typename IT, bool SMEM>
+__device__ __forceinline__ float fold_thread_masked(const int32_t* __restrict__ col, const uint32_t* m, const void* inf,
+                                                    const void* w, int w_bf16, int w_uniform, float w_val,
+                                                    int64_t lo, int64_t hi) {
+  float acc = 0.0f;
+  for (int64_t e = lo; e < hi; e += kFoldB) {
+    int32_t c[kFoldB];
+#pragma unroll
+    for (int u = 0; u < kFoldB; ++u) c[u] = (e + u < hi) ? __ldg(col + e + u) : 0;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int u = 0; u < kFoldB; ++u)
+      if (e + u < hi) bits |= (uint32_t)mask_bit<SMEM>(m, c[u]) << u;
+    if (bits) {
+      float v[kFoldB];
+#pragma unroll
+      for (int u = 0; u < kFoldB; ++u)
+        if ((bits >> u) & 1u) v[u] = __fmul_rn(load_inf<IT>(inf, c[u]), w_uniform ? w_val : load_w(w, w_bf16, e + u));
+#pragma unroll
+      for (int u = 0; u < kFoldB; ++u)
+        if ((bits >> u) & 1u) acc = __fadd_rn(acc, v[u]);
+    }
+  }
+  return acc;
+}
+
+// One hub row [lo, hi) folded by the whole warp with the mask prefilter:
+// passes of 8 x 32 coalesced column loads, mask tests and ballots; the lanes
+// gather the infectivities of their set columns (in registers), stage them in
+// shared memory in edge order, and lane 0 folds only the set positions, in
+// CSR order, while the next pass's loads are in flight.  Every lane returns
+// the sum.
+constexpr int kHubPass = 256;
+template <typename IT, bool SMEM_MASK>
+__device__ __forceinline__ float fold_hub_masked(const int32_t* __restrict__ col, const uint32_t* m, const void* inf,
+                                                 const void* w, int w_bf16, int w_uniform, float w_val, int64_t lo,
+                                                 int64_t hi, int lane, float* stage, uint64_t col_pol) {
+  constexpr int U = kHubPass / 32;
+  float acc = 0.0f;
+  float v[U];
+  unsigned bal[U];
+  auto pass = [&](int64_t base) {
+    uint32_t c[U], word[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = base + 32 * u + lane;
+      c[u] = e < hi ? (uint32_t)ldg_hint(col + e, col_pol) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) word[u] = SMEM_MASK ? m[c[u] >> 5] : ldg_hint(m + (c[u] >> 5), l2_policy_last());
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = base + 32 * u + lane;
+      const bool on = e < hi && ((word[u] >> (c[u] & 31)) & 1u);
+      bal[u] = __ballot_sync(0xffffffffu, on);
+      v[u] = on ? __fmul_rn(load_inf<IT>(inf, (int32_t)c[u]), w_uniform ? w_val : load_w(w, w_bf16, e)) : 0.0f;
+    }
+  };
+  pass(lo);
+  for (int64_t base = lo; base < hi; base += kHubPass) {
+    unsigned sb[U];
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      stage[32 * u + lane] = v[u];
+      sb[u] = bal[u];
+    }
+    __syncwarp();
+    if (base + kHubPass < hi) pass(base + kHubPass);  // in flight during the chain below
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        unsigned W = sb[u];
+        while (W) {
+          const int bit = __ffs(W) - 1;
+          W &= W - 1;
+          acc = __fadd_rn(acc, stage[32 * u + bit]);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  return __shfl_sync(0xffffffffu, acc, 0);
+}
+
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // warp-cooperative fold of one slice, still in CSR order: lanes load 32
 // consecutive contributions, then every lane folds them in lane order
 // (renewal.py:221-242 semantics; padding lanes contribute +0).
@@ -437,10 +548,12 @@ __device__ __forceinline__ float fold_warp(const int32_t* __restrict__ col, cons
 // sequential fold (renewal.py:60-68) — while the next 128 contributions are
 // already in flight.
 constexpr int kFoldStage = 128;
-template <typename IT>
+// FM: nonzero-infectivity mask prefilter (mask `m`, in shared memory when SM):
+// only set columns are gathered, and a stage without one is not folded.
+template <typename IT, bool FM = false, bool SM = false>
 __device__ __forceinline__ float fold_warp_staged(const int32_t* __restrict__ col, const void* inf, const void* w,
                                                   int w_bf16, int w_uniform, float w_val, int64_t lo, int64_t hi,
-                                                  int lane, float* stage) {
+                                                  int lane, float* stage, const uint32_t* m = nullptr) {
   constexpr int R = kFoldStage / 32;
   float acc = 0.0f;
   float v[R];
@@ -455,17 +568,23 @@ __device__ __forceinline__ float fold_warp_staged(const int32_t* __restrict__ co
     for (int r = 0; r < R; ++r) {
       const int64_t e = base + 32 * r + lane;
       v[r] = 0.0f;
-      if (e < hi) v[r] = __fmul_rn(load_inf<IT>(inf, c[r]), w_uniform ? w_val : load_w(w, w_bf16, e));
+      if (e < hi && (!FM || mask_bit<SM>(m, c[r])))
+        v[r] = __fmul_rn(load_inf<IT>(inf, c[r]), w_uniform ? w_val : load_w(w, w_bf16, e));
     }
   };
   gather(lo);
   for (int64_t base = lo; base < hi; base += kFoldStage) {
     __syncwarp();
+    bool any = !FM;
 #pragma unroll
-    for (int r = 0; r < R; ++r) stage[32 * r + lane] = v[r];
+    for (int r = 0; r < R; ++r) {
+      stage[32 * r + lane] = v[r];
+      if (FM) any |= v[r] != 0.0f;
+    }
+    if (FM) any = __any_sync(kFull, any);  // skipped stages hold only +-0: the chain is unchanged
     __syncwarp();
     if (base + kFoldStage < hi) gather(base + kFoldStage);  // in flight during the chain below
-    if (lane == 0) {
+    if (lane == 0 && any) {
       const int64_t rem = hi - base;
       const int live = rem < kFoldStage ? (int)rem : kFoldStage;
       if (live == kFoldStage) {
@@ -505,6 +624,7 @@ struct StepConst {
   int edge_from, infectious, shed;
   float beta_f;
   bool write_inf;
+  bool write_mask;               // maintain the next-step mask words
 };
 
 // shared-memory model tables + the per-warp deferral queues
@@ -559,6 +679,7 @@ __device__ __forceinline__ StepConst step_const(const StepParams& p, bool count_
   k.shed = p.model.shedding;
   k.beta_f = __double2float_rn(p.model.beta);
   k.write_inf = !count_gather;
+  k.write_mask = count_gather || p.f32_mask;
   return k;
 }
 
@@ -759,7 +880,12 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
       nage = __fadd_rn(age, k.tau_f);  // queued nodes are never terminal
     }
     if (!UNI || fire || s != k.edge_from) reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
-    if (k.write_inf) inf_nxt[n] = from_f32<IT>(inf_value(p, k, ns, nage));
+    if (k.write_inf) {
+      const IT iv = from_f32<IT>(inf_value(p, k, ns, nage));
+      inf_nxt[n] = iv;
+      // f32 mask: phase A left this (deferred) node's bit clear
+      if (k.write_mask && to_f32<IT>(iv) != 0.0f) atomicOr(mask_nxt + p.tile_base + (n >> 5), 1u << (n & 31));
+    }
     if (MAT) p.rates[n] = rate;
   }
   if (p.cnt) {
@@ -832,20 +958,27 @@ __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepCons
   const bool isS = s == k.edge_from;
   const bool term = valid && sh.term[s] != 0;
   const bool defer = valid && !term && (!isS || pressure > 0.0f);
+  bool nz = false;  // f32 gather: this node's next-step infectivity is nonzero (deferred nodes: phase B)
   if (!UNI && valid && !term && !defer) {  // S with zero pressure: rate 0, ages (UNI: the uniform scalar)
     const float nage = __fadd_rn(age, k.tau_f);
     reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
-    if (k.write_inf) inf_nxt[n] = from_f32<IT>(inf_value(p, k, s, nage));
+    if (k.write_inf) {
+      const IT iv = from_f32<IT>(inf_value(p, k, s, nage));
+      inf_nxt[n] = iv;
+      nz = to_f32<IT>(iv) != 0.0f;
+    }
   } else if (term && k.write_inf) {
-    inf_nxt[n] = from_f32<IT>(inf_value(p, k, s, age));
+    const IT iv = from_f32<IT>(inf_value(p, k, s, age));
+    inf_nxt[n] = iv;
+    nz = to_f32<IT>(iv) != 0.0f;
   }
   if (MAT && valid) {
     p.pressure[n] = pressure;
     if (!defer) p.rates[n] = 0.0f;
   }
-  if (!k.write_inf) {
+  if (k.write_mask) {
     // next-step mask word; deferred nodes are fixed up in phase B
-    const unsigned word = __ballot_sync(0xffffffffu, valid && s == k.infectious);
+    const unsigned word = __ballot_sync(0xffffffffu, k.write_inf ? nz : (valid && s == k.infectious));
     if (lane == 0) mask_nxt[p.tile_base + tile] = word;
   }
   const unsigned dm = __ballot_sync(0xffffffffu, defer);
@@ -910,14 +1043,23 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   constexpr int WARPS = BLOCK / 32;
   __shared__ StepShared<WARPS> sh;
   __shared__ __align__(8) uint64_t s_bar;
-  __shared__ __align__(16) float s_fold[STRAT == S_HYBRID ? WARPS * kFoldStage : 4];  // hub fold stages
   constexpr bool COUNT = (GATHER == G_COUNT_SMEM || GATHER == G_COUNT_GLOBAL);
+  constexpr bool FMASK = (GATHER == G_F32M_SMEM || GATHER == G_F32M_GLOBAL);  // f32 fold, mask prefilter
+  constexpr bool F32 = GATHER == G_F32 || FMASK;
+  constexpr bool SMASK = (GATHER == G_COUNT_SMEM || GATHER == G_F32M_SMEM);   // mask staged in shared memory
+  // hub fold stages: static, or behind the staged mask in dynamic shared
+  // memory (a 1024-thread CTA's static tables would pass 48 KB)
+  constexpr int kStage = FMASK ? kHubPass : kFoldStage;  // per-warp hub stage
+  __shared__ __align__(16) float s_fold_static[(STRAT == S_HYBRID && !SMASK) ? WARPS * kStage : 4];
+  float* const s_fold = (STRAT == S_HYBRID && SMASK)
+                            ? reinterpret_cast<float*>(s_mask + ((p.ntiles_mask + 3) & ~3LL))
+                            : s_fold_static;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   pdl_wait();
-  if (GATHER == G_COUNT_SMEM && tid == 0) mbar_init(&s_bar, 1);
+  if (SMASK && tid == 0) mbar_init(&s_bar, 1);
   load_tables<WARPS>(p, sh, tid);
-  const StepConst k = step_const(p, COUNT || p.count_mode);
+  const StepConst k = step_const(p, COUNT || (p.count_mode && !F32));
   if (blockIdx.x == 0 && tid == 0) commit_step_start(p, k);
   const int cur = (int)(k.step & 1);
   const uint32_t* mask_cur = p.mask[cur];
@@ -927,11 +1069,36 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   __syncthreads();
   // stage the whole infectious mask (N/8 bytes) in shared memory with TMA
   // bulk copies; the first tile's node loads below overlap the transfer
-  if (GATHER == G_COUNT_SMEM) stage_mask_async(s_mask, mask_cur, (uint32_t)(((p.ntiles_mask + 3) & ~3LL) * 4), &s_bar);
-  bool mask_ready = GATHER != G_COUNT_SMEM;
-  const uint32_t* gmask = (GATHER == G_COUNT_SMEM) ? s_mask : mask_cur;
+  if (SMASK) stage_mask_async(s_mask, mask_cur, (uint32_t)(((p.ntiles_mask + 3) & ~3LL) * 4), &s_bar);
+  bool mask_ready = !SMASK;
+  const uint32_t* gmask = SMASK ? s_mask : mask_cur;
   float lmax = 0.0f;
   int qn = 0;  // queued entries of this warp (warp-uniform)
+  const uint32_t hub_tag = (uint32_t)k.step + 1u;
+  if (STRAT == S_HYBRID && FMASK) {
+    // fused edge-merge: the hubs first, heaviest first, round robin over every
+    // warp of the grid (all CTAs are resident: grid <= SMs x occupancy), so no
+    // warp folds more than its share of hub edges; the tile sweep below reads
+    // the results
+    if (SMASK && !mask_ready) {
+      mbar_wait_parity(&s_bar, 0);
+      mask_ready = true;
+    }
+    const uint64_t pol = l2_policy_stream(p.stream_evict_first);
+    for (int64_t h = (int64_t)blockIdx.x * WARPS + warp; h < p.nhubs; h += (int64_t)gridDim.x * WARPS) {
+      const int32_t hn = __ldg(p.hub_list + h);
+      const int hs = (int)reinterpret_cast<const ST*>(p.states)[hn];
+      if (hs != k.edge_from && !MAT) continue;  // only S nodes' pressure is used (all of them materialised)
+      const int64_t lo = p.ro32 ? (int64_t)__ldg(p.ro32 + hn) : __ldg(p.ro + hn);
+      const int64_t hi = p.ro32 ? (int64_t)__ldg(p.ro32 + hn + 1) : __ldg(p.ro + hn + 1);
+      const float pr = fold_hub_masked<IT, SMASK>(p.col, gmask, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lo, hi,
+                                                  lane, s_fold + warp * kStage, pol);
+      if (lane == 0) {
+        p.hub_pre[hn] = pr;
+        st_release_u32(p.hub_flag + hn, hub_tag);
+      }
+    }
+  }
 
   const int64_t ntiles = p.active_tiles ? *p.num_active : p.ntiles;
   const int64_t stride = (int64_t)gridDim.x * WARPS;
@@ -984,29 +1151,50 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
     } else if (GATHER == G_PRE) {
       if (need) pressure = __ldg(p.pre + n);
     } else {
-      if (GATHER == G_COUNT_SMEM && !mask_ready) {
+      if (SMASK && !mask_ready) {
         mbar_wait_parity(&s_bar, 0);
         mask_ready = true;
       }
       const unsigned todo = __ballot_sync(kFull, need);
       if (STRAT == S_THREAD) {
-        if (GATHER == G_F32) {
+        if (FMASK) {
+          // (the tile-cooperative sweep, fold_tile_masked, measured slower
+          // here: 40 vs 34 us at C2 with shedding — fewer sectors, more
+          // instructions)
+          if (need)
+            pressure = fold_thread_masked<IT, SMASK>(p.col, gmask, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo,
+                                                     in.hi);
+        } else if (GATHER == G_F32) {
           if (need) pressure = fold_thread<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo, in.hi);
         } else if (todo) {
           const int kk = count_tile<GATHER == G_COUNT_SMEM>(p.col, gmask, in.lo, in.hi, need, todo, lane,
                                                             l2_policy_stream(p.stream_evict_first));
           if (need) pressure = p.ptab_mul ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
         }
+      } else if (STRAT == S_HYBRID && FMASK) {  // fused edge-merge: hubs from the pre-pass
+        const bool wide = need && (in.hi - in.lo > kWide);
+        if (need && !wide) {
+          pressure = fold_thread_masked<IT, SMASK>(p.col, gmask, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo,
+                                                   in.hi);
+        }
+        if (wide) {
+          while (ld_acquire_u32(p.hub_flag + n) != hub_tag) {
+          }
+          pressure = __ldcg(p.hub_pre + n);
+        }
       } else if (STRAT == S_HYBRID) {  // f32 fold: thread per short slice, warp per hub
         const bool wide = need && (in.hi - in.lo > kWide);
-        if (need && !wide) pressure = fold_thread<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo, in.hi);
+        if (need && !wide)
+          pressure = FMASK ? fold_thread_masked<IT, SMASK>(p.col, gmask, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val,
+                                                           in.lo, in.hi)
+                           : fold_thread<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo, in.hi);
         unsigned rest = __ballot_sync(kFull, wide);
         while (rest) {
           const int j = __ffs(rest) - 1;
           rest &= rest - 1;
           const int64_t lj = __shfl_sync(kFull, in.lo, j), hj = __shfl_sync(kFull, in.hi, j);
-          const float pj = fold_warp_staged<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lj, hj, lane,
-                                                s_fold + warp * kFoldStage);
+          const float pj = fold_warp_staged<IT, FMASK, SMASK>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lj,
+                                                              hj, lane, s_fold + warp * kFoldStage, gmask);
           if (lane == j) pressure = pj;
         }
       } else {  // warp per node (LANE strategy)
@@ -1016,7 +1204,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
           rest &= rest - 1;
           const int64_t lj = __shfl_sync(kFull, in.lo, j), hj = __shfl_sync(kFull, in.hi, j);
           float pj;
-          if (GATHER == G_F32) {
+          if (F32) {
             pj = fold_warp<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lj, hj, lane);
           } else {
             const int kk = count_warp<GATHER == G_COUNT_SMEM>(p.col, gmask, lj, hj, lane);
@@ -1031,7 +1219,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   }
   if (qn > 0) drain_queue<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, inf_nxt);
   // a warp without tiles still has to see the bulk copy land before exit
-  if (GATHER == G_COUNT_SMEM && !mask_ready) mbar_wait_parity(&s_bar, 0);
+  if (SMASK && !mask_ready) mbar_wait_parity(&s_bar, 0);
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);
 }
 

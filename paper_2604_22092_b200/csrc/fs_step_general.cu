@@ -27,6 +27,14 @@ StepFn pick_step2(int gather, int strat, int& block) {
       if (strat == S_HYBRID) return k_step<ST, AT, IT, G_F32, S_HYBRID, MAT, 512>;
       return strat == S_WARP ? k_step<ST, AT, IT, G_F32, S_WARP, MAT, 512>
                              : k_step<ST, AT, IT, G_F32, S_THREAD, MAT, 512>;
+    case G_F32M_SMEM:  // the mask in shared memory: one CTA per SM
+      block = 1024;
+      return strat == S_HYBRID ? k_step<ST, AT, IT, G_F32M_SMEM, S_HYBRID, MAT, 1024>
+                               : k_step<ST, AT, IT, G_F32M_SMEM, S_THREAD, MAT, 1024>;
+    case G_F32M_GLOBAL:
+      block = 512;
+      return strat == S_HYBRID ? k_step<ST, AT, IT, G_F32M_GLOBAL, S_HYBRID, MAT, 512>
+                               : k_step<ST, AT, IT, G_F32M_GLOBAL, S_THREAD, MAT, 512>;
     default:
       block = 512;
       return k_step<ST, AT, IT, G_PRE, S_THREAD, MAT, 512>;

@@ -376,9 +376,12 @@ class _Engine:
         dev = state._dev
         self.stream = _device.stream_handle(dev)
         _, _, it = _storage(state.mixed_precision)
+        w = ((n + 31) // 32 + 1 + 3) // 4 * 4  # + a zero sentinel word, 16-byte multiple (TMA)
+        # the infectious mask (count gather), or the nonzero-infectivity
+        # bitmap kept next to the f32 infectivity (the f32 gather's prefilter)
+        self.masks = [_fill(torch.empty(w, dtype=torch.int32, device=dev), 0) for _ in range(2)]
         if plan.count_mode:
-            w = ((n + 31) // 32 + 1 + 3) // 4 * 4  # + a zero sentinel word, 16-byte multiple (TMA)
-            self.bufs = [_fill(torch.empty(w, dtype=torch.int32, device=dev), 0) for _ in range(2)]
+            self.bufs = self.masks
         else:
             self.bufs = [_fill(torch.empty(n, dtype=it, device=dev), 0) for _ in range(2)]
         self.materialize = materialize
@@ -387,9 +390,8 @@ class _Engine:
         b = _lib.FsStateBuffers()
         b.states = _lib.ptr(state._t["states"])
         b.ages = _lib.ptr(state._t["ages"])
-        if plan.count_mode:
-            b.imask[0], b.imask[1] = _lib.ptr(self.bufs[0]), _lib.ptr(self.bufs[1])
-        else:
+        b.imask[0], b.imask[1] = _lib.ptr(self.masks[0]), _lib.ptr(self.masks[1])
+        if not plan.count_mode:
             b.infectivity[0], b.infectivity[1] = _lib.ptr(self.bufs[0]), _lib.ptr(self.bufs[1])
         b.pressure = _lib.ptr(state._t.get("pressure"))
         b.rates = _lib.ptr(state._t.get("rates"))
@@ -454,13 +456,17 @@ class _Engine:
         same step window twice."""
         self.sync_ages()
         t = self.state._t
-        return (t["states"].clone(), t["ages"].clone(), [b.clone() for b in self.bufs], self.scalars())
+        return (t["states"].clone(), t["ages"].clone(), [b.clone() for b in self._mutable_bufs()], self.scalars())
+
+    def _mutable_bufs(self) -> list:
+        # the double buffers a step writes (f32 gather: infectivity and its bitmap)
+        return self.bufs if self.plan.count_mode else self.bufs + self.masks
 
     def restore(self, snap: tuple) -> None:
         st, ag, bufs, sc = snap
         self.state._t["states"].copy_(st)
         self.state._t["ages"].copy_(ag)
-        for dst, src in zip(self.bufs, bufs):
+        for dst, src in zip(self._mutable_bufs(), bufs):
             dst.copy_(src)
         self.set_scalars(sc)
         # incremental counts / pending deltas follow the restored mask, not

@@ -156,6 +156,28 @@ def test_variants_are_result_neutral(name, overrides):
     assert_matches(st, log, cps, ref)
 
 
+@pytest.mark.parametrize("env", [{}, {"FS_MERGE_UNFUSED": "1"}, {"FS_NO_F32_MASK": "1"}])
+@pytest.mark.parametrize("overrides", [
+    {"gather": "f32", "strategy": Strategy.EDGE_MERGE},           # fused edge-merge: hub pre-pass + tile sweep
+    {"gather": "f32", "strategy": Strategy.EDGE_MERGE, "edges_per_block": 64},
+    {"gather": "f32", "strategy": Strategy.PER_NODE},             # thread-per-node fold, mask prefilter
+    {"gather": "f32", "strategy": Strategy.EDGE_MERGE, "compaction": True},
+])
+@pytest.mark.parametrize("name", ["ba_merge", "shed_hazard", "weighted", "c1_mixed"])
+def test_f32_gather_forms_bit_exact(name, overrides, env, monkeypatch):
+    """Every form of the f32 CSR fold — with and without the nonzero-
+    infectivity mask, the one-launch edge-merge and the two-launch one —
+    against the reference goldens, stepwise and graph-replayed."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    st, log, cps, ref = run_engine_case(name, overrides=overrides)
+    assert_matches(st, log, cps, ref)
+    st, log, _, ref = run_engine_case(name, overrides=overrides, batches_via_graph=True)
+    assert np.array_equal(log["counts"], ref["counts"])
+    assert np.array_equal(log["clock"], ref["clock"])
+    assert np.array_equal(st.states.astype(np.int32), ref["states"])
+
+
 @pytest.mark.parametrize("gather", ["incremental", "count"])
 @pytest.mark.parametrize("name", ["c1", "ba_merge"])
 def test_compaction_graph_replay_neutral(name, gather):

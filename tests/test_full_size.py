@@ -74,22 +74,32 @@ def test_c3_ba_merge_vs_oracle():
     assert np.allclose(st.ages, ref.ages, rtol=1e-5, atol=0)
 
 
-def test_c3_full_size_ba_weibull_erlang_vs_oracle():
-    """BASELINE C3 at its own size: BA N=1e6, m=5, seed 1, Weibull/Erlang,
-    60 steps (graph-replayed batches) against the oracle port.  Counts
-    per step, states, ages and clock exact."""
+@pytest.fixture(scope="module")
+def c3_oracle():
     g = fs.gen_barabasi_albert(N, 5, seed=1)
     m = fs.seir_weibull_erlang(0.25)
     cfg = fs.RenewalConfig(steps_per_batch=20)
-    assert fs.select_strategy(fs.degree_stats(g)) == Strategy.EDGE_MERGE
     ref = O.init_state(g, m, cfg, 7)
+    for _ in range(3):
+        O.run_batch(ref, g, m, cfg, 7)
+    return g, m, ref
+
+
+@pytest.mark.parametrize("gather", ["auto", "f32", "count"])
+def test_c3_full_size_ba_weibull_erlang_vs_oracle(c3_oracle, gather):
+    """BASELINE C3 at its own size: BA N=1e6, m=5, seed 1, Weibull/Erlang,
+    60 steps (graph-replayed batches) against the oracle port, through the
+    default incremental counts, the one-launch f32 edge-merge fold and the
+    count-gather merge.  Counts per step, states, ages and clock exact."""
+    g, m, ref = c3_oracle
+    cfg = fs.RenewalConfig(steps_per_batch=20, gather=gather)
+    assert fs.select_strategy(fs.degree_stats(g)) == Strategy.EDGE_MERGE
     st = fs.init_renewal_state(g, m, cfg, 7)
     counts = []
     for _ in range(3):
         rec = []
         fs.run_batch(st, g, m, cfg, 7, recorder=rec)
         counts += [c for _, c in rec]
-        O.run_batch(ref, g, m, cfg, 7)
     assert np.array_equal(np.array(counts), np.array([c for _, _, c in ref.log]))
     assert np.array_equal(st.states.astype(np.int32), ref.states.astype(np.int32))
     assert np.array_equal(st.ages, ref.ages)
