@@ -678,6 +678,13 @@ int sync_s_ages(fs_engine* e, cudaStream_t st) {
   return 0;
 }
 
+// the streaming step variants for the engine's current flags.  (A two-
+// nodes-per-lane form — 64-node tiles, vector loads, SIMD halfword count
+// folds — measured slower: C2 -3.5 %, C4 -10 %.)
+void set_stream_fns(fs_engine* e, bool uni) {
+  for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, e->stream_memo, e->stream_hubs, uni);
+}
+
 // (re)decide the uniform-S-age mode from the ages array (engine creation,
 // host edits): on iff every S node holds the same age; the scalar is set to
 // it.  Switching the mode switches the step kernel, so batch graphs go.
@@ -706,8 +713,7 @@ int recheck_uniform(fs_engine* e, cudaStream_t st) {
   if (uni != e->s_uniform) {
     e->s_uniform = uni;
     drop_batch_graphs(e);
-    for (int mat = 0; mat < 2; ++mat)
-      e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, e->stream_memo, e->stream_hubs, uni);
+    set_stream_fns(e, uni);
   }
   return 0;
 }
@@ -1029,7 +1035,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     if (buf->padded >= 2 && !getenv("FS_NO_STREAM")) {
       e->stream = true;
       e->stream_hubs = g->d_max > 32;
-      for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, false, e->stream_hubs, false);
+      set_stream_fns(e, false);
       int socc = 1;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&socc, (const void*)e->stream_fn[0], 512, 0) != cudaSuccess || socc < 1) socc = 1;
       if (getenv("FS_INCR_CTAS_PER_SM")) socc = std::max(1, std::min(socc, atoi(getenv("FS_INCR_CTAS_PER_SM"))));
@@ -1058,7 +1064,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
       TRY(reset_memo(e, nullptr));
       if (e->stream) {  // the memo's shared-memory table only in the variant that uses it
         e->stream_memo = true;
-        for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, true, e->stream_hubs, false);
+        set_stream_fns(e, false);
       }
     }
   }

@@ -309,6 +309,21 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// [lo, hi) of node n in two halves, so the loads of the next tile stay in
+// flight while this one is processed: load_slice_raw issues them (lo <- the
+// lane's own offset, hi <- offset n+1 where no neighbour lane holds it) and
+// finish_slice, at the tile's turn, takes hi from lane+1
+__device__ __forceinline__ void load_slice_raw(const int64_t* __restrict__ ro, const int32_t* __restrict__ ro32,
+                                               int64_t n, int64_t N, bool valid, int lane, int64_t& lo, int64_t& hi) {
+  lo = valid ? (ro32 ? (int64_t)__ldg(ro32 + n) : __ldg(ro + n)) : 0;
+  hi = (valid && (lane == 31 || n + 1 >= N)) ? (ro32 ? (int64_t)__ldg(ro32 + n + 1) : __ldg(ro + n + 1)) : 0;
+}
+__device__ __forceinline__ void finish_slice(int64_t n, int64_t N, bool valid, int lane, int64_t lo, int64_t& hi) {
+  const int64_t up = __shfl_down_sync(0xffffffffu, lo, 1);
+  hi = !valid ? lo : ((lane == 31 || n + 1 >= N) ? hi : up);
+}
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 // [lo, hi) of node n: int32 copy when present; neighbouring lanes share
 // boundaries, so each lane loads one offset and takes hi from lane+1
 __device__ __forceinline__ void load_slice(const int64_t* __restrict__ ro, const int32_t* __restrict__ ro32,
@@ -1114,7 +1129,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
         in.hi = reinterpret_cast<const uint16_t*>(p.pend[cur])[n];
       }
     } else if (GATHER != G_PRE) {
-      load_slice(p.ro, p.ro32, n, valid, lane, in.lo, in.hi);
+      load_slice_raw(p.ro, p.ro32, n, p.n, valid, lane, in.lo, in.hi);  // finished at the tile's turn
     }
   };
   auto tile_of = [&](int64_t t) -> int64_t { return p.active_tiles ? (int64_t)p.active_tiles[t] : t; };
@@ -1127,14 +1142,16 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
     load_in(tile_n, nxt);
   }
   for (; t < ntiles; t += stride) {
-    const NodeIn<ST, AT> in = nxt;
+    NodeIn<ST, AT> in = nxt;
     const int64_t tile = tile_n;
-    if (t + stride < ntiles) {  // next tile's node loads overlap this tile
+    const bool more = t + stride < ntiles;
+    if (more) {  // next tile's node loads overlap this tile
       tile_n = tile_of(t + stride);
       load_in(tile_n, nxt);
     }
     const int64_t n = tile * 32 + lane;
     const bool valid = n < p.n;
+    if (GATHER != G_INCR && GATHER != G_PRE) finish_slice(n, p.n, valid, lane, in.lo, in.hi);
     const bool need = valid && (in.s == k.edge_from || MAT);
 
     float pressure = 0.0f;
@@ -1214,6 +1231,9 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
         }
       }
     }
+    // the next tile's first column line, while this tile's outcome and
+    // drains run (its offsets were loaded at the top of this iteration)
+    if (F32 && more && tile_n * 32 + lane < p.n) prefetch_l1(p.col + nxt.lo);
     tile_outcome<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, (uint32_t)tile, (uint32_t)n, valid, in.s, in.age, pressure, qn, lmax,
                                          mask_nxt, inf_nxt);
   }
@@ -1393,6 +1413,7 @@ template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, in
 __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
   step_incr_body<ST, AT, MAT, MEMO, HUBS, UNI, BLOCK>(p, blockIdx.x, gridDim.x);
 }
+
 
 // Ensemble launch (fs_ensemble, DESIGN.md §8 row 2): one step of every member
 // engine in one grid.  Member m owns CTAs [m * ctas_per, (m + 1) * ctas_per)
