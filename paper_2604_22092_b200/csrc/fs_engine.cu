@@ -883,13 +883,14 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     }
     e->fmask = finite;
   }
-  // EDGE_MERGE (scale-free graphs), f32 gather with the mask: ONE launch —
-  // the grid's warps first fold the hub rows (in-degree > kWide), heaviest
-  // first, round robin, then sweep the tiles, reading the hubs' results
-  // (S_HYBRID).  Count gather without incremental counts:
-  // the edge-chunked merge gather kernel, then the step (2 launches).
-  e->merge = c->strategy == FS_MERGE && g->num_edges > 0 && !e->incr && (!e->fmask || getenv("FS_MERGE_UNFUSED"));
-  if (c->strategy == FS_MERGE && !e->merge && !e->count_mode) e->strat = S_HYBRID;
+  // EDGE_MERGE (scale-free graphs), the f32 gather with the mask or the count
+  // gather: ONE launch — the grid's warps first fold / count the hub rows
+  // (in-degree > kWide), heaviest first, round robin, then sweep the tiles,
+  // reading the hubs' results (S_HYBRID).  f32 with
+  // non-finite weights (or FS_MERGE_UNFUSED): the edge-chunked merge gather
+  // kernel, then the step (2 launches).
+  e->merge = c->strategy == FS_MERGE && g->num_edges > 0 && !e->incr && ((!e->fmask && !e->count_mode) || getenv("FS_MERGE_UNFUSED"));
+  if (c->strategy == FS_MERGE && !e->merge && !e->incr && g->num_edges > 0) e->strat = S_HYBRID;
   if (e->merge) e->fmask = false;
   if (e->incr) e->gather = G_INCR;
   else if (e->merge) e->gather = G_PRE;
@@ -903,7 +904,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   e->step_smem = (e->gather == G_COUNT_SMEM || e->gather == G_F32M_SMEM) ? (size_t)((e->ntiles_mask + 3) & ~3LL) * 4 : 0;
   if (e->gather == G_F32M_SMEM && e->strat == S_HYBRID)
     e->step_smem += (size_t)(e->step_block / 32) * kHubPass * sizeof(float);  // the hub fold stages behind the mask
-  if (e->strat == S_HYBRID && e->fmask) TRY(build_hub_list(e));
+  if (e->strat == S_HYBRID) TRY(build_hub_list(e));
   int occ = 1;
   for (int mat = 0; mat < 2; ++mat) {
     if (e->step_smem > 0)

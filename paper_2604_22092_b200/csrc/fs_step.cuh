@@ -475,6 +475,7 @@ __device__ __forceinline__ float fold_thread_masked(const int32_t* __restrict__ 
 // CSR order, while the next pass's loads are in flight.  Every lane returns
 // the sum.
 constexpr int kHubPass = 256;
+constexpr int kFoldStage = kHubPass;  // per-warp stage of the hub fold (floats)
 template <typename IT, bool SMEM_MASK>
 __device__ __forceinline__ float fold_hub_masked(const int32_t* __restrict__ col, const uint32_t* m, const void* inf,
                                                  const void* w, int w_bf16, int w_uniform, float w_val, int64_t lo,
@@ -527,6 +528,27 @@ __device__ __forceinline__ float fold_hub_masked(const int32_t* __restrict__ col
   return __shfl_sync(0xffffffffu, acc, 0);
 }
 
+// infectious in-neighbours of one hub row, counted by the whole warp: passes
+// of 8 x 32 coalesced column loads and mask tests (every lane returns the total)
+template <bool SMEM_MASK>
+__device__ __forceinline__ int count_hub(const int32_t* __restrict__ col, const uint32_t* m, int64_t lo, int64_t hi,
+                                         int lane, uint64_t col_pol) {
+  int cnt = 0;
+  for (int64_t base = lo; base < hi; base += kHubPass) {
+    uint32_t c[8], word[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t e = base + 32 * u + lane;
+      c[u] = e < hi ? (uint32_t)ldg_hint(col + e, col_pol) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) word[u] = SMEM_MASK ? m[c[u] >> 5] : ldg_hint(m + (c[u] >> 5), l2_policy_last());
+#pragma unroll
+    for (int u = 0; u < 8; ++u) cnt += (base + 32 * u + lane < hi) ? (int)((word[u] >> (c[u] & 31)) & 1u) : 0;
+  }
+  return __reduce_add_sync(0xffffffffu, cnt);
+}
+
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -555,67 +577,6 @@ __device__ __forceinline__ float fold_warp(const int32_t* __restrict__ col, cons
     for (int l = 0; l < live; ++l) acc = __fadd_rn(acc, __shfl_sync(kFull, v, l));
   }
   return acc;
-}
-
-// warp-cooperative fold of one long slice (a hub) in CSR order, exact: the
-// lanes gather 4 x 32 contributions at a time into a per-warp shared-memory
-// stage, and lane 0 adds them in order — one f32 add chain, as the reference's
-// sequential fold (renewal.py:60-68) — while the next 128 contributions are
-// already in flight.
-constexpr int kFoldStage = 128;
-// FM: nonzero-infectivity mask prefilter (mask `m`, in shared memory when SM):
-// only set columns are gathered, and a stage without one is not folded.
-template <typename IT, bool FM = false, bool SM = false>
-__device__ __forceinline__ float fold_warp_staged(const int32_t* __restrict__ col, const void* inf, const void* w,
-                                                  int w_bf16, int w_uniform, float w_val, int64_t lo, int64_t hi,
-                                                  int lane, float* stage, const uint32_t* m = nullptr) {
-  constexpr int R = kFoldStage / 32;
-  float acc = 0.0f;
-  float v[R];
-  auto gather = [&](int64_t base) {
-    int32_t c[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int64_t e = base + 32 * r + lane;
-      c[r] = e < hi ? __ldg(col + e) : 0;
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int64_t e = base + 32 * r + lane;
-      v[r] = 0.0f;
-      if (e < hi && (!FM || mask_bit<SM>(m, c[r])))
-        v[r] = __fmul_rn(load_inf<IT>(inf, c[r]), w_uniform ? w_val : load_w(w, w_bf16, e));
-    }
-  };
-  gather(lo);
-  for (int64_t base = lo; base < hi; base += kFoldStage) {
-    __syncwarp();
-    bool any = !FM;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      stage[32 * r + lane] = v[r];
-      if (FM) any |= v[r] != 0.0f;
-    }
-    if (FM) any = __any_sync(kFull, any);  // skipped stages hold only +-0: the chain is unchanged
-    __syncwarp();
-    if (base + kFoldStage < hi) gather(base + kFoldStage);  // in flight during the chain below
-    if (lane == 0 && any) {
-      const int64_t rem = hi - base;
-      const int live = rem < kFoldStage ? (int)rem : kFoldStage;
-      if (live == kFoldStage) {
-        const float4* s4 = reinterpret_cast<const float4*>(stage);
-#pragma unroll
-        for (int q = 0; q < kFoldStage / 4; ++q) {
-          const float4 x = s4[q];
-          acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, x.x), x.y), x.z), x.w);
-        }
-      } else {
-        for (int l = 0; l < live; ++l) acc = __fadd_rn(acc, stage[l]);
-      }
-    }
-  }
-  __syncwarp();
-  return __shfl_sync(kFull, acc, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1064,8 +1025,8 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   constexpr bool SMASK = (GATHER == G_COUNT_SMEM || GATHER == G_F32M_SMEM);   // mask staged in shared memory
   // hub fold stages: static, or behind the staged mask in dynamic shared
   // memory (a 1024-thread CTA's static tables would pass 48 KB)
-  constexpr int kStage = FMASK ? kHubPass : kFoldStage;  // per-warp hub stage
-  __shared__ __align__(16) float s_fold_static[(STRAT == S_HYBRID && !SMASK) ? WARPS * kStage : 4];
+  constexpr int kStage = kFoldStage;  // per-warp hub fold stage
+  __shared__ __align__(16) float s_fold_static[(STRAT == S_HYBRID && FMASK && !SMASK) ? WARPS * kStage : 4];
   float* const s_fold = (STRAT == S_HYBRID && SMASK)
                             ? reinterpret_cast<float*>(s_mask + ((p.ntiles_mask + 3) & ~3LL))
                             : s_fold_static;
@@ -1090,7 +1051,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
   float lmax = 0.0f;
   int qn = 0;  // queued entries of this warp (warp-uniform)
   const uint32_t hub_tag = (uint32_t)k.step + 1u;
-  if (STRAT == S_HYBRID && FMASK) {
+  if (STRAT == S_HYBRID) {
     // fused edge-merge: the hubs first, heaviest first, round robin over every
     // warp of the grid (all CTAs are resident: grid <= SMs x occupancy), so no
     // warp folds more than its share of hub edges; the tile sweep below reads
@@ -1106,8 +1067,14 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
       if (hs != k.edge_from && !MAT) continue;  // only S nodes' pressure is used (all of them materialised)
       const int64_t lo = p.ro32 ? (int64_t)__ldg(p.ro32 + hn) : __ldg(p.ro + hn);
       const int64_t hi = p.ro32 ? (int64_t)__ldg(p.ro32 + hn + 1) : __ldg(p.ro + hn + 1);
-      const float pr = fold_hub_masked<IT, SMASK>(p.col, gmask, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lo, hi,
-                                                  lane, s_fold + warp * kStage, pol);
+      float pr;
+      if (COUNT) {
+        const int kk = count_hub<SMASK>(p.col, gmask, lo, hi, lane, pol);
+        pr = p.ptab_mul ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
+      } else {
+        pr = fold_hub_masked<IT, SMASK>(p.col, gmask, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lo, hi, lane,
+                                        s_fold + warp * kStage, pol);
+      }
       if (lane == 0) {
         p.hub_pre[hn] = pr;
         st_release_u32(p.hub_flag + hn, hub_tag);
@@ -1188,31 +1155,21 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
                                                             l2_policy_stream(p.stream_evict_first));
           if (need) pressure = p.ptab_mul ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
         }
-      } else if (STRAT == S_HYBRID && FMASK) {  // fused edge-merge: hubs from the pre-pass
+      } else if (STRAT == S_HYBRID) {  // fused edge-merge: hubs from the pre-pass
         const bool wide = need && (in.hi - in.lo > kWide);
         if (need && !wide) {
-          pressure = fold_thread_masked<IT, SMASK>(p.col, gmask, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo,
-                                                   in.hi);
+          if (COUNT) {
+            const int kk = count_thread<SMASK>(p.col, gmask, in.lo, in.hi);
+            pressure = p.ptab_mul ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
+          } else {
+            pressure = fold_thread_masked<IT, SMASK>(p.col, gmask, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo,
+                                                     in.hi);
+          }
         }
         if (wide) {
           while (ld_acquire_u32(p.hub_flag + n) != hub_tag) {
           }
           pressure = __ldcg(p.hub_pre + n);
-        }
-      } else if (STRAT == S_HYBRID) {  // f32 fold: thread per short slice, warp per hub
-        const bool wide = need && (in.hi - in.lo > kWide);
-        if (need && !wide)
-          pressure = FMASK ? fold_thread_masked<IT, SMASK>(p.col, gmask, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val,
-                                                           in.lo, in.hi)
-                           : fold_thread<IT>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, in.lo, in.hi);
-        unsigned rest = __ballot_sync(kFull, wide);
-        while (rest) {
-          const int j = __ffs(rest) - 1;
-          rest &= rest - 1;
-          const int64_t lj = __shfl_sync(kFull, in.lo, j), hj = __shfl_sync(kFull, in.hi, j);
-          const float pj = fold_warp_staged<IT, FMASK, SMASK>(p.col, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lj,
-                                                              hj, lane, s_fold + warp * kFoldStage, gmask);
-          if (lane == j) pressure = pj;
         }
       } else {  // warp per node (LANE strategy)
         unsigned rest = todo;

@@ -13,10 +13,12 @@ StepFn pick_step2(int gather, int strat, int& block) {
   switch (gather) {
     case G_COUNT_SMEM:
       block = 1024;
+      if (strat == S_HYBRID) return k_step<ST, AT, IT, G_COUNT_SMEM, S_HYBRID, MAT, 1024>;
       return strat == S_WARP ? k_step<ST, AT, IT, G_COUNT_SMEM, S_WARP, MAT, 1024>
                              : k_step<ST, AT, IT, G_COUNT_SMEM, S_THREAD, MAT, 1024>;
     case G_COUNT_GLOBAL:
       block = 512;
+      if (strat == S_HYBRID) return k_step<ST, AT, IT, G_COUNT_GLOBAL, S_HYBRID, MAT, 512>;
       return strat == S_WARP ? k_step<ST, AT, IT, G_COUNT_GLOBAL, S_WARP, MAT, 512>
                              : k_step<ST, AT, IT, G_COUNT_GLOBAL, S_THREAD, MAT, 512>;
     case G_INCR:
@@ -24,7 +26,6 @@ StepFn pick_step2(int gather, int strat, int& block) {
       return k_step<ST, AT, IT, G_INCR, S_THREAD, MAT, 512>;
     case G_F32:
       block = 512;
-      if (strat == S_HYBRID) return k_step<ST, AT, IT, G_F32, S_HYBRID, MAT, 512>;
       return strat == S_WARP ? k_step<ST, AT, IT, G_F32, S_WARP, MAT, 512>
                              : k_step<ST, AT, IT, G_F32, S_THREAD, MAT, 512>;
     case G_F32M_SMEM:  // the mask in shared memory: one CTA per SM

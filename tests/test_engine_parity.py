@@ -162,12 +162,17 @@ def test_variants_are_result_neutral(name, overrides):
     {"gather": "f32", "strategy": Strategy.EDGE_MERGE, "edges_per_block": 64},
     {"gather": "f32", "strategy": Strategy.PER_NODE},             # thread-per-node fold, mask prefilter
     {"gather": "f32", "strategy": Strategy.EDGE_MERGE, "compaction": True},
+    {"gather": "count", "strategy": Strategy.EDGE_MERGE},         # one-launch edge-merge, count gather
+    {"gather": "count", "strategy": Strategy.EDGE_MERGE, "compaction": True},
 ])
 @pytest.mark.parametrize("name", ["ba_merge", "shed_hazard", "weighted", "c1_mixed"])
-def test_f32_gather_forms_bit_exact(name, overrides, env, monkeypatch):
-    """Every form of the f32 CSR fold — with and without the nonzero-
-    infectivity mask, the one-launch edge-merge and the two-launch one —
-    against the reference goldens, stepwise and graph-replayed."""
+def test_gather_forms_bit_exact(name, overrides, env, monkeypatch):
+    """Every form of the CSR gather — the f32 fold with and without the
+    nonzero-infectivity mask, the count gather, the one-launch edge-merge and
+    the two-launch one — against the reference goldens, stepwise and
+    graph-replayed."""
+    if overrides["gather"] == "count" and name in ("shed_hazard", "weighted"):
+        pytest.skip("the count gather needs constant transmission and uniform weights")
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     st, log, cps, ref = run_engine_case(name, overrides=overrides)
