@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 4
+#define FS_ABI_VERSION 5
 #define FS_MAX_COMPARTMENTS 16
 
 /* error codes */
@@ -216,6 +216,20 @@ int fs_engines_exchange_local(fs_engine* const* engines, int32_t count, void* st
  * the other engines' pointers directly (one device) or peer mappings from
  * fs_ipc_open_handle (one process per GPU). */
 int fs_engine_delta_buffers(fs_engine* e, void** out2);
+/* Bulk exchange of the pushes to other ranks: each warp
+ * stages them in shared memory per owner and writes them, after each drain,
+ * into the owner's mailbox with one remote cursor atomic per owner and
+ * coalesced peer stores (instead of one NVLink atomic per push); after the
+ * step's exchange every rank folds its mailbox into its pending deltas.
+ * fs_engine_mailbox exposes this rank's mailbox (2 x world x (32 + cap)
+ * words, for CUDA IPC export); fs_engine_set_peer_mailboxes(ptrs[world])
+ * turns the mode on (ptrs[rank] = own mailbox; FS_NO_BULK keeps the direct
+ * atomics).  Engines stepped with a communicator, or through
+ * fs_engines_exchange_local, apply their mailbox automatically; with a
+ * host-side exchange call fs_engine_apply_mailbox after it. */
+int fs_engine_mailbox(fs_engine* e, void** out, int64_t* words);
+int fs_engine_set_peer_mailboxes(fs_engine* e, void* const* ptrs);
+int fs_engine_apply_mailbox(fs_engine* e, void* stream);
 /* host-side step exchange (partitioned engines without a communicator): the
  * last step's accumulator — 16 count deltas and the max-rate bits, 17 u64 —
  * out to the host and, reduced over ranks, back before the next step */

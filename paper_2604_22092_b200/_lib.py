@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import FlashSpreadNativeError, InvalidConfigError, ReconfigureAfterStartError
 
 MAX_COMPARTMENTS = 16
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 # enum fs_dtype
 I8, I32, I64, F16, BF16, F32, F64, U32, U64 = 1, 2, 3, 4, 5, 6, 7, 8, 9
@@ -165,6 +165,9 @@ _SIGNATURES = {
     "fs_engine_reset_age_memo": (_c_i32, [_vp, _vp]),
     "fs_engine_states_edited": (_c_i32, [_vp, _vp]),
     "fs_engine_set_peer_deltas": (_c_i32, [_vp, _vp]),
+    "fs_engine_mailbox": (_c_i32, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_c_i64)]),
+    "fs_engine_set_peer_mailboxes": (_c_i32, [_vp, _vp]),
+    "fs_engine_apply_mailbox": (_c_i32, [_vp, _vp]),
     "fs_ipc_get_handle": (_c_i32, [_vp, _vp, _c_i32]),
     "fs_ipc_open_handle": (_c_i32, [_vp, _c_i32, ctypes.POINTER(_vp)]),
     "fs_ipc_close": (_c_i32, [_vp]),

@@ -279,6 +279,34 @@ __global__ void k_exchange_local(AccPtrs ptrs, int count, int slot) {
   }
 }
 
+// bulk exchange, owner side: after the step's exchange (every rank's step —
+// hence every mailbox write — complete), fold the entries the senders left
+// in this rank's mailbox [par][sender] into the pending deltas of that parity;
+// the last CTA of each sender resets its cursor for the step after next
+__global__ void k_apply_mailbox(uint32_t* __restrict__ mbox, int par, int world, int rank, int64_t cap,
+                                uint32_t* __restrict__ pend, unsigned* __restrict__ ticket) {
+  const int s = blockIdx.y;
+  if (s == rank) return;  // the whole block: nothing is ever staged to oneself
+  uint32_t* hdr = mbox + ((size_t)par * world + s) * (size_t)(kMboxHdr + cap);
+  const int64_t n = min((int64_t)__ldcg(hdr), cap);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = __ldcg(hdr + kMboxHdr + i);
+    const uint32_t jl = v >> 1;
+    const uint32_t one = 1u << (16 * (jl & 1));
+    if (v & 1u) atomicAdd(pend + (jl >> 1), one);
+    else atomicSub(pend + (jl >> 1), one);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ticket + s, 1u) == gridDim.x - 1) {
+      hdr[0] = 0u;
+      ticket[s] = 0u;
+      __threadfence();
+    }
+  }
+}
+
 // widest 16-byte-aligned column span of any 32-node tile (TMA slot size)
 __global__ void k_max_tile_span(const int32_t* __restrict__ ro32, int64_t n, int64_t ntiles, unsigned long long* out) {
   unsigned long long best = 0;
@@ -384,6 +412,15 @@ struct fs_engine {
   bool incr = false;
   uint32_t* peer_pend[2][FS_MAX_PARTITIONS] = {};  // partitioned incremental: every rank's delta arrays
   bool peers_linked = false;
+  // bulk exchange: this rank's mailbox [2 parity][world sender]
+  // x (kMboxHdr + mbox_cap) words, every rank's mailbox, the apply tickets
+  uint32_t* mbox = nullptr;
+  int64_t mbox_cap = 0;
+  uint32_t* peer_mbox[FS_MAX_PARTITIONS] = {};
+  unsigned* mbox_ticket = nullptr;
+  bool bulk = false;
+  int stage_cap = 0;
+  size_t stream_smem = 0;
   bool stream = false;         // k_step_incr fast path of the incremental mode
   StepFn stream_fn[2] = {nullptr, nullptr};
   bool stream_memo = false, stream_hubs = false;  // k_step_incr variant flags
@@ -494,6 +531,11 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.hubs = e->g.d_max > 32 ? 1 : 0;  // local rows; partitioned rows of a symmetric graph mirror the degrees
   for (int r = 0; r <= FS_MAX_PARTITIONS; ++r) p.part_bound[r] = e->part_bound[r];
   p.remote_log = (e->incr && e->world > 1) ? e->remote_log : nullptr;
+  for (int r = 0; r < FS_MAX_PARTITIONS; ++r) p.peer_mbox[r] = e->peer_mbox[r];
+  p.mbox_cap = e->mbox_cap;
+  p.bulk = e->bulk ? 1 : 0;
+  p.stage_cap = e->stage_cap;
+  p.rank = e->rank;
   for (int par = 0; par < 2; ++par)
     for (int r = 0; r < FS_MAX_PARTITIONS; ++r) p.peer_pend[par][r] = e->peer_pend[par][r];
   p.dbg = e->dbg;
@@ -536,6 +578,17 @@ MergeParams make_merge_params(const fs_engine* e) {
   return q;
 }
 
+// the mailbox entries of the step just run (h_step, before the host mirror
+// advances) into this rank's pending deltas of the next parity
+int apply_mailbox(fs_engine* e, cudaStream_t st) {
+  const int par = (int)((e->h_step & 1) ^ 1);
+  const int bx = std::max(1, std::min(64, 2 * e->sms / std::max(1, e->world)));
+  k_apply_mailbox<<<dim3(bx, e->world), 256, 0, st>>>(e->mbox, par, e->world, e->rank, e->mbox_cap, e->delta[par],
+                                                      e->mbox_ticket);
+  FS_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_active, cudaStream_t st) {
   if (e->incr && e->world > 1 && !e->peers_linked)
     return set_error(FS_ESTATE, "partitioned incremental engine: link the ranks' delta buffers first");
@@ -550,7 +603,7 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(e->stream_grid);
       cfg.blockDim = dim3(512);
-      cfg.dynamicSmemBytes = 0;
+      cfg.dynamicSmemBytes = e->bulk ? e->stream_smem : 0;  // the warps' push staging
       cfg.stream = st;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -588,6 +641,10 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
       const int rc = fs_exchange_step(e->comm, &e->acc[slot].d[0], &e->acc[slot].max_bits, e->incr ? nullptr : mask_nxt,
                                       e->mask_seg_words, e->rank, st);
       if (rc) return rc;
+      if (e->bulk) {
+        const int rc2 = apply_mailbox(e, st);
+        if (rc2) return rc2;
+      }
     }
     ++e->h_step;
   }
@@ -682,7 +739,8 @@ int sync_s_ages(fs_engine* e, cudaStream_t st) {
 // nodes-per-lane form — 64-node tiles, vector loads, SIMD halfword count
 // folds — measured slower: C2 -3.5 %, C4 -10 %.)
 void set_stream_fns(fs_engine* e, bool uni) {
-  for (int mat = 0; mat < 2; ++mat) e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, e->stream_memo, e->stream_hubs, uni);
+  for (int mat = 0; mat < 2; ++mat)
+    e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, e->stream_memo, e->stream_hubs, uni, e->world > 1);
 }
 
 // (re)decide the uniform-S-age mode from the ages array (engine creation,
@@ -1031,6 +1089,20 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     e->delta_ipc = e->world > 1 || part != nullptr;  // peers map these over CUDA IPC
     TRY(dalloc(&e->delta[0], cap / 2, e->delta_ipc));
     TRY(dalloc(&e->delta[1], cap / 2, e->delta_ipc));
+    if (e->world > 1) {
+      // bulk exchange: mailbox entries per sender and parity ~2 per local node
+      // (clamped), exported over CUDA IPC like the delta buffers; used once
+      // every rank's mailbox is linked (fs_engine_set_peer_mailboxes)
+      const char* mc = getenv("FS_MBOX_CAP");
+      e->mbox_cap = mc ? std::max<int64_t>(1, atoll(mc)) : std::max<int64_t>(65536, std::min<int64_t>(2 * n, 1 << 24));
+      const size_t words = (size_t)2 * e->world * (size_t)(kMboxHdr + e->mbox_cap);
+      TRY(dalloc(&e->mbox, words, true));
+      FS_CUDA(cudaMemset(e->mbox, 0, words * sizeof(uint32_t)));
+      TRY(dalloc(&e->mbox_ticket, (size_t)e->world));
+      FS_CUDA(cudaMemset(e->mbox_ticket, 0, sizeof(unsigned) * e->world));
+      e->stage_cap = std::max(16, 512 / e->world - 1);  // 512 words of staging per warp
+      e->stream_smem = (size_t)(512 / 32) * e->world * (e->stage_cap + 1) * sizeof(uint32_t);
+    }
     TRY(recount(e, scal->step, nullptr));
     // streaming kernel: per-node arrays readable to a multiple of 128 nodes
     if (buf->padded >= 2 && !getenv("FS_NO_STREAM")) {
@@ -1125,8 +1197,9 @@ void fs_engine_destroy(fs_engine* e) {
   void* ptrs[] = {e->dstate, e->acc, e->log_clock, e->log_tau, e->log_counts, e->ptab,
                   e->active_tiles, e->num_active, e->chunk_first, e->pre, e->bad_flag,
                   e->cnt, e->entry, e->ctab, e->cage, e->dbg, e->uni_range, e->remote_log,
-                  e->hub_list, e->hub_pre, e->hub_flag};
+                  e->hub_list, e->hub_pre, e->hub_flag, e->mbox_ticket};
   for (void* q : ptrs) if (q) cudaFreeAsync(q, (cudaStream_t)0);
+  if (e->mbox) cudaFree(e->mbox);
   for (void* q : {(void*)e->delta[0], (void*)e->delta[1]})
     if (q) {
       if (e->delta_ipc) cudaFree(q);
@@ -1559,7 +1632,46 @@ int fs_engines_exchange_local(fs_engine* const* engines, int32_t count, void* st
   FS_CUDA(cudaSetDevice(engines[0]->device));
   k_exchange_local<<<1, 32, 0, (cudaStream_t)stream>>>(ptrs, count, (int)((h - 1) % 3));
   FS_CUDA(cudaGetLastError());
+  for (int r = 0; r < count; ++r)  // the bulk exchange's mailboxes (h_step already advanced: step h-1 ran)
+    if (engines[r]->bulk) {
+      engines[r]->h_step -= 1;
+      const int rc = apply_mailbox(engines[r], (cudaStream_t)stream);
+      engines[r]->h_step += 1;
+      if (rc) return rc;
+    }
   return 0;
+}
+
+int fs_engine_mailbox(fs_engine* e, void** out, int64_t* words) {
+  if (!e || !out) return set_error(FS_EINVAL, "null argument");
+  if (!e->mbox) return set_error(FS_EINVAL, "engine has no mailbox (node-partitioned incremental engines only)");
+  *out = e->mbox;
+  if (words) *words = (int64_t)2 * e->world * (kMboxHdr + e->mbox_cap);
+  return 0;
+}
+
+int fs_engine_set_peer_mailboxes(fs_engine* e, void* const* ptrs) {
+  if (!e || !ptrs) return set_error(FS_EINVAL, "null argument");
+  if (!e->mbox) return set_error(FS_EINVAL, "engine has no mailbox (node-partitioned incremental engines only)");
+  if (ptrs[e->rank] != e->mbox) return set_error(FS_EINVAL, "ptrs[rank] must be this engine's own mailbox");
+  for (int r = 0; r < e->world; ++r) {
+    if (!ptrs[r]) return set_error(FS_EINVAL, "mailbox of rank %d missing", r);
+    e->peer_mbox[r] = (uint32_t*)ptrs[r];
+  }
+  e->bulk = !getenv("FS_NO_BULK");
+  drop_batch_graphs(e);  // captured launches bake the exchange in
+  return 0;
+}
+
+int fs_engine_apply_mailbox(fs_engine* e, void* stream) {
+  if (!e) return set_error(FS_EINVAL, "null engine");
+  if (!e->bulk) return 0;
+  if (e->h_step < 1) return set_error(FS_ESTATE, "no step to apply");
+  FS_CUDA(cudaSetDevice(e->device));
+  e->h_step -= 1;  // the step that ran
+  const int rc = apply_mailbox(e, (cudaStream_t)stream);
+  e->h_step += 1;
+  return rc;
 }
 
 }  // extern "C"

@@ -111,6 +111,15 @@ struct StepParams {
   int64_t part_bound[FS_MAX_PARTITIONS + 1];  // node range boundaries of the ranks
   uint32_t* remote_log;          // partitioned: per-step count of pushes sent to other ranks (log ring)
   uint32_t* peer_pend[2][FS_MAX_PARTITIONS];  // every rank's pending-delta arrays, by parity
+  // bulk (mailbox) exchange of remote pushes: every rank's
+  // mailbox, [parity][sender] regions of kMboxHdr + mbox_cap words; pushes to
+  // other ranks are staged per warp in shared memory (stage_cap per owner)
+  // and written to the owner's mailbox as coalesced peer stores
+  uint32_t* peer_mbox[FS_MAX_PARTITIONS];
+  int64_t mbox_cap;
+  int bulk;
+  int stage_cap;
+  int rank;
   int stream_evict_first;        // CSR stream larger than L2: evict-first hint on column loads
   int host_parity;               // the host's mirror of (step & 1) for this launch (early loads), -1: none
   // age-cohort hazard memo: entry step of each node's
@@ -726,6 +735,15 @@ __device__ __forceinline__ float inf_value(const StepParams& p, const StepConst&
 // Results are bit-identical with or without the table.  The preparation runs
 // in lane 31 of each warp's final drain (drain_entries, argument `prep`).
 
+constexpr int kMboxHdr = 32;  // words before a sender's mailbox entries (word 0: the cursor)
+// a warp's staging of remote pushes in shared memory: world counters, then
+// world segments of `cap` entries ((owner-local id << 1) | up)
+struct MboxStage {
+  uint32_t* e;
+  int* n;
+  int cap;
+};
+
 // incremental counts: +-1 on node j's pending delta (buffer `nxt`), in this
 // device's memory or, node-partitioned, the owner's — possibly a peer GPU's
 // over NVLink.  Chunk boundaries are even, so the 16-bit lane
@@ -748,11 +766,67 @@ __device__ __forceinline__ int push_delta(const StepParams& p, int nxt, int32_t 
   return remote;
 }
 
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false>
+// partitioned form with the bulk exchange: a push to another rank is staged
+// in the warp's shared-memory segment of its owner (flushed by
+// flush_stage); a full segment falls back to the direct peer atomic
+__device__ __forceinline__ int push_delta_staged(const StepParams& p, int nxt, int32_t j, bool up, const MboxStage& sg) {
+  int owner = 0;
+  for (int r = 1; r < p.world; ++r) owner += (int64_t)j >= p.part_bound[r];
+  const uint32_t jl = (uint32_t)((int64_t)j - p.part_bound[owner]);
+  if (owner != p.rank) {
+    const int at = atomicAdd(sg.n + owner, 1);
+    if (at < sg.cap) {
+      sg.e[owner * sg.cap + at] = (jl << 1) | (up ? 1u : 0u);
+      return 1;
+    }
+  }
+  uint32_t* dn = p.peer_pend[nxt][owner] + (jl >> 1);
+  const uint32_t one = 1u << (16 * (jl & 1));
+  if (up) atomicAdd(dn, one);
+  else atomicSub(dn, one);
+  return owner != p.rank;
+}
+
+// the warp's staged pushes to their owners' mailboxes (region [nxt][this
+// rank]): one remote cursor atomic per owner, then coalesced peer stores;
+// entries past the mailbox's capacity go as direct peer atomics.  The owner
+// applies them after the step's exchange (k_apply_mailbox).  Warp-converged.
+__device__ __forceinline__ void flush_stage(const StepParams& p, int nxt, const MboxStage& sg, int lane) {
+  __syncwarp();
+  for (int o = 0; o < p.world; ++o) {
+    const int cnt = min(sg.n[o], sg.cap);
+    if (cnt == 0) continue;
+    uint32_t* hdr = p.peer_mbox[o] + ((size_t)nxt * p.world + p.rank) * (size_t)(kMboxHdr + p.mbox_cap);
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(hdr, (unsigned)cnt);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int i = lane; i < cnt; i += 32) {
+      const uint32_t v = sg.e[o * sg.cap + i];
+      const unsigned long long slot = base + (unsigned long long)i;
+      if (slot < (unsigned long long)p.mbox_cap) {
+        hdr[kMboxHdr + slot] = v;
+      } else {
+        const uint32_t jl = v >> 1;
+        uint32_t* dn = p.peer_pend[nxt][o] + (jl >> 1);
+        const uint32_t one = 1u << (16 * (jl & 1));
+        if (v & 1u) atomicAdd(dn, one);
+        else atomicSub(dn, one);
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < p.world) sg.n[lane] = 0;
+  __syncwarp();
+}
+
+// PART: node-partitioned engine (pushes may go to other ranks; `sg.e` set:
+// staged for the bulk exchange); false compiles the multi-rank code out
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false, bool PART = true>
 __device__ __forceinline__ void drain_entries(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh,
                                               const int* qn_node, const int* qn_state, const float* qn_age,
                                               const float* qn_press, int lane, int cnt, float& lmax,
-                                              uint32_t* mask_nxt, IT* inf_nxt, int prep = -1) {
+                                              uint32_t* mask_nxt, IT* inf_nxt, int prep = -1,
+                                              MboxStage sg = MboxStage{nullptr, nullptr, 0}) {
   __syncwarp();
   const bool ok = lane < cnt;
   int push = 0;  // +1 / -1: this node's infectious status changed
@@ -876,6 +950,15 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
     }
     const bool wide = HUBS && p.hubs && push && (e1 - e0 > 32);
     int remote = 0;  // pushes this lane sent to other ranks (partitioned runs)
+    auto push1 = [&](int32_t j, bool up) -> int {
+      if (!PART) {  // one partition: straight into the local pending delta
+        const uint32_t one = 1u << (16 * (j & 1));
+        if (up) atomicAdd(p.pend[nxt] + (j >> 1), one);
+        else atomicSub(p.pend[nxt] + (j >> 1), one);
+        return 0;
+      }
+      return sg.e ? push_delta_staged(p, nxt, j, up, sg) : push_delta(p, nxt, j, up);
+    };
     // column loads are batched ahead of their atomics: a load-then-push loop
     // would wait one memory round trip per edge (each push needs its column)
     constexpr int kPB = 8;
@@ -886,7 +969,7 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
         for (int j = 0; j < kPB; ++j) cj[j] = (b + j < e1) ? __ldg(p.out_col + b + j) : -1;
 #pragma unroll
         for (int j = 0; j < kPB; ++j)
-          if (cj[j] >= 0) remote += push_delta(p, nxt, cj[j], push > 0);
+          if (cj[j] >= 0) remote += push1(cj[j], push > 0);
       }
     }
     unsigned wides = HUBS ? __ballot_sync(kFull, wide) : 0u;
@@ -902,35 +985,38 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
         for (int j = 0; j < kHB; ++j) cj[j] = (b + 32 * j < a1) ? __ldg(p.out_col + b + 32 * j) : -1;
 #pragma unroll
         for (int j = 0; j < kHB; ++j)
-          if (cj[j] >= 0) remote += push_delta(p, nxt, cj[j], up);
+          if (cj[j] >= 0) remote += push1(cj[j], up);
       }
     }
-    if (p.remote_log) {
+    if (PART && sg.e) flush_stage(p, nxt, sg, lane);
+    if (PART && p.remote_log) {
       const int tot = __reduce_add_sync(kFull, remote);
       if (lane == 0 && tot) atomicAdd(p.remote_log + k.step % p.log_cap, (unsigned)tot);
     }
     // partitioned: the pushes into peer GPUs' memory are ordered before
     // anything this thread's rank does next — in particular before the NCCL
     // all-reduce the next step waits on — so they are visible to the owner
-    if (p.world > 1 && __any_sync(kFull, push != 0)) __threadfence_system();
+    if (PART && p.world > 1 && __any_sync(kFull, push != 0)) __threadfence_system();
   }
   __syncwarp();
 }
 
 // phase B on this warp's own queue
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false>
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false, bool PART = true>
 __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
-                                            int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
-  drain_entries<ST, AT, IT, MAT, WARPS, HUBS, UNI>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
-                                              sh.q_press[warp], lane, cnt, lmax, mask_nxt, inf_nxt);
+                                            int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt,
+                                            MboxStage sg = MboxStage{nullptr, nullptr, 0}) {
+  drain_entries<ST, AT, IT, MAT, WARPS, HUBS, UNI, PART>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
+                                                         sh.q_press[warp], lane, cnt, lmax, mask_nxt, inf_nxt, -1, sg);
 }
 
 // phase A outcome of one tile (pressure already gathered): cheap outcomes
 // now, possible transitions appended to the warp queue (drained at 32)
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false>
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false, bool PART = true>
 __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
                                              int lane, uint32_t tile, uint32_t n, bool valid, int s, float age,
-                                             float pressure, int& qn, float& lmax, uint32_t* mask_nxt, IT* inf_nxt) {
+                                             float pressure, int& qn, float& lmax, uint32_t* mask_nxt, IT* inf_nxt,
+                                             MboxStage sg = MboxStage{nullptr, nullptr, 0}) {
   const bool isS = s == k.edge_from;
   const bool term = valid && sh.term[s] != 0;
   const bool defer = valid && !term && (!isS || pressure > 0.0f);
@@ -967,7 +1053,7 @@ __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepCons
   }
   qn += __popc(dm);
   if (qn >= 32) {
-    drain_queue<ST, AT, IT, MAT, WARPS, HUBS, UNI>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt);
+    drain_queue<ST, AT, IT, MAT, WARPS, HUBS, UNI, PART>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt, sg);
     if (lane < qn - 32) {
       sh.q_node[warp][lane] = sh.q_node[warp][32 + lane];
       sh.q_state[warp][lane] = sh.q_state[warp][32 + lane];
@@ -1214,12 +1300,23 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
 #endif
 // `cta` / `nctas`: this CTA and the CTAs sharing the engine `p` (the whole
 // grid, or one member's CTAs of an ensemble launch)
-template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, int BLOCK>
+template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, int BLOCK, bool PART = false>
 __device__ __forceinline__ void step_incr_body(const StepParams& p, const uint32_t cta, const uint32_t nctas) {
   constexpr int WARPS = BLOCK / 32;
   __shared__ StepShared<WARPS> sh;
   __shared__ StepConst s_k;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // bulk exchange: this warp's staging of remote pushes (dynamic shared memory)
+  MboxStage sg{nullptr, nullptr, 0};
+  if (PART && p.bulk) {
+    extern __shared__ __align__(16) uint32_t fs_dyn[];
+    uint32_t* base = fs_dyn + (size_t)warp * p.world * (p.stage_cap + 1);
+    sg.n = reinterpret_cast<int*>(base);
+    sg.e = base + p.world;
+    sg.cap = p.stage_cap;
+    if (lane < p.world) sg.n[lane] = 0;
+    __syncwarp();
+  }
 #if FS_STEP_PROBE  // build with -DFS_STEP_PROBE=1 and run with FS_DEBUG_TIMES=1 (scripts/cta_times_incr.py)
   __shared__ unsigned long long s_entry;
   if (p.dbg && tid == 0) {
@@ -1322,8 +1419,8 @@ __device__ __forceinline__ void step_incr_body(const StepParams& p, const uint32
 #if FS_STEP_PROBE
     const int q0 = qn;
 #endif
-    tile_outcome<ST, AT, float, MAT, WARPS, HUBS, UNI>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure,
-                                                       qn, lmax, mask_nxt, nullptr);
+    tile_outcome<ST, AT, float, MAT, WARPS, HUBS, UNI, PART>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure,
+                                                             qn, lmax, mask_nxt, nullptr, sg);
 #if FS_STEP_PROBE
     pr_def += qn - q0 + (qn < q0 ? 32 : 0);
     pr_drains += qn < q0;
@@ -1335,8 +1432,9 @@ __device__ __forceinline__ void step_incr_body(const StepParams& p, const uint32
     const int gw = (int)cta * WARPS + warp;
     const int prep = (MEMO && gw < kCohortW * p.ncslots) ? gw : -1;
     if (qn > 0 || prep >= 0)
-      drain_entries<ST, AT, float, MAT, WARPS, HUBS, UNI>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
-                                                           sh.q_press[warp], lane, qn, lmax, mask_nxt, nullptr, prep);
+      drain_entries<ST, AT, float, MAT, WARPS, HUBS, UNI, PART>(p, k, sh, sh.q_node[warp], sh.q_state[warp],
+                                                                 sh.q_age[warp], sh.q_press[warp], lane, qn, lmax,
+                                                                 mask_nxt, nullptr, prep, sg);
   }
 #if FS_STEP_PROBE  // per-warp [phase end, deferred << 20 | mid-loop drains] after the per-CTA block
   if (p.dbg && lane == 0) {
@@ -1366,9 +1464,9 @@ __device__ __forceinline__ void step_incr_body(const StepParams& p, const uint32
 }
 
 
-template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, int BLOCK>
+template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, int BLOCK, bool PART = false>
 __global__ void __launch_bounds__(BLOCK, 2) k_step_incr(const StepParams p) {
-  step_incr_body<ST, AT, MAT, MEMO, HUBS, UNI, BLOCK>(p, blockIdx.x, gridDim.x);
+  step_incr_body<ST, AT, MAT, MEMO, HUBS, UNI, BLOCK, PART>(p, blockIdx.x, gridDim.x);
 }
 
 
@@ -1631,7 +1729,7 @@ using MultiFn = void (*)(const StepParams*, uint32_t);
 
 // instantiation units
 StepFn pick_step(bool mixed, int gather, int strat, bool mat, int& block);  // fs_step_general.cu
-StepFn pick_stream(bool mixed, bool mat, bool memo, bool hubs, bool uni);           // fs_step_incr.cu
+StepFn pick_stream(bool mixed, bool mat, bool memo, bool hubs, bool uni, bool part = false);  // fs_step_incr.cu
 MultiFn pick_stream_multi(bool mixed, bool mat, bool memo, bool hubs, bool uni);    // fs_step_incr.cu
 MergeFn pick_merge(bool inf_bf16, int mode, int& block);                    // fs_step_incr.cu
 TmaFn pick_tma(bool mixed, bool smem_mask, bool mat, bool ptab_mul, int block);  // fs_step_tma.cu

@@ -201,6 +201,9 @@ class _Partition:
         bufs = (ctypes.c_void_p * 2)()
         self.incremental = self.lib.fs_engine_delta_buffers(self.handle, bufs) == 0
         self.delta_buffers = (bufs[0], bufs[1]) if self.incremental else None
+        mb = ctypes.c_void_p()
+        self.mailbox = mb.value if (plan.world > 1 and self.incremental and
+                                    self.lib.fs_engine_mailbox(self.handle, ctypes.byref(mb), None) == 0) else None
 
     def link_peers(self, table) -> None:
         """table[parity][rank] = device address of that rank's delta buffer
@@ -208,6 +211,15 @@ class _Partition:
         world = len(table[0])
         arr = (ctypes.c_void_p * (2 * world))(*[table[par][r] for par in range(2) for r in range(world)])
         _lib.check(self.lib.fs_engine_set_peer_deltas(self.handle, arr))
+
+    def link_mailboxes(self, table) -> None:
+        """table[rank] = device address of that rank's mailbox: the bulk
+        exchange of remote pushes."""
+        arr = (ctypes.c_void_p * len(table))(*table)
+        _lib.check(self.lib.fs_engine_set_peer_mailboxes(self.handle, arr))
+
+    def apply_mailbox(self) -> None:
+        _lib.check(self.lib.fs_engine_apply_mailbox(self.handle, self.stream))
 
     def close(self) -> None:
         if getattr(self, "handle", None):
@@ -253,7 +265,12 @@ class LocalPartitionedRun:
     exchange done in place (shared mask buffers + fs_engines_exchange_local).
     `graph_parts[r]` holds rows plan.ranges[r] with global column ids."""
 
-    def __init__(self, graph_parts, m, cfg: RenewalConfig, seed: int, plan: PartitionPlan, seed_count=None):
+    def __init__(self, graph_parts, m, cfg: RenewalConfig, seed: int, plan: PartitionPlan, seed_count=None,
+                 exchange: str = "bulk"):
+        """exchange "bulk": pushes to other partitions staged and written to
+        their mailboxes in bulk; "atomic": one peer atomic per push."""
+        if exchange not in ("bulk", "atomic"):
+            raise ValueError("exchange must be 'bulk' or 'atomic'")
         dev = _device.device()
         self.plan, self.cfg, self.M = plan, cfg, m.num_compartments
         ids = _seed_ids(m, plan.num_nodes, seed, seed_count, dev)
@@ -265,6 +282,10 @@ class LocalPartitionedRun:
             table = [[p.delta_buffers[par] for p in self.parts] for par in range(2)]
             for p in self.parts:
                 p.link_peers(table)
+            if exchange == "bulk":
+                boxes = [p.mailbox for p in self.parts]
+                for p in self.parts:
+                    p.link_mailboxes(boxes)
         self._arr = (ctypes.c_void_p * len(self.parts))(*[p.handle.value for p in self.parts])
         self.steps = 0
 
@@ -299,7 +320,7 @@ class DistributedRun:
     torch.distributed group used once, to broadcast the NCCL unique id."""
 
     def __init__(self, graph_local, m, cfg: RenewalConfig, seed: int, plan: PartitionPlan, rank: int,
-                 seed_count=None, pg=None, transport: str = "nccl"):
+                 seed_count=None, pg=None, transport: str = "nccl", exchange: str = "bulk"):
         """transport "nccl": the per-step all-reduce is an NCCL group inside
         the engine's launches (and CUDA graphs); "host": eager steps only, the
         accumulator is all-reduced through `pg` (any torch.distributed
@@ -333,6 +354,9 @@ class DistributedRun:
         self._opened = []
         if transport == "host" and plan.world > 1 and not self.part.incremental:
             raise InvalidConfigError("the host transport needs the incremental-count mode (no mask exchange)")
+        if exchange not in ("bulk", "atomic"):
+            raise ValueError("exchange must be 'bulk' or 'atomic'")
+        self.exchange = exchange
         if plan.world > 1 and self.part.incremental:
             self._link_peers_ipc(dev, pg)
 
@@ -343,7 +367,8 @@ class DistributedRun:
 
         lib = _lib.load()
         mine = []
-        for ptr in self.part.delta_buffers:
+        bulk = self.exchange == "bulk" and self.part.mailbox is not None
+        for ptr in list(self.part.delta_buffers) + ([self.part.mailbox] if bulk else []):
             h = (ctypes.c_uint8 * 128)()
             nb = _lib.check(lib.fs_ipc_get_handle(ptr, h, 128))
             mine.append(bytes(h)[:nb])
@@ -361,6 +386,18 @@ class DistributedRun:
                 self._opened.append(out)
                 table[par][r] = out.value
         self.part.link_peers(table)
+        if bulk:  # every rank's mailbox, for the bulk exchange
+            boxes = [None] * self.plan.world
+            for r in range(self.plan.world):
+                if r == self.rank:
+                    boxes[r] = self.part.mailbox
+                    continue
+                buf = (ctypes.c_uint8 * 128).from_buffer_copy(allh[r][2].ljust(128, b"\0"))
+                out = ctypes.c_void_p()
+                _lib.check(lib.fs_ipc_open_handle(buf, dev.index, ctypes.byref(out)))
+                self._opened.append(out)
+                boxes[r] = out.value
+            self.part.link_mailboxes(boxes)
         dist.barrier(group=pg)  # every rank linked before anyone pushes
 
     def exchange_us(self, iters: int = 200) -> float | None:
@@ -403,6 +440,7 @@ class DistributedRun:
             acc[:16] = d.numpy().view(np.uint64)
             acc[16] = np.uint64(mx.item())
             _lib.check(lib.fs_engine_acc_set(self.part.handle, acc.ctypes.data, self.part.stream))
+            self.part.apply_mailbox()  # after every rank's step (the all-reduce above is the barrier)
             self.steps += 1
 
     def close(self) -> None:

@@ -107,17 +107,25 @@ def test_partitioned_oracle_matches_single_process_gloo():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,mixed", [(3, False), (2, True), (4, False)])
-def test_virtual_ranks_match_single_engine(world, mixed):
+@pytest.mark.parametrize("world,mixed,exchange,cap", [
+    (3, False, "bulk", None), (2, True, "bulk", None), (4, False, "bulk", None),
+    (3, False, "atomic", None),
+    (4, False, "bulk", "8"),  # mailboxes overflow every step: the rest goes as direct peer atomics
+])
+def test_virtual_ranks_match_single_engine(world, mixed, exchange, cap, monkeypatch):
+    """P partitions on one device, pushes to other partitions through their
+    mailboxes (bulk) or as direct peer atomics: bit-identical to one engine."""
     from paper_2604_22092_b200.distributed import LocalPartitionedRun
 
+    if cap:
+        monkeypatch.setenv("FS_MBOX_CAP", cap)
     n, k = 50_000, 10
     m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
     cfg = fs.RenewalConfig(mixed_precision=mixed)
     plan = partition_plan(n, world)
     whole = fs.gen_fixed_degree_device(n, k, seed=2)
     parts = [fs.gen_fixed_degree_device(n, k, seed=2, row_lo=lo, row_hi=hi) for lo, hi in plan.ranges]
-    run = LocalPartitionedRun(parts, m, cfg, 7, plan)
+    run = LocalPartitionedRun(parts, m, cfg, 7, plan, exchange=exchange)
     st = fs.init_renewal_state(whole, m, cfg, 7)
     for _ in range(3):
         clocks, _, counts = run.run_batch()
@@ -162,7 +170,7 @@ def test_nccl_world1_matches_single_engine():
     assert same and s1 == s2
 
 
-def _ipc_worker(rank: int, world: int, port: int, steps: int, out_q) -> None:
+def _ipc_worker(rank: int, world: int, port: int, steps: int, out_q, exchange: str = "bulk") -> None:
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
@@ -173,7 +181,7 @@ def _ipc_worker(rank: int, world: int, port: int, steps: int, out_q) -> None:
     plan = partition_plan(n, world)
     lo, hi = plan.ranges[rank]
     g = fs.gen_fixed_degree_device(n, 10, seed=2, row_lo=lo, row_hi=hi)
-    run = DistributedRun(g, m, fs.RenewalConfig(), 7, plan, rank, transport="host")
+    run = DistributedRun(g, m, fs.RenewalConfig(), 7, plan, rank, transport="host", exchange=exchange)
     assert run.part.incremental
     run.step(steps)
     s = run.part.scalars()
@@ -185,7 +193,8 @@ def _ipc_worker(rank: int, world: int, port: int, steps: int, out_q) -> None:
 
 
 @pytest.mark.gpu
-def test_two_processes_push_through_cuda_ipc():
+@pytest.mark.parametrize("exchange", ["bulk", "atomic"])
+def test_two_processes_push_through_cuda_ipc(exchange):
     """Two ranks as two processes on the one GPU: the step kernels push into
     each other's pending-delta arrays through CUDA IPC mappings (the
     multi-GPU path's transport, minus NVLink), the accumulator is all-reduced
@@ -194,7 +203,7 @@ def test_two_processes_push_through_cuda_ipc():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, steps, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict((r, rest) for r, *rest in (q.get(timeout=600) for _ in range(world)))
