@@ -62,7 +62,9 @@ __host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, uint32_t k0
   return c;
 }
 
-__device__ __forceinline__ double philox_uniform(uint64_t seed, uint64_t step, uint64_t stream) {
+// not inlined: the step kernels carry it for the rng="philox" option only, and
+// its 10 rounds' state would otherwise weigh on their register allocation
+static __device__ __noinline__ double philox_uniform(uint64_t seed, uint64_t step, uint64_t stream) {
   Philox4 c{(uint32_t)stream, (uint32_t)(stream >> 32), (uint32_t)step, (uint32_t)(step >> 32)};
   Philox4 o = philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
   uint64_t b = ((uint64_t)o.x1 << 32) | (uint64_t)o.x0;
@@ -156,14 +158,11 @@ __device__ __forceinline__ float hazard_erlang_f32(float tau, int k, float r) {
   return r * term / sum;
 }
 
-// rate of a nodal compartment at age `age` (f32 storage value), cast to the
-// f32 rate buffer exactly as renewal.py:474-480 (f64 math, f32 store)
-__device__ __forceinline__ float nodal_rate(int kind, double p0, double p1, float age, int prec) {
+// the hazards other than the f64 log-normal, out of line: a call per drain
+// where they are used, and no register pressure where they are not
+static __device__ __noinline__ float nodal_rate_other(int kind, double p0, double p1, float age, int prec) {
   switch (kind) {
-    case FS_HZ_EXPONENTIAL: return __double2float_rn(p0);
-    case FS_HZ_LOGNORMAL:
-      return prec == FS_HAZ_F64 ? __double2float_rn(hazard_lognormal_f64((double)age, p0, p1))
-                                : hazard_lognormal_f32(age, (float)p0, (float)p1);
+    case FS_HZ_LOGNORMAL: return hazard_lognormal_f32(age, (float)p0, (float)p1);
     case FS_HZ_WEIBULL:
       return prec == FS_HAZ_F64 ? __double2float_rn(hazard_weibull_f64((double)age, p0, p1))
                                 : hazard_weibull_f32(age, (float)p0, (float)p1);
@@ -172,6 +171,14 @@ __device__ __forceinline__ float nodal_rate(int kind, double p0, double p1, floa
                                 : hazard_erlang_f32(age, (int)p0, (float)p1);
     default: return 0.0f;
   }
+}
+
+// rate of a nodal compartment at age `age` (f32 storage value), cast to the
+// f32 rate buffer exactly as renewal.py:474-480 (f64 math, f32 store)
+__device__ __forceinline__ float nodal_rate(int kind, double p0, double p1, float age, int prec) {
+  if (kind == FS_HZ_EXPONENTIAL) return __double2float_rn(p0);
+  if (kind == FS_HZ_LOGNORMAL && prec == FS_HAZ_F64) return __double2float_rn(hazard_lognormal_f64((double)age, p0, p1));
+  return nodal_rate_other(kind, p0, p1, age, prec);
 }
 
 // shedding profile s(tau), hazards.py:196-218 (f64)

@@ -821,7 +821,10 @@ __device__ __forceinline__ void flush_stage(const StepParams& p, int nxt, const 
 
 // PART: node-partitioned engine (pushes may go to other ranks; `sg.e` set:
 // staged for the bulk exchange); false compiles the multi-rank code out
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false, bool PART = true>
+// CNT: a count-encoding kernel (no infectivity buffers): the f32 infectivity
+// write-back is compiled out rather than skipped at run time
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false, bool PART = true,
+          bool CNT = false>
 __device__ __forceinline__ void drain_entries(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh,
                                               const int* qn_node, const int* qn_state, const float* qn_age,
                                               const float* qn_press, int lane, int cnt, float& lmax,
@@ -922,7 +925,7 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
       if (p.entry) p.entry[n] = (int32_t)k.step;  // age cohort of the new compartment
       atomicAdd(&sh.cnt[ns], 1);
       atomicAdd(&sh.cnt[s], -1);
-      if (!k.write_inf && ((ns == k.infectious) != (s == k.infectious))) {
+      if ((CNT || !k.write_inf) && ((ns == k.infectious) != (s == k.infectious))) {
         atomicXor(mask_nxt + p.tile_base + (n >> 5), 1u << (n & 31));
         if (p.cnt) push = (ns == k.infectious) ? 1 : -1;  // incremental counts: pushes below
       }
@@ -930,7 +933,7 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
       nage = __fadd_rn(age, k.tau_f);  // queued nodes are never terminal
     }
     if (!UNI || fire || s != k.edge_from) reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
-    if (k.write_inf) {
+    if (!CNT && k.write_inf) {
       const IT iv = from_f32<IT>(inf_value(p, k, ns, nage));
       inf_nxt[n] = iv;
       // f32 mask: phase A left this (deferred) node's bit clear
@@ -1002,17 +1005,19 @@ __device__ __forceinline__ void drain_entries(const StepParams& p, const StepCon
 }
 
 // phase B on this warp's own queue
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false, bool PART = true>
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false, bool PART = true,
+          bool CNT = false>
 __device__ __forceinline__ void drain_queue(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
                                             int lane, int cnt, float& lmax, uint32_t* mask_nxt, IT* inf_nxt,
                                             MboxStage sg = MboxStage{nullptr, nullptr, 0}) {
-  drain_entries<ST, AT, IT, MAT, WARPS, HUBS, UNI, PART>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
+  drain_entries<ST, AT, IT, MAT, WARPS, HUBS, UNI, PART, CNT>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
                                                          sh.q_press[warp], lane, cnt, lmax, mask_nxt, inf_nxt, -1, sg);
 }
 
 // phase A outcome of one tile (pressure already gathered): cheap outcomes
 // now, possible transitions appended to the warp queue (drained at 32)
-template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false, bool PART = true>
+template <typename ST, typename AT, typename IT, bool MAT, int WARPS, bool HUBS = true, bool UNI = false, bool PART = true,
+          bool CNT = false>
 __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepConst& k, StepShared<WARPS>& sh, int warp,
                                              int lane, uint32_t tile, uint32_t n, bool valid, int s, float age,
                                              float pressure, int& qn, float& lmax, uint32_t* mask_nxt, IT* inf_nxt,
@@ -1024,12 +1029,12 @@ __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepCons
   if (!UNI && valid && !term && !defer) {  // S with zero pressure: rate 0, ages (UNI: the uniform scalar)
     const float nage = __fadd_rn(age, k.tau_f);
     reinterpret_cast<AT*>(p.ages)[n] = from_f32<AT>(nage);
-    if (k.write_inf) {
+    if (!CNT && k.write_inf) {
       const IT iv = from_f32<IT>(inf_value(p, k, s, nage));
       inf_nxt[n] = iv;
       nz = to_f32<IT>(iv) != 0.0f;
     }
-  } else if (term && k.write_inf) {
+  } else if (!CNT && term && k.write_inf) {
     const IT iv = from_f32<IT>(inf_value(p, k, s, age));
     inf_nxt[n] = iv;
     nz = to_f32<IT>(iv) != 0.0f;
@@ -1040,7 +1045,7 @@ __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepCons
   }
   if (k.write_mask) {
     // next-step mask word; deferred nodes are fixed up in phase B
-    const unsigned word = __ballot_sync(0xffffffffu, k.write_inf ? nz : (valid && s == k.infectious));
+    const unsigned word = __ballot_sync(0xffffffffu, (!CNT && k.write_inf) ? nz : (valid && s == k.infectious));
     if (lane == 0) mask_nxt[p.tile_base + tile] = word;
   }
   const unsigned dm = __ballot_sync(0xffffffffu, defer);
@@ -1053,7 +1058,7 @@ __device__ __forceinline__ void tile_outcome(const StepParams& p, const StepCons
   }
   qn += __popc(dm);
   if (qn >= 32) {
-    drain_queue<ST, AT, IT, MAT, WARPS, HUBS, UNI, PART>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt, sg);
+    drain_queue<ST, AT, IT, MAT, WARPS, HUBS, UNI, PART, CNT>(p, k, sh, warp, lane, 32, lmax, mask_nxt, inf_nxt, sg);
     if (lane < qn - 32) {
       sh.q_node[warp][lane] = sh.q_node[warp][32 + lane];
       sh.q_state[warp][lane] = sh.q_state[warp][32 + lane];
@@ -1419,8 +1424,8 @@ __device__ __forceinline__ void step_incr_body(const StepParams& p, const uint32
 #if FS_STEP_PROBE
     const int q0 = qn;
 #endif
-    tile_outcome<ST, AT, float, MAT, WARPS, HUBS, UNI, PART>(p, k, sh, warp, lane, t, n, valid, s, in.age, pressure,
-                                                             qn, lmax, mask_nxt, nullptr, sg);
+    tile_outcome<ST, AT, float, MAT, WARPS, HUBS, UNI, PART, true>(p, k, sh, warp, lane, t, n, valid, s, in.age,
+                                                                   pressure, qn, lmax, mask_nxt, nullptr, sg);
 #if FS_STEP_PROBE
     pr_def += qn - q0 + (qn < q0 ? 32 : 0);
     pr_drains += qn < q0;
@@ -1432,7 +1437,7 @@ __device__ __forceinline__ void step_incr_body(const StepParams& p, const uint32
     const int gw = (int)cta * WARPS + warp;
     const int prep = (MEMO && gw < kCohortW * p.ncslots) ? gw : -1;
     if (qn > 0 || prep >= 0)
-      drain_entries<ST, AT, float, MAT, WARPS, HUBS, UNI, PART>(p, k, sh, sh.q_node[warp], sh.q_state[warp],
+      drain_entries<ST, AT, float, MAT, WARPS, HUBS, UNI, PART, true>(p, k, sh, sh.q_node[warp], sh.q_state[warp],
                                                                  sh.q_age[warp], sh.q_press[warp], lane, qn, lmax,
                                                                  mask_nxt, nullptr, prep, sg);
   }
@@ -1644,11 +1649,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step_tma(const StepParams p, const
     __syncwarp();
     // the slot is consumed: refill it with tile t + slots
     if (t + L.slots < t1) issue_cols(t + L.slots, sl);
-    tile_outcome<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, (uint32_t)t, (uint32_t)n, valid, s, in.age, pressure, qn, lmax,
+    tile_outcome<ST, AT, float, MAT, WARPS, true, false, true, true>(p, k, sh, warp, lane, (uint32_t)t, (uint32_t)n, valid, s, in.age, pressure, qn, lmax,
                                             mask_nxt, nullptr);
     sl = (sl + 1 == L.slots) ? 0 : sl + 1;
   }
-  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
+  if (qn > 0) drain_queue<ST, AT, float, MAT, WARPS, true, false, true, true>(p, k, sh, warp, lane, qn, lmax, mask_nxt, nullptr);
   if (dbg && lane == 0) {
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
