@@ -20,13 +20,13 @@ if [ -z "$SKIP_BENCH" ]; then
   timeout 900 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_${TAG}_ref_c2.json 2> gpurun_out/bench_${TAG}_ref_c2.err; echo "ref rc=$?"
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_" --csv --log-file gpurun_out/launches_${TAG}_c2.csv python bench.py --steps 20 --warmup 3 --no-e2e --cpu-steps 0 > /dev/null 2>&1; echo "list rc=$?"
 fi
-for W in ${PROF:-c2 c3 c4 c2s c3f c3c ens}; do
+for W in ${PROF:-c2 c3 c4 c5 c2s c3f c3c ens}; do
   case $W in c2s|c3f) K="^k_step$";; c3c) K="^k_gather_merge$";; ens) K="^k_step_incr_multi$";; *) K="^k_step_incr$";; esac
   R=gpurun_out/prof_${TAG}_$W
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$K" -s ${SKIP:-6} -c 1 -o $R -f \
     python bench.py --workload $W --steps 10 --warmup 3 --no-e2e --cpu-steps 0 > gpurun_out/ncu_${TAG}_$W.log 2>&1; echo "ncu $W rc=$?"
   python scripts/ncu_hot.py $R.ncu-rep 40 > gpurun_out/${TAG}_${W}_ncu_hot.txt 2>&1
 done
-OUT=gpurun_out python scripts/ncu_to_summary.py $TAG ${PROF:-c2 c3 c4 c2s c3f c3c ens}
+OUT=gpurun_out python scripts/ncu_to_summary.py $TAG ${PROF:-c2 c3 c4 c5 c2s c3f c3c ens}
 rm -f gpurun_out/prof_${TAG}_*.ncu-rep
 du -sh gpurun_out
