@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 5
+#define FS_ABI_VERSION 6
 #define FS_MAX_COMPARTMENTS 16
 
 /* error codes */
@@ -153,8 +153,13 @@ typedef struct fs_state_buffers {
   float* pressure;       /* f32[N], written on materialising steps            */
   float* rates;          /* f32[N], written on materialising steps            */
   int32_t padded;        /* 1: states/ages readable to a multiple of 32 nodes,
-                            2: to a multiple of 128 nodes (streaming kernel) */
+                            2: to a multiple of 128 nodes (streaming kernel);
+                            | FS_BUF_FRESH: a fresh init_renewal_state —
+                            every age 0, infectivity beta at the infectious
+                            seeds — so the engine skips the checks that need
+                            host round trips */
 } fs_state_buffers;
+#define FS_BUF_FRESH 4
 
 /* node partition of a multi-GPU run: this
  * engine owns global nodes [node_base, node_base + g->num_nodes); its CSR
@@ -320,6 +325,13 @@ int fs_host_csr_scan(const int64_t* row_offsets, int64_t n, const float* weights
 int fs_seed_select(int64_t n, uint64_t seed_key, int64_t count, void* states, int32_t states_dtype,
                    int32_t compartment, void* inf, int32_t inf_dtype, float inf_value, uint8_t* flags,
                    void* stream);
+/* the same selection for `trials` independent trials of one small graph
+ * (N <= 4096) in one launch: trial t's states / infectivity at offset
+ * t * stride, its pick key pick_keys[t] (host array) — the ensemble's
+ * per-trial init_renewal_state (renewal.py:162-169) without host round trips */
+int fs_seed_select_batch(int64_t n, int32_t trials, const uint64_t* pick_keys, int64_t count, void* states,
+                         int64_t stride, int32_t states_dtype, int32_t compartment, void* inf, int32_t inf_dtype,
+                         float inf_value, void* stream);
 /* ids of the set flags in increasing order (sorted seed ids) */
 int fs_flags_to_ids(const uint8_t* flags, int64_t n, int64_t* out_ids, int64_t* num_out, void* stream);
 /* Is the incoming CSR its own transpose (an undirected graph, R/graph.py:

@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import FlashSpreadNativeError, InvalidConfigError, ReconfigureAfterStartError
 
 MAX_COMPARTMENTS = 16
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 # enum fs_dtype
 I8, I32, I64, F16, BF16, F32, F64, U32, U64 = 1, 2, 3, 4, 5, 6, 7, 8, 9
@@ -32,6 +32,7 @@ RNG_SPLITMIX, RNG_PHILOX = 0, 1
 HAZ_F64, HAZ_F32 = 0, 1
 
 FS_EINVAL, FS_ECUDA, FS_ENOMEM, FS_ESTATE, FS_ECONSERVE, FS_EREPR = -1, -2, -3, -4, -5, -6
+FS_BUF_FRESH = 4  # fs_state_buffers.padded flag: a fresh state
 
 _c_i32, _c_i64, _c_u64, _c_f32, _c_f64, _vp = (
     ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float, ctypes.c_double, ctypes.c_void_p,
@@ -191,6 +192,8 @@ _SIGNATURES = {
     "fs_engine_state_restored": (_c_i32, [_vp, _vp]),
     "fs_seed_select": (_c_i32, [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, _vp, ctypes.c_int32, ctypes.c_int32,
                                 _vp, ctypes.c_int32, ctypes.c_float, _vp, _vp]),
+    "fs_seed_select_batch": (_c_i32, [ctypes.c_int64, ctypes.c_int32, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
+                                      ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int32, ctypes.c_float, _vp]),
     "fs_flags_to_ids": (_c_i32, [_vp, ctypes.c_int64, _vp, ctypes.POINTER(ctypes.c_int64), _vp]),
     "fs_check_symmetric": (_c_i32, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int32),
                                     _vp]),

@@ -128,20 +128,6 @@ __global__ void k_chunk_first(const int64_t* __restrict__ ro, int64_t n, int64_t
 // ptab[k] = k-fold sequential f32 sum of c (count-gather pressure table);
 // *exact_mul = 1 when every entry equals the single product f32(k * c)
 // (e.g. beta = 0.25 with unit weights), letting the kernels skip the lookup
-__global__ void k_ptab(float* ptab, int64_t len, float c, int* exact_mul) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    float acc = 0.0f;
-    int ok = 1;
-    ptab[0] = 0.0f;
-    for (int64_t k = 1; k < len; ++k) {
-      acc = __fadd_rn(acc, c);
-      ptab[k] = acc;
-      if (acc != __fmul_rn((float)k, c)) ok = 0;
-    }
-    *exact_mul = ok;
-  }
-}
-
 // batch prologue (renewal.py:583-597): fold a pending step into the
 // scalars, then reset tau unless carry_tau
 __device__ __forceinline__ void begin_batch_one(DevState* D, StepAcc* acc, int64_t* log_counts, int64_t log_cap,
@@ -339,6 +325,7 @@ struct fs_engine {
   bool count_mode = false;
   bool mask_smem = false;
   bool fmask = false;     // f32 gather with the nonzero-infectivity mask prefilter (G_F32M_*)
+  bool fresh = false;     // built on a fresh state (FS_BUF_FRESH): its first infectivity load is trusted
   int32_t* hub_list = nullptr;  // fused edge-merge: nodes with in-degree > kWide, heaviest first
   int64_t nhubs = 0;
   float* hub_pre = nullptr;     // [N]
@@ -855,6 +842,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   e->c = *c;
   e->b = *buf;
   e->mixed = c->mixed_precision != 0;
+  e->fresh = (buf->padded & FS_BUF_FRESH) != 0;
   const int64_t n = g->num_nodes;
   e->ntiles = (n + 31) / 32;
   e->ntiles_mask = e->ntiles;
@@ -980,9 +968,20 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     TRY(dalloc(&e->ptab, e->ptab_len));
     volatile float a_ = e->inf_val, w_ = g->uniform_weight;
     const float cval = a_ * w_;  // f32(inf * w): one IEEE single multiply
-    FS_CUDA(cudaMemset(e->bad_flag, 0, sizeof(int)));
-    k_ptab<<<1, 1>>>(e->ptab, e->ptab_len, cval, e->bad_flag);
-    FS_CUDA(cudaMemcpy(&e->ptab_mul, e->bad_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    // the k-fold sequential f32 sums of c, on the host (IEEE single adds, no
+    // contraction: volatile), and whether each equals f32(k * c)
+    std::vector<float> tab((size_t)e->ptab_len);
+    volatile float acc = 0.0f;
+    int ok = 1;
+    tab[0] = 0.0f;
+    for (int64_t kk = 1; kk < e->ptab_len; ++kk) {
+      acc = acc + cval;
+      tab[(size_t)kk] = acc;
+      volatile float prod = (float)kk * cval;
+      if (acc != prod) ok = 0;
+    }
+    FS_CUDA(cudaMemcpyAsync(e->ptab, tab.data(), sizeof(float) * tab.size(), cudaMemcpyHostToDevice, (cudaStream_t)0));
+    e->ptab_mul = ok;
     e->ptab_c = cval;
   }
   {
@@ -997,7 +996,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   e->step_grid_general = e->step_grid;
   e->step_smem_general = e->step_smem;
   // streaming fast path: count gather, PER_NODE, padded buffers, int32 offsets
-  if (e->count_mode && !e->incr && c->strategy == FS_PER_NODE && !e->merge && g->row_offsets32 && g->padded && buf->padded &&
+  if (e->count_mode && !e->incr && c->strategy == FS_PER_NODE && !e->merge && g->row_offsets32 && g->padded && (buf->padded & 3) &&
       g->num_edges > 0) {
     unsigned long long* d_span = nullptr;
     TRY(dalloc(&d_span, 1));
@@ -1105,7 +1104,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     }
     TRY(recount(e, scal->step, nullptr));
     // streaming kernel: per-node arrays readable to a multiple of 128 nodes
-    if (buf->padded >= 2 && !getenv("FS_NO_STREAM")) {
+    if ((buf->padded & 3) >= 2 && !getenv("FS_NO_STREAM")) {
       e->stream = true;
       e->stream_hubs = g->d_max > 32;
       set_stream_fns(e, false);
@@ -1151,7 +1150,12 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     e->uni_ok = e->stream && !c->compaction && part == nullptr && !reenter && !getenv("FS_NO_UNI");
     if (e->uni_ok) {
       TRY(dalloc(&e->uni_range, 2));
-      TRY(recheck_uniform(e, nullptr));
+      if (buf->padded & FS_BUF_FRESH) {  // every age is 0 (a fresh state): uniform, scalar 0
+        e->s_uniform = true;
+        set_stream_fns(e, true);
+      } else {
+        TRY(recheck_uniform(e, nullptr));
+      }
     }
   }
   if (getenv("FS_DEBUG_TIMES")) {
@@ -1159,14 +1163,11 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     TRY(dalloc(&e->dbg, g * (4 + 32) * 16));  // per-CTA block, then the per-warp block of the probe build
     FS_CUDA(cudaMemset(e->dbg, 0, sizeof(unsigned long long) * g * (4 + 32) * 16));
   }
-  FS_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
-  FS_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
-  for (int i = 0; i < fs_engine::kBatchEv; ++i) {
-    FS_CUDA(cudaEventCreateWithFlags(&e->batch_ev[i], cudaEventDisableTiming));
-    e->batch_ev_end[i] = -1;
-  }
+  for (int i = 0; i < fs_engine::kBatchEv; ++i) e->batch_ev_end[i] = -1;
+  // the capture / copy streams and batch events are made on first use
+  // (ensemble members never need them); the setup kernels above are ordered
+  // before any later work on the legacy stream, so no device-wide sync here
   FS_CUDA(cudaGetLastError());
-  FS_CUDA(cudaDeviceSynchronize());
 #undef TRY
   *out = e;
   return 0;
@@ -1238,10 +1239,22 @@ int fs_engine_step(fs_engine* e, int32_t nsteps, int32_t materialize, int32_t us
   return launch_steps(e, nsteps, materialize != 0, use_active != 0, (cudaStream_t)stream);
 }
 
+static int batch_resources(fs_engine* e) {
+  if (e->cap_stream) return 0;
+  FS_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+  FS_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < fs_engine::kBatchEv; ++i) FS_CUDA(cudaEventCreateWithFlags(&e->batch_ev[i], cudaEventDisableTiming));
+  return 0;
+}
+
 int fs_engine_run_batch(fs_engine* e, int32_t materialize, void* stream) {
   if (!e) return set_error(FS_EINVAL, "null engine");
   if (materialize && (!e->b.pressure || !e->b.rates)) return set_error(FS_EINVAL, "materialize needs pressure/rates buffers");
   FS_CUDA(cudaSetDevice(e->device));
+  {
+    const int rc0 = batch_resources(e);
+    if (rc0) return rc0;
+  }
   // one graph per (materialise, starting scalar slot): the kernels' slot
   // pointers are baked in at capture
   const int s0 = e->s_cur;
@@ -1433,6 +1446,21 @@ int fs_engine_load_infectivity(fs_engine* e, const void* inf, void* stream) {
   FS_CUDA(cudaSetDevice(e->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = e->g.num_nodes;
+  if (e->count_mode && e->fresh) {
+    // a fresh state's infectivity is beta at the infectious seeds and 0
+    // elsewhere by construction: no representability check, no host sync
+    e->fresh = false;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8));
+    if (e->mixed)
+      k_load_mask<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)inf, n, e->inf_val, e->b.imask[0] + e->node_base / 32,
+                                                          e->b.imask[1] + e->node_base / 32, nullptr);
+    else
+      k_load_mask<float><<<blocks, 256, 0, st>>>((const float*)inf, n, e->inf_val, e->b.imask[0] + e->node_base / 32,
+                                                 e->b.imask[1] + e->node_base / 32, nullptr);
+    FS_CUDA(cudaGetLastError());
+    return recount(e, e->h_step, st);
+  }
+  e->fresh = false;
   if (e->count_mode) {
     FS_CUDA(cudaMemsetAsync(e->bad_flag, 0, sizeof(int), st));
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);

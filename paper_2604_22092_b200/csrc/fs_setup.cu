@@ -120,31 +120,60 @@ __global__ void k_seed_mark(int64_t n, uint64_t step_key, const unsigned long lo
   }
 }
 
-// symmetric iff every edge's multiplicity matches its reverse's
+// symmetric iff every edge's multiplicity matches its reverse's.  Edge e
+// (row i, [a, b)) is checked when it is the first of its run of equal
+// columns: the run's length against the length of i's run in row j.
+template <typename RO>
+__device__ __forceinline__ bool edge_symmetric(const RO* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
+                                               int64_t i, int64_t a, int64_t b, int64_t e) {
+  const int32_t j = col[e];
+  if (e > a && col[e - 1] == j) return true;  // counted with the first of its run
+  if (j < 0 || j >= n) return false;
+  int64_t mult = 1;
+  while (e + mult < b && col[e + mult] == j) ++mult;
+  // equal range of i in row j (sorted by source)
+  int64_t lo = ro[j], hi = ro[j + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (col[mid] < i) lo = mid + 1; else hi = mid;
+  }
+  int64_t lo2 = lo, hi2 = ro[j + 1];
+  while (lo2 < hi2) {
+    const int64_t mid = (lo2 + hi2) >> 1;
+    if (col[mid] <= i) lo2 = mid + 1; else hi2 = mid;
+  }
+  return lo2 - lo == mult;
+}
+
+// a warp takes 32 rows: a lane checks a short row (<= 32 edges) alone; the
+// long rows (scale-free hubs) are checked by the whole warp, 32 edges at a
+// time, so one hub does not serialise the check
 template <typename RO>
 __global__ void k_symmetric(const RO* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
                             int* __restrict__ bad) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = ro[i], b = ro[i + 1];
-    for (int64_t e = a; e < b; ++e) {
-      const int32_t j = col[e];
-      if (e > a && col[e - 1] == j) continue;  // counted with the first of its run
-      int64_t mult = 1;
-      while (e + mult < b && col[e + mult] == j) ++mult;
-      if (j < 0 || j >= n) { atomicExch(bad, 1); return; }
-      // equal range of i in row j (sorted by source)
-      int64_t lo = ro[j], hi = ro[j + 1];
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (col[mid] < i) lo = mid + 1; else hi = mid;
-      }
-      int64_t lo2 = lo, hi2 = ro[j + 1];
-      while (lo2 < hi2) {
-        const int64_t mid = (lo2 + hi2) >> 1;
-        if (col[mid] <= i) lo2 = mid + 1; else hi2 = mid;
-      }
-      if (lo2 - lo != mult) { atomicExch(bad, 1); return; }
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp_g * 32; base < n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    int64_t a = 0, b = 0;
+    if (i < n) {
+      a = ro[i];
+      b = ro[i + 1];
     }
+    const bool wide = b - a > 32;
+    bool ok = true;
+    if (!wide)
+      for (int64_t e = a; e < b && ok; ++e) ok = edge_symmetric(ro, col, n, i, a, b, e);
+    unsigned rest = __ballot_sync(0xffffffffu, wide);
+    while (rest) {
+      const int src = __ffs(rest) - 1;
+      rest &= rest - 1;
+      const int64_t r = base + src;
+      const int64_t ra = __shfl_sync(0xffffffffu, a, src), rb = __shfl_sync(0xffffffffu, b, src);
+      for (int64_t e = ra + lane; e < rb && ok; e += 32) ok = edge_symmetric(ro, col, n, r, ra, rb, e);
+    }
+    if (!ok) atomicExch(bad, 1);
   }
 }
 
@@ -165,6 +194,52 @@ __global__ void k_fill_pattern(T* __restrict__ p, int64_t n, T v) {
 __global__ void k_narrow(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (int32_t)in[i];
+}
+
+// many trials of a small graph at once (ensembles): one CTA per trial sorts
+// all N <= kSmallSeedN (key, id) pairs in shared memory and marks the first
+// `count` — the same selection as the radix path, without host round trips
+constexpr int kSmallSeedN = 4096;
+template <typename ST, typename IT>
+__global__ void __launch_bounds__(1024) k_seed_small(int64_t n, const uint64_t* __restrict__ pick_keys, int64_t count,
+                                                     ST* __restrict__ states, int64_t stride, int comp,
+                                                     IT* __restrict__ inf, float inf_val) {
+  __shared__ unsigned long long sk[kSmallSeedN];
+  __shared__ unsigned short si[kSmallSeedN];
+  const int t = blockIdx.x;
+  const uint64_t step_key = splitmix_step_key(pick_keys[t], 0);
+  int p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+    sk[i] = i < n ? (unsigned long long)seed_key(step_key, (uint64_t)i) : ~0ull;
+    si[i] = (unsigned short)(i < n ? i : 0xFFFF);
+  }
+  __syncthreads();
+  for (int size = 2; size <= p2; size <<= 1) {
+    for (int stride2 = size >> 1; stride2 > 0; stride2 >>= 1) {
+      for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+        const int j = i ^ stride2;
+        if (j > i) {
+          const bool up = (i & size) == 0;
+          const bool gt = sk[i] > sk[j] || (sk[i] == sk[j] && si[i] > si[j]);
+          if (gt == up) {
+            const unsigned long long tk = sk[i];
+            sk[i] = sk[j];
+            sk[j] = tk;
+            const unsigned short ti = si[i];
+            si[i] = si[j];
+            si[j] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    const int id = si[i];
+    states[(int64_t)t * stride + id] = (ST)comp;
+    if (inf) inf[(int64_t)t * stride + id] = from_f32<IT>(inf_val);
+  }
 }
 
 int grid_of(int64_t n, int block = 256) {
@@ -258,6 +333,34 @@ int fs_seed_select(int64_t n, uint64_t seed_key_in, int64_t count, void* states,
   FS_CUDA(cudaGetLastError());
   for (void* q : {(void*)hist, (void*)keys, (void*)ids, (void*)num, (void*)pivot}) cudaFreeAsync(q, st);
   return rc;
+}
+
+int fs_seed_select_batch(int64_t n, int32_t trials, const uint64_t* pick_keys, int64_t count, void* states,
+                         int64_t stride, int32_t states_dtype, int32_t compartment, void* inf, int32_t inf_dtype,
+                         float inf_value, void* stream) {
+  if (n < 1 || n > kSmallSeedN) return set_error(FS_EINVAL, "batched seed selection needs 1 <= N <= %d", kSmallSeedN);
+  if (trials < 1 || !pick_keys || !states) return set_error(FS_EINVAL, "bad batched seed-selection arguments");
+  if (count < 0 || count > n) return set_error(FS_EINVAL, "seed count %lld outside [0, N=%lld]", (long long)count, (long long)n);
+  if (states_dtype != FS_I32 && states_dtype != FS_I8) return set_error(FS_EINVAL, "states dtype must be i32 or i8");
+  if (inf && inf_dtype != FS_F32 && inf_dtype != FS_BF16) return set_error(FS_EINVAL, "infectivity dtype must be f32 or bf16");
+  if (count == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint64_t* dk = nullptr;
+  FS_CUDA(cudaMallocAsync(&dk, sizeof(uint64_t) * trials, st));
+  FS_CUDA(cudaMemcpyAsync(dk, pick_keys, sizeof(uint64_t) * trials, cudaMemcpyHostToDevice, st));
+#define SEED_SMALL(ST_, IT_) \
+  k_seed_small<ST_, IT_><<<trials, 1024, 0, st>>>(n, dk, count, (ST_*)states, stride, compartment, (IT_*)inf, inf_value)
+  if (states_dtype == FS_I8) {
+    if (inf_dtype == FS_BF16) SEED_SMALL(int8_t, __nv_bfloat16);
+    else SEED_SMALL(int8_t, float);
+  } else {
+    if (inf_dtype == FS_BF16) SEED_SMALL(int32_t, __nv_bfloat16);
+    else SEED_SMALL(int32_t, float);
+  }
+#undef SEED_SMALL
+  FS_CUDA(cudaGetLastError());
+  cudaFreeAsync(dk, st);
+  return 0;
 }
 
 int fs_flags_to_ids(const uint8_t* flags, int64_t n, int64_t* out_ids, int64_t* num_out, void* stream) {

@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _device, _lib
-from .renewal import RenewalConfig, _build_plan, as_config, _check_conservation, init_renewal_state
+from .renewal import RenewalConfig, _build_plan, as_config, _check_conservation, init_renewal_state, init_renewal_states
 from .rng import derive_seed
 from .analysis import make_records
 from .trajectory import DEFAULT_GRID_POINTS, TrajectoryRecord
@@ -76,7 +76,8 @@ class _Lockstep:
         self.lib = _lib.load()
         self.trials = trials
         self.seeds = [derive_seed(seed, t) for t in trials]
-        self.states = [init_renewal_state(g, m, cfg, s, seed_count, seed_compartment) for s in self.seeds]
+        self.states = init_renewal_states(g, m, cfg, self.seeds, seed_count, seed_compartment)
+        self.c0 = np.stack([st.counts for st in self.states])  # host scalars: read before the engines own them
         self.engines = [st._bind(plan, s, materialize=False) for st, s in zip(self.states, self.seeds)]
         arr = (ctypes.c_void_p * len(trials))(*[e.handle.value for e in self.engines])
         h = ctypes.c_void_p()
@@ -85,9 +86,9 @@ class _Lockstep:
         self.rc = rc
         self.stream = _device.stream_handle(_device.device())
         self.M = len(m.compartments)
-        self.times = [[0.0] for _ in trials]
-        self.rows = [[st.counts.copy()] for st in self.states]
-        self.end = [None] * len(trials)  # steps a single run would have taken (whole batches)
+        self.clk = []   # per batch: clocks [R, b] and counts [R, b, M] of every trial
+        self.cnt = []
+        self.end = np.zeros(len(trials), dtype=np.int64)  # batches a single run would have taken (0: running)
         self.done = 0
 
     def run_batch(self) -> None:
@@ -100,15 +101,19 @@ class _Lockstep:
         _lib.check(self.lib.fs_ensemble_wait_log(self.handle, self.done, b, clocks.ctypes.data, None,
                                                  counts.ctypes.data))
         self.done += b
-        for r in range(R):
-            if self.end[r] is not None:
-                continue  # past its own stopping batch: a single run would have stopped
-            _check_conservation(counts[r], n)
-            self.times[r].extend(clocks[r].tolist())
-            self.rows[r].extend(counts[r])
-            if clocks[r, -1] >= t_final:
-                self.end[r] = self.done
-        return all(e is not None for e in self.end)
+        live = self.end == 0  # past its own stopping batch a single run would have stopped
+        _check_conservation(counts[live], n)
+        self.clk.append(clocks)
+        self.cnt.append(counts)
+        self.end[live & (clocks[:, -1] >= t_final)] = len(self.clk)
+        return bool((self.end > 0).all())
+
+    def logs(self, r: int):
+        """(times, counts) of trial r over its own batches, the t = 0 sample first."""
+        k = int(self.end[r])
+        times = np.concatenate([[0.0]] + [c[r] for c in self.clk[:k]])
+        rows = np.concatenate([self.c0[r:r + 1]] + [c[r] for c in self.cnt[:k]])
+        return times, rows
 
     def close(self) -> None:
         if self.handle is not None:
@@ -141,9 +146,9 @@ def _run_lockstep(g, m, cfg, seed, t_final, runs, seed_count, seed_compartment, 
             ls.close()
         wall = time.perf_counter() - t0
         for r in range(len(ls.trials)):
-            t_arr = np.asarray(ls.times[r])
-            steps = min(int(np.searchsorted(t_arr, t_final, side="left")), ls.end[r])
-            out.append((t_arr, np.asarray(ls.rows[r]), {"step_count": steps, "wall_clock": wall, "engine": "renewal"}))
+            t_arr, rows = ls.logs(r)
+            steps = min(int(np.searchsorted(t_arr, t_final, side="left")), int(ls.end[r]) * b)
+            out.append((t_arr, rows, {"step_count": steps, "wall_clock": wall, "engine": "renewal"}))
     return out
 
 

@@ -396,6 +396,9 @@ class _Engine:
         b.pressure = _lib.ptr(state._t.get("pressure"))
         b.rates = _lib.ptr(state._t.get("rates"))
         b.padded = 2  # states / ages come from _node_buffer (whole 128-node units)
+        if state._fresh:  # untouched init_renewal_state: ages 0, infectivity {0, beta}
+            b.padded |= _lib.FS_BUF_FRESH
+        state._fresh = False
         self._buffers = b
         h = ctypes.c_void_p()
         _lib.check(self.lib.fs_engine_create(plan.graph.view(), plan.model, plan.config, b, scal,
@@ -535,6 +538,7 @@ class RenewalState:
         self._plans: dict = {}
         self._mirror: dict[str, tuple[np.ndarray, np.ndarray]] = {}
         self._scal_cache: _lib.FsScalars | None = None
+        self._fresh = False  # set by the initialisers; any host write clears it
 
     # ---- engine binding ------------------------------------------------
     def _scal(self) -> _lib.FsScalars:
@@ -543,6 +547,7 @@ class RenewalState:
         return self._scal_cache
 
     def _write_scal(self, **kw) -> None:
+        self._fresh = False
         s = _lib.FsScalars()
         ctypes.memmove(ctypes.byref(s), ctypes.byref(self._scal()), ctypes.sizeof(s))
         for k, v in kw.items():
@@ -636,6 +641,7 @@ class RenewalState:
         return hit[0]
 
     def _upload(self, name: str, arr: np.ndarray) -> None:
+        self._fresh = False
         st, at, it = _storage(self._mixed)
         if name == "counts":
             self._write_scal(counts=np.asarray(arr, dtype=np.int64))
@@ -687,6 +693,7 @@ class RenewalState:
     # ---- reference fields ----------------------------------------------
     def device_tensors(self) -> dict:
         """The live device buffers (no copies)."""
+        self._fresh = False  # the caller may write them
         self._push_host()
         if self._engine is not None:
             self._engine.sync_ages()
@@ -833,8 +840,53 @@ def init_renewal_state(g, m, cfg: RenewalConfig, seed: int, seed_count: int | No
     counts = np.zeros(m.num_compartments, dtype=np.int64)
     counts[m.edge_from] += n - seed_count
     counts[comp] += seed_count
-    return RenewalState(n, m.num_compartments, mixed, dev, {"states": states, "ages": ages, "inf": inf},
-                        counts, cfg.tau_max)
+    st = RenewalState(n, m.num_compartments, mixed, dev, {"states": states, "ages": ages, "inf": inf},
+                      counts, cfg.tau_max)
+    st._fresh = True
+    return st
+
+
+def init_renewal_states(g, m, cfg: RenewalConfig, seeds, seed_count: int | None = None,
+                        seed_compartment: int | None = None) -> list[RenewalState]:
+    """init_renewal_state for many seeds (an ensemble's trials) at once: for
+    graphs of up to 4096 nodes one batched device allocation and one seed-
+    selection launch for every trial (fs_seed_select_batch); each state is
+    exactly init_renewal_state(g, m, cfg, seed, ...)."""
+    cfg = as_config(cfg)
+    seeds = list(seeds)
+    n = int(g.num_nodes)
+    if n > 4096 or len(seeds) < 2:
+        return [init_renewal_state(g, m, cfg, s, seed_count, seed_compartment) for s in seeds]
+    if seed_count is None:
+        seed_count = default_seed_count(n)
+    if not 0 <= seed_count <= n:
+        raise ValueError(f"seed_count {seed_count} outside [0, N]")
+    comp = m.edge_to if seed_compartment is None else int(seed_compartment)
+    dev = _device.device()
+    mixed = bool(cfg.mixed_precision)
+    st_t, at_t, it_t = _storage(mixed)
+    R = len(seeds)
+    cap = (n + 127) // 128 * 128
+    states = _fill(torch.empty((R, cap), dtype=st_t, device=dev), int(m.edge_from))
+    ages = _fill(torch.empty((R, cap), dtype=at_t, device=dev), 0)
+    inf = _fill(torch.empty((R, cap), dtype=it_t, device=dev), 0)
+    seeded_inf = comp == m.infectious and m.transmission.kind == "constant"
+    keys = np.array([derive_seed(s, _SEED_PICK_SALT) & ((1 << 64) - 1) for s in seeds], dtype=np.uint64)
+    if seed_count:
+        _lib.check(_lib.load().fs_seed_select_batch(
+            n, R, keys.ctypes.data, seed_count, _lib.ptr(states), cap, _lib.I8 if mixed else _lib.I32, comp,
+            _lib.ptr(inf) if seeded_inf else None, _lib.BF16 if mixed else _lib.F32, float(np.float32(m.beta)),
+            _device.stream_handle(dev)))
+    counts = np.zeros(m.num_compartments, dtype=np.int64)
+    counts[m.edge_from] += n - seed_count
+    counts[comp] += seed_count
+    out = []
+    for r in range(R):
+        st = RenewalState(n, m.num_compartments, mixed, dev,
+                          {"states": states[r, :n], "ages": ages[r, :n], "inf": inf[r, :n]}, counts, cfg.tau_max)
+        st._fresh = True
+        out.append(st)
+    return out
 
 
 def set_mixed_precision(state: RenewalState, on: bool) -> RenewalState:

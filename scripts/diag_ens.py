@@ -13,7 +13,7 @@ for rep in range(3):
     t = time.perf_counter()
     plan = Rn._build_plan(g, m, cfg, False); torch.cuda.synchronize(); T["plan"] = time.perf_counter() - t; t = time.perf_counter()
     seeds = [fs.derive_seed(20250809, k) for k in range(100)]
-    states = [Rn.init_renewal_state(g, m, cfg, s, 10) for s in seeds]; torch.cuda.synchronize(); T["states"] = time.perf_counter() - t; t = time.perf_counter()
+    states = Rn.init_renewal_states(g, m, cfg, seeds, 10); torch.cuda.synchronize(); T["states"] = time.perf_counter() - t; t = time.perf_counter()
     engs = [st._bind(plan, s, materialize=False) for st, s in zip(states, seeds)]; torch.cuda.synchronize(); T["bind"] = time.perf_counter() - t; t = time.perf_counter()
     lib = _lib.load()
     arr = (ctypes.c_void_p * 100)(*[e.handle.value for e in engs]); h = ctypes.c_void_p()
