@@ -179,3 +179,20 @@ def test_ensemble_abi_rejects_mismatched_members():
     h = ctypes.c_void_p()
     assert lib.fs_ensemble_create(arr, 2, ctypes.byref(h)) == _lib.FS_EINVAL
     assert b"same device, graph" in lib.fs_last_error()
+
+
+def test_batched_init_equals_per_trial_init():
+    """init_renewal_states (one seed-selection launch for every trial) is
+    init_renewal_state per seed, state by state."""
+    m = fs.seir_standard(0.25, 5.0, 4.0, 7.5, 5.0)
+    for n, mixed, count in ((1000, False, 10), (4096, True, 37), (37, False, 37), (2500, False, 0)):
+        g = fs.gen_erdos_renyi(n, 6.0, seed=n)
+        cfg = fs.RenewalConfig(mixed_precision=mixed)
+        seeds = [fs.derive_seed(11, t) for t in range(9)]
+        batch = fs.renewal.init_renewal_states(g, m, cfg, seeds, count)
+        for s, b in zip(seeds, batch):
+            one = fs.init_renewal_state(g, m, cfg, s, count)
+            assert np.array_equal(b.states, one.states)
+            assert np.array_equal(b.ages, one.ages)
+            assert np.array_equal(b.infectivity.astype(np.float32), one.infectivity.astype(np.float32))
+            assert np.array_equal(b.counts, one.counts)
