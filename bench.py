@@ -53,7 +53,7 @@ WORKLOADS = {
     "c3c": dict(desc="C3 graph and model, gather='count': 1-bit infectious-mask gather of the CSR every step "
                      "(EDGE_MERGE)", kind="ba", n=1_000_000, k=5, model="seir_we", gather="count"),
     "c5": dict(desc="C5: SEIR log-normal, uniform-degree k=10, N=1e9, node-partitioned across the GPUs "
-                    "(NCCL mask all-gather + max/count all-reduce per step)",
+                    "(cross-rank pushes to peer mailboxes over NVLink + one 17-word NCCL all-reduce per step)",
                kind="regular_dev", n=1_000_000_000, k=10, model="seir", cpu_n=10_000_000, t_final=10.0),
     "m2": dict(desc="M2 (SURVEY §8f row 3): Markovian SIR (beta 0.25, gamma 0.15), uniform-degree k=10, N=1e6",
                kind="fixed", n=1_000_000, k=10, model="sir_markov", engine="markov"),
@@ -597,7 +597,22 @@ def run_partitioned(args, w, rank: int, world: int, local: int) -> None:
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": None,
+        "scaling_t1": scaling_t1(args.workload, weak),
     }))
+
+
+def scaling_t1(workload: str, weak: bool) -> dict | None:
+    """The one-GPU point of this scaling line: the same workload's committed
+    single-GPU bench line (strong scaling: C5 N = 1e9 on one GPU; weak: C2),
+    so the efficiency value_N / (N x T1) compares like with like — the
+    driver's own N = 1 run is the headline C2, a different workload."""
+    name = {"c5": "c5", "c2w": "c2"}.get(workload)
+    p = ROOT / "profiles" / f"r2_bench_{name}.json" if name else None
+    if not p or not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
+            "scaling": "weak" if weak else "strong", "source": str(p.relative_to(ROOT))}
 
 
 def main() -> None:

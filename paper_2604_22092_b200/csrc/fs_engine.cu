@@ -726,8 +726,13 @@ int sync_s_ages(fs_engine* e, cudaStream_t st) {
 // nodes-per-lane form — 64-node tiles, vector loads, SIMD halfword count
 // folds — measured slower: C2 -3.5 %, C4 -10 %.)
 void set_stream_fns(fs_engine* e, bool uni) {
-  for (int mat = 0; mat < 2; ++mat)
+  for (int mat = 0; mat < 2; ++mat) {
     e->stream_fn[mat] = pick_stream(e->mixed, mat != 0, e->stream_memo, e->stream_hubs, uni, e->world > 1);
+    // the bulk exchange's per-warp push staging (dynamic shared memory on top
+    // of the kernel's static tables: past the 48 KB default)
+    if (e->stream_smem && e->stream_fn[mat])
+      cudaFuncSetAttribute((const void*)e->stream_fn[mat], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->stream_smem);
+  }
 }
 
 // (re)decide the uniform-S-age mode from the ages array (engine creation,
@@ -1092,8 +1097,12 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
       // bulk exchange: mailbox entries per sender and parity ~2 per local node
       // (clamped), exported over CUDA IPC like the delta buffers; used once
       // every rank's mailbox is linked (fs_engine_set_peer_mailboxes)
+      // every rank must lay its mailbox out alike (senders index it with
+      // their own copy of the capacity): sized from the largest range
+      int64_t widest = 0;
+      for (int r = 0; r < e->world; ++r) widest = std::max<int64_t>(widest, e->part_bound[r + 1] - e->part_bound[r]);
       const char* mc = getenv("FS_MBOX_CAP");
-      e->mbox_cap = mc ? std::max<int64_t>(1, atoll(mc)) : std::max<int64_t>(65536, std::min<int64_t>(2 * n, 1 << 24));
+      e->mbox_cap = mc ? std::max<int64_t>(1, atoll(mc)) : std::max<int64_t>(65536, std::min<int64_t>(2 * widest, 1 << 24));
       const size_t words = (size_t)2 * e->world * (size_t)(kMboxHdr + e->mbox_cap);
       TRY(dalloc(&e->mbox, words, true));
       FS_CUDA(cudaMemset(e->mbox, 0, words * sizeof(uint32_t)));
@@ -1147,7 +1156,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     bool reenter = m->comp[m->edge_from].terminal != 0;
     for (int c2 = 0; c2 < m->num_compartments; ++c2)
       if (c2 != m->edge_from && !m->comp[c2].terminal && m->comp[c2].succ == m->edge_from) reenter = true;
-    e->uni_ok = e->stream && !c->compaction && part == nullptr && !reenter && !getenv("FS_NO_UNI");
+    e->uni_ok = e->stream && !c->compaction && !reenter && !getenv("FS_NO_UNI");
     if (e->uni_ok) {
       TRY(dalloc(&e->uni_range, 2));
       if (buf->padded & FS_BUF_FRESH) {  // every age is 0 (a fresh state): uniform, scalar 0

@@ -19,21 +19,25 @@ StepFn pick_stream2(bool mixed, bool mat, bool uni) {
 // pushes for rows over 32 edges (compiled out for bounded-degree graphs);
 // UNI: S ages kept as one uniform scalar, quiet tiles skipped
 // node-partitioned engines (PART): multi-rank pushes (direct peer atomics or
-// the staged bulk exchange); never the uniform S age
-template <bool MEMO, bool HUBS>
-StepFn pick_part(bool mixed, bool mat) {
+// the staged bulk exchange)
+template <bool MEMO, bool HUBS, bool UNI>
+StepFn pick_part3(bool mixed, bool mat) {
   if (mixed)
-    return mat ? k_step_incr<int8_t, __half, true, MEMO, HUBS, false, 512, true>
-               : k_step_incr<int8_t, __half, false, MEMO, HUBS, false, 512, true>;
-  return mat ? k_step_incr<int32_t, float, true, MEMO, HUBS, false, 512, true>
-             : k_step_incr<int32_t, float, false, MEMO, HUBS, false, 512, true>;
+    return mat ? k_step_incr<int8_t, __half, true, MEMO, HUBS, UNI, 512, true>
+               : k_step_incr<int8_t, __half, false, MEMO, HUBS, UNI, 512, true>;
+  return mat ? k_step_incr<int32_t, float, true, MEMO, HUBS, UNI, 512, true>
+             : k_step_incr<int32_t, float, false, MEMO, HUBS, UNI, 512, true>;
+}
+
+template <bool MEMO, bool HUBS>
+StepFn pick_part(bool mixed, bool mat, bool uni) {
+  return uni ? pick_part3<MEMO, HUBS, true>(mixed, mat) : pick_part3<MEMO, HUBS, false>(mixed, mat);
 }
 
 StepFn pick_stream(bool mixed, bool mat, bool memo, bool hubs, bool uni, bool part) {
   if (part) {
-    if (uni) return nullptr;
-    if (memo) return hubs ? pick_part<true, true>(mixed, mat) : pick_part<true, false>(mixed, mat);
-    return hubs ? pick_part<false, true>(mixed, mat) : pick_part<false, false>(mixed, mat);
+    if (memo) return hubs ? pick_part<true, true>(mixed, mat, uni) : pick_part<true, false>(mixed, mat, uni);
+    return hubs ? pick_part<false, true>(mixed, mat, uni) : pick_part<false, false>(mixed, mat, uni);
   }
   if (memo) return hubs ? pick_stream2<true, true>(mixed, mat, uni) : pick_stream2<true, false>(mixed, mat, uni);
   return hubs ? pick_stream2<false, true>(mixed, mat, uni) : pick_stream2<false, false>(mixed, mat, uni);

@@ -185,7 +185,7 @@ class _Partition:
         b = _lib.FsStateBuffers()
         b.states, b.ages = _lib.ptr(self.states), _lib.ptr(self.ages)
         b.imask[0], b.imask[1] = _lib.ptr(masks[0]), _lib.ptr(masks[1])
-        b.padded = 1
+        b.padded = 2  # _node_buffer: whole 128-node units (the streaming step kernel)
         self._b = b
         self._bounds = plan.bounds if plan.balanced else None  # kept alive for the create call
         part = _lib.FsPartition(node_base=lo, num_nodes_global=plan.num_nodes,
@@ -221,9 +221,16 @@ class _Partition:
     def apply_mailbox(self) -> None:
         _lib.check(self.lib.fs_engine_apply_mailbox(self.handle, self.stream))
 
+    def sync_ages(self) -> None:
+        """The uniform S age back into `ages` (the engine keeps it as one
+        scalar while every S node shares it): call before
+        reading `ages`."""
+        _lib.check(self.lib.fs_engine_sync_ages(self.handle, self.stream))
+
     def close(self) -> None:
         if getattr(self, "handle", None):
-            torch.cuda.current_stream().synchronize()
+            if torch is not None and torch.cuda is not None:  # (interpreter teardown)
+                torch.cuda.current_stream().synchronize()
             self.lib.fs_engine_destroy(self.handle)
             self.handle = None
 
@@ -303,6 +310,8 @@ class LocalPartitionedRun:
 
     def gather(self) -> dict:
         """Whole-graph states / ages (concatenated partitions) and scalars."""
+        for p in self.parts:
+            p.sync_ages()
         s = self.parts[0].scalars()
         return {"states": torch.cat([p.states for p in self.parts]).cpu().numpy(),
                 "ages": torch.cat([p.ages for p in self.parts]).cpu().numpy(),

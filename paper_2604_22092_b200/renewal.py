@@ -33,7 +33,7 @@ import torch
 
 from . import _device, _lib
 from .errors import InvalidConfigError, ReconfigureAfterStartError
-from .graph import CsrGraph, Strategy, as_strategy, resolve_strategy
+from .graph import CsrGraph, DegreeStats, Strategy, as_strategy, resolve_strategy, select_strategy
 from .models import ModelSpec, model_descriptor
 from .rng import RNG_KINDS, derive_seed, uniform_array
 from .trajectory import DEFAULT_GRID_POINTS, TrajectoryRecord, make_record
@@ -339,8 +339,12 @@ class _EnginePlan:
 
 def _build_plan(g, m, cfg: RenewalConfig, mixed: bool) -> _EnginePlan:
     cfg = as_config(cfg)
-    strategy = resolve_strategy(g, cfg.strategy)
     dg = device_graph(g, mixed)
+    strategy = as_strategy(cfg.strategy)
+    if strategy == Strategy.AUTO:  # degree_stats from the upload's own max-degree scan (no second host pass)
+        strategy = (select_strategy(DegreeStats(d_avg=dg.num_edges / dg.num_nodes, d_max=dg.d_max,
+                                                rho=dg.d_max / (dg.num_edges / dg.num_nodes)))
+                    if dg.num_edges > 0 else Strategy.PER_NODE)
     count_mode = m.transmission.kind == "constant" and dg.uniform and cfg.gather != "f32"
     if cfg.gather in ("count", "incremental") and not count_mode:
         raise InvalidConfigError(f"gather={cfg.gather!r} needs constant transmission and uniform weights")

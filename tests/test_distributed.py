@@ -185,6 +185,7 @@ def _ipc_worker(rank: int, world: int, port: int, steps: int, out_q, exchange: s
     assert run.part.incremental
     run.step(steps)
     s = run.part.scalars()
+    run.part.sync_ages()
     out_q.put((rank, run.part.states.cpu().numpy(), run.part.ages.cpu().numpy(),
                np.array(s.counts[:4], dtype=np.int64), s.clock))
     dist.barrier()
