@@ -19,9 +19,12 @@ if [ -z "$SKIP_BENCH" ]; then
   done
   timeout 900 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_${TAG}_ref_c2.json 2> gpurun_out/bench_${TAG}_ref_c2.err; echo "ref rc=$?"
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_" --csv --log-file gpurun_out/launches_${TAG}_c2.csv python bench.py --steps 20 --warmup 3 --no-e2e --cpu-steps 0 > /dev/null 2>&1; echo "list rc=$?"
+  # the C4 step kernel over the bench window (its per-launch times grow with the epidemic)
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"^k_step_incr$" --csv --log-file gpurun_out/launches_${TAG}_c4.csv python bench.py --workload c4 --steps 50 --warmup 3 --no-e2e --cpu-steps 0 > /dev/null 2>&1; echo "list c4 rc=$?"
+  timeout 900 python bench.py --partitioned --workload c5 --steps 50 --warmup 3 --cpu-steps 0 > gpurun_out/bench_${TAG}_c5_partitioned_world1.json 2> gpurun_out/bench_${TAG}_c5p.err; echo "c5 partitioned rc=$?"
 fi
 for W in ${PROF:-c2 c3 c4 c5 c2s c3f c3c ens}; do
-  case $W in c2s|c3f) K="^k_step$";; c3c) K="^k_gather_merge$";; ens) K="^k_step_incr_multi$";; *) K="^k_step_incr$";; esac
+  case $W in c2s|c3f|c3c) K="^k_step$";; ens) K="^k_step_incr_multi$";; *) K="^k_step_incr$";; esac
   R=gpurun_out/prof_${TAG}_$W
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$K" -s ${SKIP:-6} -c 1 -o $R -f \
     python bench.py --workload $W --steps 10 --warmup 3 --no-e2e --cpu-steps 0 > gpurun_out/ncu_${TAG}_$W.log 2>&1; echo "ncu $W rc=$?"
