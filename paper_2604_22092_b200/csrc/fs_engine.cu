@@ -330,6 +330,7 @@ struct fs_engine {
   int64_t nhubs = 0;
   float* hub_pre = nullptr;     // [N]
   uint32_t* hub_flag = nullptr; // [N]
+  int hub_spin = 256;           // bounded wait for a hub's tag (FS_HUB_SPIN; 0: always fold it in place)
   bool mixed = false;
   int gather = G_F32;
   int strat = S_THREAD;
@@ -496,6 +497,7 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.nhubs = e->nhubs;
   p.hub_pre = e->hub_pre;
   p.hub_flag = e->hub_flag;
+  p.hub_spin = e->hub_spin;
   p.stream_evict_first = e->stream_evict_first;
   p.host_parity = (int)(e->h_step & 1);
   p.entry = e->entry;
@@ -956,6 +958,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   if (e->gather == G_F32M_SMEM && e->strat == S_HYBRID)
     e->step_smem += (size_t)(e->step_block / 32) * kHubPass * sizeof(float);  // the hub fold stages behind the mask
   if (e->strat == S_HYBRID) TRY(build_hub_list(e));
+  if (getenv("FS_HUB_SPIN")) e->hub_spin = std::max(0, atoi(getenv("FS_HUB_SPIN")));
   int occ = 1;
   for (int mat = 0; mat < 2; ++mat) {
     if (e->step_smem > 0)
