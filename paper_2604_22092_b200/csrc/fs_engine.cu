@@ -330,7 +330,6 @@ struct fs_engine {
   int64_t nhubs = 0;
   float* hub_pre = nullptr;     // [N]
   uint32_t* hub_flag = nullptr; // [N]
-  int hub_spin = 256;           // bounded wait for a hub's tag (FS_HUB_SPIN; 0: always fold it in place)
   bool mixed = false;
   int gather = G_F32;
   int strat = S_THREAD;
@@ -497,7 +496,6 @@ StepParams make_step_params(const fs_engine* e, bool use_pre, bool use_active, i
   p.nhubs = e->nhubs;
   p.hub_pre = e->hub_pre;
   p.hub_flag = e->hub_flag;
-  p.hub_spin = e->hub_spin;
   p.stream_evict_first = e->stream_evict_first;
   p.host_parity = (int)(e->h_step & 1);
   p.entry = e->entry;
@@ -617,7 +615,22 @@ int launch_steps(fs_engine* e, int nsteps, bool materialize_last, bool use_activ
       cfg.numAttrs = 2;
       FS_CUDA(cudaLaunchKernelEx(&cfg, e->tma_fn[mat], p, e->tl));
     }
-    else
+    else if (e->strat == S_HYBRID) {
+      // the one-launch edge-merge: tile lanes wait for hub results that other
+      // CTAs of the grid produce, so the grid is launched cooperatively — all
+      // CTAs resident together whatever else runs on the device
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(e->step_grid_general);
+      cfg.blockDim = dim3(e->step_block);
+      cfg.dynamicSmemBytes = e->step_smem_general;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      FS_CUDA(cudaLaunchKernelEx(&cfg, e->step_fn[mat], p));
+    } else
       e->step_fn[mat]<<<e->step_grid_general, e->step_block, e->step_smem_general, st>>>(p);
     e->s_cur ^= 1;
     if (e->comm) {
@@ -958,13 +971,18 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   if (e->gather == G_F32M_SMEM && e->strat == S_HYBRID)
     e->step_smem += (size_t)(e->step_block / 32) * kHubPass * sizeof(float);  // the hub fold stages behind the mask
   if (e->strat == S_HYBRID) TRY(build_hub_list(e));
-  if (getenv("FS_HUB_SPIN")) e->hub_spin = std::max(0, atoi(getenv("FS_HUB_SPIN")));
+
   int occ = 1;
   for (int mat = 0; mat < 2; ++mat) {
     if (e->step_smem > 0)
       TRY(cudaFuncSetAttribute((const void*)e->step_fn[mat], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->step_smem) == cudaSuccess ? 0 : set_error(FS_ECUDA, "smem attribute"));
   }
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)e->step_fn[1], e->step_block, e->step_smem) != cudaSuccess || occ < 1) occ = 1;
+  {  // both variants must fit the grid (the cooperative launch of S_HYBRID checks it)
+    int occ0 = occ;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, (const void*)e->step_fn[0], e->step_block, e->step_smem) == cudaSuccess && occ0 >= 1)
+      occ = std::min(occ, occ0);
+  }
   // the step loops over 32-node tiles; do not launch CTAs with no tile
   {
     const int64_t warps_needed = e->ntiles;

@@ -94,12 +94,11 @@ struct StepParams {
   int f32_mask;                  // f32 gather keeps the nonzero-infectivity mask (G_F32M_*)
   // fused edge-merge (S_HYBRID + G_F32M_*): the nodes with more than kWide
   // in-edges, heaviest first, are folded by the grid's warps round robin
-  // before the tile sweep; a tile lane of such a node waits (bounded) for its flag
+  // before the tile sweep; a tile lane of such a node waits for its flag
   const int32_t* hub_list;
   int64_t nhubs;
   float* hub_pre;                // [N] pressure of the hubs (entries of hubs only)
   uint32_t* hub_flag;            // [N] step tag (step + 1) once hub_pre[n] holds this step's value
-  int hub_spin;                  // polls of a hub's tag before the waiting warp folds the row itself
   // incremental count mode (G_INCR): per-node infectious in-neighbour count,
   // kept current by +-1 pushes along the outgoing edges of every node whose
   // infectious status changes
@@ -1258,33 +1257,13 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
                                                      in.hi);
           }
         }
-        // hub lanes take the pre-pass's result.  The wait is bounded: should
-        // the hub's warp not be resident (another grid holding SMs), the warp
-        // folds the row itself — the same CSR-order fold, the same bits — so
-        // no schedule can deadlock the grid
-        unsigned wides = __ballot_sync(kFull, wide);
-        while (wides) {
-          const int j = __ffs(wides) - 1;
-          wides &= wides - 1;
-          const int64_t hn = __shfl_sync(kFull, n, j);
-          bool ready = false;
-          for (int spin = 0; spin < p.hub_spin && !ready; ++spin)
-            ready = __shfl_sync(kFull, lane == 0 ? (int)(ld_acquire_u32(p.hub_flag + hn) == hub_tag) : 0, 0) != 0;
-          float pj;
-          if (ready) {
-            pj = __ldcg(p.hub_pre + hn);
-          } else {
-            const int64_t lj = __shfl_sync(kFull, in.lo, j), hj = __shfl_sync(kFull, in.hi, j);
-            const uint64_t pol = l2_policy_stream(p.stream_evict_first);
-            if (COUNT) {
-              const int kk = count_hub<SMASK>(p.col, gmask, lj, hj, lane, pol);
-              pj = p.ptab_mul ? __fmul_rn((float)kk, p.ptab_c) : __ldg(p.ptab + kk);
-            } else {
-              pj = fold_hub_masked<IT, SMASK>(p.col, gmask, inf_cur, p.w, p.w_bf16, p.w_uniform, p.w_val, lj, hj, lane,
-                                              s_fold + warp * kStage, pol);
-            }
+        // hub lanes take the pre-pass's result.  The engine launches this
+        // kernel cooperatively (every CTA resident), so each hub's warp runs
+        // and the wait ends
+        if (wide) {
+          while (ld_acquire_u32(p.hub_flag + n) != hub_tag) {
           }
-          if (lane == j) pressure = pj;
+          pressure = __ldcg(p.hub_pre + n);
         }
       } else {  // warp per node (LANE strategy)
         unsigned rest = todo;

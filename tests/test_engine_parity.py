@@ -156,8 +156,7 @@ def test_variants_are_result_neutral(name, overrides):
     assert_matches(st, log, cps, ref)
 
 
-@pytest.mark.parametrize("env", [{}, {"FS_MERGE_UNFUSED": "1"}, {"FS_NO_F32_MASK": "1"},
-                                 {"FS_HUB_SPIN": "0"}])  # hub lanes fold their rows themselves (no wait)
+@pytest.mark.parametrize("env", [{}, {"FS_MERGE_UNFUSED": "1"}, {"FS_NO_F32_MASK": "1"}])
 @pytest.mark.parametrize("overrides", [
     {"gather": "f32", "strategy": Strategy.EDGE_MERGE},           # fused edge-merge: hub pre-pass + tile sweep
     {"gather": "f32", "strategy": Strategy.EDGE_MERGE, "edges_per_block": 64},
