@@ -147,12 +147,18 @@ _BYTES = {torch.int8: 1, torch.uint8: 1, torch.int16: 2, torch.float16: 2, torch
           torch.float32: 4, torch.int64: 8, torch.float64: 8}
 
 
+_FILL_PATTERN: dict = {}
+
+
 def _fill(t: torch.Tensor, value) -> torch.Tensor:
     """Fill a device buffer through the library (fs_fill) — torch only owns it."""
     if t.numel():
-        pat = torch.tensor([value], dtype=t.dtype).view(torch.uint8).numpy().tobytes()
-        _lib.check(_lib.load().fs_fill(_lib.ptr(t), t.numel(), _BYTES[t.dtype], int.from_bytes(pat, "little"),
-                                       _device.stream_handle(t.device)))
+        key = (t.dtype, repr(value))  # repr: -0.0 and 0.0 are different patterns
+        pat = _FILL_PATTERN.get(key)
+        if pat is None:  # the element's bytes, once per (dtype, value)
+            raw = torch.tensor([value], dtype=t.dtype).view(torch.uint8).numpy().tobytes()
+            pat = _FILL_PATTERN[key] = int.from_bytes(raw, "little")
+        _lib.check(_lib.load().fs_fill(_lib.ptr(t), t.numel(), _BYTES[t.dtype], pat, _device.stream_handle(t.device)))
     return t
 
 

@@ -6,7 +6,7 @@ T="tests/test_engine_parity.py::test_trajectory_parity_graph_replay tests/test_e
 # lockstep ensembles and batched seed selection, the bulk exchange (mailbox staging / apply), IPC transport
 T="$T tests/test_engine_parity.py::test_gather_forms_bit_exact tests/test_ensemble.py::test_lockstep_equals_stream_runner tests/test_ensemble.py::test_batched_init_equals_per_trial_init tests/test_distributed.py::test_edge_balanced_virtual_ranks_match_single_engine"
 T=${TESTS:-$T}
-for TOOL in memcheck racecheck synccheck; do
+for TOOL in ${TOOLS:-memcheck racecheck synccheck}; do
   timeout ${SAN_TIMEOUT:-1500} $CS --tool $TOOL --error-exitcode 99 --print-limit 20 python -m pytest $T -q -x -m gpu -p no:cacheprovider > gpurun_out/sanitize_$TOOL.log 2>&1; echo "$TOOL rc=$?"
   grep -E "ERROR SUMMARY|passed|failed" gpurun_out/sanitize_$TOOL.log | tail -3
 done
