@@ -1154,11 +1154,16 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     // the cohort table is prepared inside the step kernel's final drains
     // (an idle lane, the same hazard call: DESIGN.md §3.3).  It replaces the
     // f64 hazard of every queued E / I node by a lookup: a win for the
-    // log-normal hazard (erfc / exp / log chain) at every size — C2 full run
+    // log-normal hazard (erfc / exp / log chain) from ~1.3e5 nodes — C2 full run
     // -30 % step time, early window -1.5 % — and for the cheaper Weibull /
     // Erlang hazards only where steps are long (N >= 4M)
     const char* mv = getenv("FS_MEMO");
-    const bool want = mv ? atoi(mv) != 0 : (e->stream && (lognormal || n >= (int64_t)4 * 1024 * 1024));
+    // (below ~1.3e5 nodes the per-warp preparation costs more than the
+    // lookups save: full C1-sized runs 9.2 -> 8.2 us/step without it, the
+    // 1e5 point even, 3e5 11.6 -> 9.8 and 1e6 24.8 -> 16.9 with it;
+    // scripts/diag_memo_size.py)
+    const bool want = mv ? atoi(mv) != 0
+                         : (e->stream && ((lognormal && n >= (int64_t)1 << 17) || n >= (int64_t)4 * 1024 * 1024));
     if (costly && want && !getenv("FS_NO_MEMO")) {
       TRY(dalloc(&e->entry, (size_t)((n + 127) / 128) * 128));
       TRY(dalloc(&e->ctab, (size_t)2 * kCohortSlots * kCohortW));

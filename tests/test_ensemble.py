@@ -196,3 +196,18 @@ def test_batched_init_equals_per_trial_init():
             assert np.array_equal(b.ages, one.ages)
             assert np.array_equal(b.infectivity.astype(np.float32), one.infectivity.astype(np.float32))
             assert np.array_equal(b.counts, one.counts)
+
+
+def test_concurrent_one_launch_merges_on_streams():
+    """The one-launch edge-merge waits inside the grid for other CTAs' hub
+    results, so it runs as a cooperative launch: trials of a BA graph with
+    the f32 fold, one engine per trial on 32 concurrent streams
+    (lockstep=False), must neither deadlock nor differ from the sequential
+    runs."""
+    g = fs.gen_barabasi_albert(6000, 4, seed=8)
+    m = fs.seir_weibull_erlang(0.25)
+    cfg = fs.RenewalConfig(gather="f32", strategy=fs.Strategy.EDGE_MERGE, steps_per_batch=25)
+    recs = fs.run_ensemble("renewal", g, m, cfg, 5, 20.0, 40, seed_count=20, lockstep=False)
+    for t in (0, 13, 39):
+        rec = fs.run_renewal(g, m, cfg, fs.derive_seed(5, t), 20.0, seed_count=20)
+        assert np.array_equal(rec.fractions, recs[t].fractions)
