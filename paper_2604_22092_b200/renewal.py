@@ -244,6 +244,12 @@ class _DeviceGraph:
         self.symmetric = sym
 
     def view(self) -> _lib.FsGraph:
+        v = self.__dict__.get("_view")
+        if v is None:  # the device arrays never change: build the descriptor once
+            v = self._view = self._make_view()
+        return v
+
+    def _make_view(self) -> _lib.FsGraph:
         return _lib.FsGraph(
             num_nodes=self.num_nodes,
             num_edges=self.num_edges,
@@ -388,8 +394,10 @@ class _Engine:
         _, _, it = _storage(state.mixed_precision)
         w = ((n + 31) // 32 + 1 + 3) // 4 * 4  # + a zero sentinel word, 16-byte multiple (TMA)
         # the infectious mask (count gather), or the nonzero-infectivity
-        # bitmap kept next to the f32 infectivity (the f32 gather's prefilter)
-        self.masks = [_fill(torch.empty(w, dtype=torch.int32, device=dev), 0) for _ in range(2)]
+        # bitmap kept next to the f32 infectivity (the f32 gather's prefilter):
+        # both parities in one allocation
+        masks = _fill(torch.empty((2, w), dtype=torch.int32, device=dev), 0)
+        self.masks = [masks[0], masks[1]]
         if plan.count_mode:
             self.bufs = self.masks
         else:
