@@ -409,6 +409,7 @@ struct fs_engine {
   int stage_cap = 0;
   size_t stream_smem = 0;
   bool stream = false;         // k_step_incr fast path of the incremental mode
+  bool stream_part() const { return world > 1; }
   StepFn stream_fn[2] = {nullptr, nullptr};
   bool stream_memo = false, stream_hubs = false;  // k_step_incr variant flags
   // uniform S age: eligible when every step runs k_step_incr
@@ -1860,6 +1861,7 @@ struct fs_ensemble {
   int count = 0;
   std::vector<fs_engine*> members;
   MultiFn fn = nullptr;
+  PersistFn persist = nullptr;    // small members: one CTA runs a whole batch of steps (k_step_incr_persist)
   StepFn member_fn = nullptr;     // the members' k_step_incr variant at creation
   uint32_t ctas_per = 1;
   int grid = 1;
@@ -1929,6 +1931,11 @@ int fs_ensemble_create(fs_engine* const* engines, int32_t count, fs_ensemble** o
   x->member_fn = e0->stream_fn[0];
   x->fn = pick_stream_multi(e0->mixed, false, e0->stream_memo, e0->stream_hubs, e0->s_uniform);
   if (!x->fn) { delete x; return set_error(FS_EINVAL, "no ensemble step kernel for this engine variant"); }
+  // members of at most 128 tiles (4096 nodes) without the cohort table: a
+  // CTA per member steps the whole batch (no launch or grid boundary per
+  // step); FS_ENSEMBLE_STEPWISE keeps one launch per step
+  if (e0->ntiles <= 128 && !e0->stream_memo && !e0->stream_part() && !getenv("FS_ENSEMBLE_STEPWISE"))
+    x->persist = pick_stream_persist(e0->mixed, e0->stream_hubs, e0->s_uniform);
   x->pdl = e0->pdl;
   x->M = e0->m.num_compartments;
   x->steps_per_batch = e0->c.steps_per_batch;
@@ -2003,7 +2010,12 @@ static int ensemble_launch_batch(fs_ensemble* x, cudaStream_t st) {
                                          x->carry_tau);
   int s = x->s_cur;
   int64_t h = x->h_step;
-  for (int k = 0; k < x->steps_per_batch; ++k) {
+  if (x->persist) {
+    x->persist<<<x->count, 512, 0, st>>>(x->dparams, (uint32_t)x->count, s, (int)(h & 1), x->steps_per_batch);
+    s ^= x->steps_per_batch & 1;
+    h += x->steps_per_batch;
+  }
+  for (int k = 0; k < x->steps_per_batch && !x->persist; ++k) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(x->grid);
     cfg.blockDim = dim3(512);

@@ -1308,7 +1308,11 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
 #endif
 // `cta` / `nctas`: this CTA and the CTAs sharing the engine `p` (the whole
 // grid, or one member's CTAs of an ensemble launch)
-template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, int BLOCK, bool PART = false>
+// PERSIST: one CTA runs several steps in a row (k_step_incr_persist): the
+// per-node arrays it rewrites are then read back inside the same kernel, so
+// no load may take the non-coherent read-only path
+template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, int BLOCK, bool PART = false,
+          bool PERSIST = false>
 __device__ __forceinline__ void step_incr_body(const StepParams& p, const uint32_t cta, const uint32_t nctas) {
   constexpr int WARPS = BLOCK / 32;
   __shared__ StepShared<WARPS> sh;
@@ -1343,8 +1347,10 @@ __device__ __forceinline__ void step_incr_body(const StepParams& p, const uint32
       if (UNI) commit_s_age<AT>(p, s_k);
     }
   }
-  const ST* __restrict__ states = reinterpret_cast<const ST*>(p.states);
-  const AT* __restrict__ ages = reinterpret_cast<const AT*>(p.ages);
+  using SP = std::conditional_t<PERSIST, const ST*, const ST* __restrict__>;
+  using AP = std::conditional_t<PERSIST, const AT*, const AT* __restrict__>;
+  SP states = reinterpret_cast<const ST*>(p.states);
+  AP ages = reinterpret_cast<const AT*>(p.ages);
   uint16_t* __restrict__ cnt = p.cnt;
   const uint32_t N = (uint32_t)p.n, ntiles = (uint32_t)p.ntiles;
   const uint32_t stride = nctas * WARPS;
@@ -1487,6 +1493,25 @@ template <typename ST, typename AT, bool MAT, bool MEMO, bool HUBS, bool UNI, in
 __global__ void __launch_bounds__(BLOCK, 2) k_step_incr_multi(const StepParams* __restrict__ P, const uint32_t ctas_per) {
   const uint32_t m = blockIdx.x / ctas_per;
   step_incr_body<ST, AT, MAT, MEMO, HUBS, UNI, BLOCK>(P[m], blockIdx.x - m * ctas_per, ctas_per);
+}
+
+// Ensembles of small trials (every member fits one CTA): CTA m runs `nsteps`
+// consecutive steps of member m — a block barrier between steps instead of
+// a kernel boundary, since no other CTA touches the member's state.  P holds
+// the members' parameters for the four (scalar slot, step parity) pairs,
+// [pair][count]; step i of the batch uses pair (s0 ^ i&1, p0 ^ i&1) — the
+// same parameters the per-step launches would pass, so the results are
+// the same bits.  The cohort table is off (its slots are read through the
+// non-coherent path); the engine only picks this form without it.
+template <typename ST, typename AT, bool HUBS, bool UNI, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, 2) k_step_incr_persist(const StepParams* __restrict__ P, const uint32_t count,
+                                                                const int s0, const int p0, const int nsteps) {
+  const uint32_t m = blockIdx.x;
+  for (int i = 0; i < nsteps; ++i) {
+    const int pair = ((s0 ^ (i & 1)) << 1) | (p0 ^ (i & 1));
+    step_incr_body<ST, AT, false, false, HUBS, UNI, BLOCK, false, true>(P[(size_t)pair * count + m], 0u, 1u);
+    __syncthreads();  // this step's writes (state, counts, pushes, accumulator, scalars) before the next step's reads
+  }
 }
 
 // thread-per-node count over a slice staged in shared memory: lane-private
@@ -1734,11 +1759,13 @@ using StepFn = void (*)(const StepParams);
 using MergeFn = void (*)(const MergeParams);
 using TmaFn = void (*)(const StepParams, const TmaLayout);
 using MultiFn = void (*)(const StepParams*, uint32_t);
+using PersistFn = void (*)(const StepParams*, uint32_t, int, int, int);
 
 // instantiation units
 StepFn pick_step(bool mixed, int gather, int strat, bool mat, int& block);  // fs_step_general.cu
 StepFn pick_stream(bool mixed, bool mat, bool memo, bool hubs, bool uni, bool part = false);  // fs_step_incr.cu
-MultiFn pick_stream_multi(bool mixed, bool mat, bool memo, bool hubs, bool uni);    // fs_step_incr.cu
+MultiFn pick_stream_multi(bool mixed, bool mat, bool memo, bool hubs, bool uni);    // fs_step_multi.cu
+PersistFn pick_stream_persist(bool mixed, bool hubs, bool uni);                     // fs_step_multi.cu
 MergeFn pick_merge(bool inf_bf16, int mode, int& block);                    // fs_step_incr.cu
 TmaFn pick_tma(bool mixed, bool smem_mask, bool mat, bool ptab_mul, int block);  // fs_step_tma.cu
 

@@ -22,4 +22,15 @@ MultiFn pick_stream_multi(bool mixed, bool mat, bool memo, bool hubs, bool uni) 
   return hubs ? pick_multi2<false, true>(mixed, uni) : pick_multi2<false, false>(mixed, uni);
 }
 
+template <bool HUBS, bool UNI>
+PersistFn pick_persist2(bool mixed) {
+  if (mixed) return k_step_incr_persist<int8_t, __half, HUBS, UNI, 512>;
+  return k_step_incr_persist<int32_t, float, HUBS, UNI, 512>;
+}
+
+PersistFn pick_stream_persist(bool mixed, bool hubs, bool uni) {
+  if (hubs) return uni ? pick_persist2<true, true>(mixed) : pick_persist2<true, false>(mixed);
+  return uni ? pick_persist2<false, true>(mixed) : pick_persist2<false, false>(mixed);
+}
+
 }  // namespace fs

@@ -130,8 +130,11 @@ def _summ(recs):
             for r in recs]
 
 
+@pytest.mark.parametrize("stepwise", [False, True])  # one CTA per trial for the whole batch / one launch per step
 @pytest.mark.parametrize("case", ["er_seir", "ba_weibull_erlang", "er_mixed", "ba_sir"])
-def test_lockstep_equals_stream_runner(case):
+def test_lockstep_equals_stream_runner(case, stepwise, monkeypatch):
+    if stepwise:
+        monkeypatch.setenv("FS_ENSEMBLE_STEPWISE", "1")
     if case.startswith("er"):
         g = fs.gen_erdos_renyi(1500, 6.0, seed=11)
     else:
