@@ -24,7 +24,7 @@ if [ -z "$SKIP_BENCH" ]; then
   timeout 900 python bench.py --partitioned --workload c5 --steps 50 --warmup 3 --cpu-steps 0 > gpurun_out/bench_${TAG}_c5_partitioned_world1.json 2> gpurun_out/bench_${TAG}_c5p.err; echo "c5 partitioned rc=$?"
 fi
 for W in ${PROF:-c2 c3 c4 c5 c2s c3f c3c ens}; do
-  case $W in c2s|c3f|c3c) K="^k_step$";; ens) K="^k_step_incr_multi$";; *) K="^k_step_incr$";; esac
+  case $W in c2s|c3f|c3c) K="^k_step$";; ens) K="^k_step_incr_persist$";; *) K="^k_step_incr$";; esac
   R=gpurun_out/prof_${TAG}_$W
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$K" -s ${SKIP:-6} -c 1 -o $R -f \
     python bench.py --workload $W --steps 10 --warmup 3 --no-e2e --cpu-steps 0 > gpurun_out/ncu_${TAG}_$W.log 2>&1; echo "ncu $W rc=$?"
