@@ -171,6 +171,34 @@ __global__ void k_begin_batch_multi(const MemberBatch* __restrict__ mb, int coun
   begin_batch_one(mb[m].D[slot], mb[m].acc, mb[m].log_counts, log_cap, M, eps, tau_max, delta, carry_tau);
 }
 
+// cohort table reset (reset_memo): entry = step - 1 for nodes of age exactly 0
+template <typename AT>
+__global__ void k_memo_reset(const AT* __restrict__ ages, int64_t n, int64_t cap, int32_t j, int32_t* __restrict__ entry) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
+    bool zero = false;  // +0 exactly (bit pattern)
+    if (i < n) {
+      if constexpr (sizeof(AT) == 4) zero = __float_as_uint(ages[i]) == 0u;
+      else zero = __half_as_ushort(ages[i]) == 0;
+    }
+    entry[i] = zero ? j : kEntryInvalid;
+  }
+}
+struct CohortSeed {
+  int n;
+  int kind[kCohortSlots];
+  double p0[kCohortSlots], p1[kCohortSlots];
+};
+// the table of `step`: the slot of the cohort entered at step - 1 (age 0)
+__global__ void k_memo_seed(unsigned long long* ctab, unsigned long long* cage, CohortSeed cs, int64_t step, int hprec) {
+  const int t = threadIdx.x;
+  const int par = (int)(step & 1);
+  const uint32_t idx = (uint32_t)(step - 1) & (kCohortW - 1);
+  const unsigned long long tag = (unsigned long long)(uint32_t)step << 32;
+  if (t == 0) cage[par * kCohortW + idx] = tag | __float_as_uint(0.0f);
+  if (t < cs.n)
+    ctab[((size_t)par * kCohortSlots + t) * kCohortW + idx] = tag | __float_as_uint(nodal_rate(cs.kind[t], cs.p0[t], cs.p1[t], 0.0f, hprec));
+}
+
 // compaction refresh at tile granularity: a 32-node tile is active if any of
 // its nodes is non-terminal (renewal.py:426-432 at node granularity; results
 // are identical because terminal nodes do rate-0 work either way)
@@ -703,13 +731,34 @@ int launch_begin_batch(fs_engine* e, cudaStream_t st) {
 }
 
 // hazard memo: every node's cohort unknown, every slot's tag stale
-int reset_memo(fs_engine* e, cudaStream_t st) {
+// `step` is the step the next launch runs.  A node whose age is exactly 0
+// then is, for the table, a member of the cohort that "entered at step - 1"
+// (its age chain from 0 is the one a fresh cohort follows), so it keeps
+// table lookups instead of direct hazards — the seeds of a fresh state above
+// all, every step until they transition; every other node's cohort is
+// unknown.  The table of `step` is seeded with that cohort's slot (age 0,
+// the hazards at age 0), everything else is stale.
+int reset_memo(fs_engine* e, cudaStream_t st, int64_t step) {
   if (!e->entry) return 0;
-  const int64_t n = (e->g.num_nodes + 127) / 128 * 128;
-  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)e->sms * 8);
-  k_fill<int32_t><<<std::max(1, blocks), 256, 0, st>>>(e->entry, n, kEntryInvalid);
+  const int64_t n = e->g.num_nodes, cap = (n + 127) / 128 * 128;
+  const int blocks = (int)std::min<int64_t>((cap + 255) / 256, (int64_t)e->sms * 8);
   FS_CUDA(cudaMemsetAsync(e->ctab, 0xFF, sizeof(unsigned long long) * 2 * kCohortSlots * kCohortW, st));
   FS_CUDA(cudaMemsetAsync(e->cage, 0xFF, sizeof(unsigned long long) * 2 * kCohortW, st));
+  const int32_t j = (int32_t)(step - 1);
+  if (e->mixed)
+    k_memo_reset<__half><<<std::max(1, blocks), 256, 0, st>>>((const __half*)e->b.ages, n, cap, j, e->entry);
+  else
+    k_memo_reset<float><<<std::max(1, blocks), 256, 0, st>>>((const float*)e->b.ages, n, cap, j, e->entry);
+  CohortSeed cs{};
+  cs.n = 0;
+  for (int c = 0; c < e->m.num_compartments && cs.n < kCohortSlots; ++c)
+    if (e->m.comp[c].hazard >= FS_HZ_LOGNORMAL) {  // the table slots, as make_step_params numbers them
+      cs.kind[cs.n] = e->m.comp[c].hazard;
+      cs.p0[cs.n] = e->m.comp[c].p0;
+      cs.p1[cs.n] = e->m.comp[c].p1;
+      ++cs.n;
+    }
+  k_memo_seed<<<1, 32, 0, st>>>(e->ctab, e->cage, cs, step, e->c.hazard_precision);
   FS_CUDA(cudaGetLastError());
   return 0;
 }
@@ -1169,7 +1218,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
       TRY(dalloc(&e->entry, (size_t)((n + 127) / 128) * 128));
       TRY(dalloc(&e->ctab, (size_t)2 * kCohortSlots * kCohortW));
       TRY(dalloc(&e->cage, (size_t)2 * kCohortW));
-      TRY(reset_memo(e, nullptr));
+      TRY(reset_memo(e, nullptr, e->h_step));
       if (e->stream) {  // the memo's shared-memory table only in the variant that uses it
         e->stream_memo = true;
         set_stream_fns(e, false);
@@ -1469,7 +1518,7 @@ int fs_engine_set_scalars(fs_engine* e, const fs_scalars* in, void* stream) {
   if (e->hub_flag && in->step != cur.s.step)  // hub tags are step numbers
     FS_CUDA(cudaMemsetAsync(e->hub_flag, 0, sizeof(uint32_t) * e->g.num_nodes, st));
   if (in->step != cur.s.step) {  // memo tags and cohorts are relative to the step counter
-    rc = reset_memo(e, st);
+    rc = reset_memo(e, st, in->step);
     if (rc) return rc;
   }
   FS_CUDA(cudaStreamSynchronize(st));
@@ -1559,7 +1608,7 @@ int fs_engine_states_edited(fs_engine* e, void* stream) {
   if (!e) return set_error(FS_EINVAL, "null engine");
   FS_CUDA(cudaSetDevice(e->device));
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = reset_memo(e, st);  // edited nodes no longer follow their age cohorts
+  int rc = reset_memo(e, st, e->h_step);  // edited nodes no longer follow their age cohorts
   if (!rc) rc = recheck_uniform(e, st);  // the caller synced S ages (fs_engine_sync_ages) before editing
   e->tiles_valid = false;       // an edit can revive nodes of an inactive tile
   if (rc || !e->incr) return rc;
@@ -1583,7 +1632,7 @@ int fs_engine_states_edited(fs_engine* e, void* stream) {
 int fs_engine_reset_age_memo(fs_engine* e, void* stream) {
   if (!e) return set_error(FS_EINVAL, "null engine");
   FS_CUDA(cudaSetDevice(e->device));
-  const int rc = reset_memo(e, (cudaStream_t)stream);
+  const int rc = reset_memo(e, (cudaStream_t)stream, e->h_step);
   return rc ? rc : recheck_uniform(e, (cudaStream_t)stream);
 }
 
@@ -1594,7 +1643,7 @@ int fs_engine_state_restored(fs_engine* e, void* stream) {
   // every per-node array and the mask were overwritten: the incremental
   // counts and pending deltas are rebuilt from the current mask, the memo and
   // the active tiles are stale, and the S-age mode is re-decided
-  int rc = reset_memo(e, st);
+  int rc = reset_memo(e, st, e->h_step);
   if (!rc && e->incr) {
     if (e->world > 1) return set_error(FS_ESTATE, "restoring a partitioned engine is not supported");
     rc = recount(e, e->h_step, st);
