@@ -1212,8 +1212,11 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     // lookups save: full C1-sized runs 9.2 -> 8.2 us/step without it, the
     // 1e5 point even, 3e5 11.6 -> 9.8 and 1e6 24.8 -> 16.9 with it;
     // scripts/diag_memo_size.py)
+    // (the kernels that prepare the table: the streaming step and the
+    // general step's f32 fold — not the TMA count gather)
+    const bool preparer = e->stream || e->gather == G_F32 || e->gather == G_F32M_SMEM || e->gather == G_F32M_GLOBAL;
     const bool want = mv ? atoi(mv) != 0
-                         : (e->stream && ((lognormal && n >= (int64_t)1 << 17) || n >= (int64_t)4 * 1024 * 1024));
+                         : (preparer && ((lognormal && n >= (int64_t)1 << 17) || n >= (int64_t)4 * 1024 * 1024));
     if (costly && want && !getenv("FS_NO_MEMO")) {
       TRY(dalloc(&e->entry, (size_t)((n + 127) / 128) * 128));
       TRY(dalloc(&e->ctab, (size_t)2 * kCohortSlots * kCohortW));

@@ -1288,7 +1288,15 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK >= 1024 ? 1 : 2)) k_step(const S
     tile_outcome<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, (uint32_t)tile, (uint32_t)n, valid, in.s, in.age, pressure, qn, lmax,
                                          mask_nxt, inf_nxt);
   }
-  if (qn > 0) drain_queue<ST, AT, IT, MAT, WARPS>(p, k, sh, warp, lane, qn, lmax, mask_nxt, inf_nxt);
+  {
+    // the final drain also prepares one (slot, cohort) pair of the next
+    // step's cohort table in its idle lane 31 (as k_step_incr does)
+    const int gw = (int)blockIdx.x * WARPS + warp;
+    const int prep = (p.ctab && gw < kCohortW * p.ncslots) ? gw : -1;
+    if (qn > 0 || prep >= 0)
+      drain_entries<ST, AT, IT, MAT, WARPS>(p, k, sh, sh.q_node[warp], sh.q_state[warp], sh.q_age[warp],
+                                            sh.q_press[warp], lane, qn, lmax, mask_nxt, inf_nxt, prep);
+  }
   // a warp without tiles still has to see the bulk copy land before exit
   if (SMASK && !mask_ready) mbar_wait_parity(&s_bar, 0);
   finish_step<WARPS>(p, k, sh, warp, lane, lmax);

@@ -316,7 +316,7 @@ def test_run_renewal_record_matches_reference():
     {"FS_NO_STREAM": "1"},                   # incremental counts in the general kernel
     {"FS_NO_PDL": "1", "FS_MEMO": "1"},
 ])
-@pytest.mark.parametrize("name", ["c1", "c1_mixed", "ba_merge", "sir"])
+@pytest.mark.parametrize("name", ["c1", "c1_mixed", "ba_merge", "sir", "shed_hazard", "weighted"])
 def test_engine_variants_bit_exact(name, env, monkeypatch):
     """Kernel variants the engine selects by size or switch (read when an
     engine is created) against the reference goldens, stepwise and replayed."""
