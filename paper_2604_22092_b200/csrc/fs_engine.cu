@@ -1196,27 +1196,20 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   }
   {
     // hazard memo for models with age-dependent holding times
-    bool costly = false, lognormal = false;
-    for (int c2 = 0; c2 < m->num_compartments; ++c2) {
-      costly |= m->comp[c2].hazard >= FS_HZ_LOGNORMAL;
-      lognormal |= m->comp[c2].hazard == FS_HZ_LOGNORMAL;
-    }
+    bool costly = false;
+    for (int c2 = 0; c2 < m->num_compartments; ++c2) costly |= m->comp[c2].hazard >= FS_HZ_LOGNORMAL;
     // the cohort table is prepared inside the step kernel's final drains
-    // (an idle lane, the same hazard call: DESIGN.md §3.3).  It replaces the
-    // f64 hazard of every queued E / I node by a lookup: a win for the
-    // log-normal hazard (erfc / exp / log chain) from ~1.3e5 nodes — C2 full run
-    // -30 % step time, early window -1.5 % — and for the cheaper Weibull /
-    // Erlang hazards only where steps are long (N >= 4M)
+    // (an idle lane, the same hazard call: DESIGN.md §3.3) — by the streaming
+    // step and the general step's f32 fold, not the TMA count gather.  It
+    // replaces the f64 hazard of every queued E / I node by a lookup: from
+    // ~1.3e5 nodes on, where that outweighs the per-warp preparation (full
+    // runs: 1e4 nodes 9.2 -> 8.2 us/step without it, 1e5 even, 3e5 11.6 ->
+    // 9.8 and 1e6 24.8 -> 16.9 with it, scripts/diag_memo_size.py), for the
+    // log-normal and the Weibull / Erlang hazards alike (C3 warm 81 -> 87,
+    // e2e 38.9 -> 44.7 G-NUPS, flushed value -1 %)
     const char* mv = getenv("FS_MEMO");
-    // (below ~1.3e5 nodes the per-warp preparation costs more than the
-    // lookups save: full C1-sized runs 9.2 -> 8.2 us/step without it, the
-    // 1e5 point even, 3e5 11.6 -> 9.8 and 1e6 24.8 -> 16.9 with it;
-    // scripts/diag_memo_size.py)
-    // (the kernels that prepare the table: the streaming step and the
-    // general step's f32 fold — not the TMA count gather)
     const bool preparer = e->stream || e->gather == G_F32 || e->gather == G_F32M_SMEM || e->gather == G_F32M_GLOBAL;
-    const bool want = mv ? atoi(mv) != 0
-                         : (preparer && ((lognormal && n >= (int64_t)1 << 17) || n >= (int64_t)4 * 1024 * 1024));
+    const bool want = mv ? atoi(mv) != 0 : (preparer && n >= (int64_t)1 << 17);
     if (costly && want && !getenv("FS_NO_MEMO")) {
       TRY(dalloc(&e->entry, (size_t)((n + 127) / 128) * 128));
       TRY(dalloc(&e->ctab, (size_t)2 * kCohortSlots * kCohortW));
