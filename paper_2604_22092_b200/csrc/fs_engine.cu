@@ -1200,7 +1200,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     for (int c2 = 0; c2 < m->num_compartments; ++c2) costly |= m->comp[c2].hazard >= FS_HZ_LOGNORMAL;
     // the cohort table is prepared inside the step kernel's final drains
     // (an idle lane, the same hazard call: DESIGN.md §3.3) — by the streaming
-    // step and the general step's f32 fold, not the TMA count gather.  It
+    // step and the general step, not the TMA count-gather kernel.  It
     // replaces the f64 hazard of every queued E / I node by a lookup: from
     // ~1.3e5 nodes on, where that outweighs the per-warp preparation (full
     // runs: 1e4 nodes 9.2 -> 8.2 us/step without it, 1e5 even, 3e5 11.6 ->
@@ -1208,7 +1208,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     // log-normal and the Weibull / Erlang hazards alike (C3 warm 81 -> 87,
     // e2e 38.9 -> 44.7 G-NUPS, flushed value -1 %)
     const char* mv = getenv("FS_MEMO");
-    const bool preparer = e->stream || e->gather == G_F32 || e->gather == G_F32M_SMEM || e->gather == G_F32M_GLOBAL;
+    const bool preparer = e->stream || !e->tma;
     const bool want = mv ? atoi(mv) != 0 : (preparer && n >= (int64_t)1 << 17);
     if (costly && want && !getenv("FS_NO_MEMO")) {
       TRY(dalloc(&e->entry, (size_t)((n + 127) / 128) * 128));
