@@ -43,6 +43,27 @@ int set_error(int code, const char* fmt, ...) {
   return code;
 }
 
+// small host values (run scalars, the pressure table) written through a
+// launch argument instead of a pageable cudaMemcpy, which waits for the
+// device: creating an engine (e.g. the members of an ensemble) then queues
+// its setup without ever blocking on the work queued before it
+struct WordBlob { uint32_t w[512]; };
+__global__ void k_put_words(uint32_t* __restrict__ dst, const WordBlob b, int nwords) {
+  for (int i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = b.w[i];
+}
+
+static int put_small(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes % 4 == 0 && bytes <= sizeof(WordBlob)) {
+    WordBlob b;
+    memcpy(b.w, src, bytes);
+    k_put_words<<<1, 128, 0, st>>>(static_cast<uint32_t*>(dst), b, (int)(bytes / 4));
+  }
+  const cudaError_t err = (bytes % 4 == 0 && bytes <= sizeof(WordBlob))
+                              ? cudaGetLastError()
+                              : cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+  return err == cudaSuccess ? 0 : set_error(FS_ECUDA, "put_small(%zu B): %s", bytes, cudaGetErrorString(err));
+}
+
 // incremental count mode: counts from scratch (engine start, host edits):
 // cnt[n] = number of infectious in-neighbours in mask m; both pending-delta
 // buffers cleared to the bias
@@ -1056,7 +1077,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
       volatile float prod = (float)kk * cval;
       if (acc != prod) ok = 0;
     }
-    FS_CUDA(cudaMemcpyAsync(e->ptab, tab.data(), sizeof(float) * tab.size(), cudaMemcpyHostToDevice, (cudaStream_t)0));
+    TRY(put_small(e->ptab, tab.data(), sizeof(float) * tab.size(), (cudaStream_t)0));
     e->ptab_mul = ok;
     e->ptab_c = cval;
   }
@@ -1148,7 +1169,7 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
     DevState d0{};
     d0.s = *scal;
     d0.pending = 0;
-    FS_CUDA(cudaMemcpy(e->dstate, &d0, sizeof(DevState), cudaMemcpyHostToDevice));
+    TRY(put_small(e->dstate, &d0, sizeof(DevState), (cudaStream_t)0));
     e->s_cur = 0;
   }
   if (e->merge) {
@@ -1246,9 +1267,12 @@ static int engine_create(const fs_graph* g, const fs_model* m, const fs_config* 
   }
   for (int i = 0; i < fs_engine::kBatchEv; ++i) e->batch_ev_end[i] = -1;
   // the capture / copy streams and batch events are made on first use
-  // (ensemble members never need them); the setup kernels above are ordered
-  // before any later work on the legacy stream, so no device-wide sync here
+  // (ensemble members never need them).  The setup work above runs on the
+  // legacy stream, which does not order against non-blocking streams (every
+  // PyTorch pool stream is one): wait for it here — one host wait per
+  // engine, the only one (small values go in by launch argument, put_small)
   FS_CUDA(cudaGetLastError());
+  TRY(cudaStreamSynchronize((cudaStream_t)0) == cudaSuccess ? 0 : set_error(FS_ECUDA, "engine setup"));
 #undef TRY
   *out = e;
   return 0;

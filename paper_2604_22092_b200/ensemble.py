@@ -116,12 +116,12 @@ class _Lockstep:
         return times, rows
 
     def close(self) -> None:
+        torch.cuda.current_stream().synchronize()  # once for the ensemble and every member
         if self.handle is not None:
-            torch.cuda.current_stream().synchronize()
             self.lib.fs_ensemble_destroy(self.handle)
             self.handle = None
         for e in self.engines:  # the trial states are dropped with their engines
-            e.close()
+            e.close(sync=False)
 
 
 def _run_lockstep(g, m, cfg, seed, t_final, runs, seed_count, seed_compartment, plan, group: int):

@@ -424,13 +424,16 @@ class _Engine:
         self.handle = h
         self.load_infectivity(inf)
 
-    def close(self) -> None:
+    def close(self, sync: bool = True) -> None:
+        """sync=False: the caller has already synchronised the engine's work."""
         if getattr(self, "handle", None):
-            torch.cuda.current_stream().synchronize()
+            if sync:
+                torch.cuda.current_stream().synchronize()
             self.lib.fs_engine_destroy(self.handle)
             self.handle = None
 
-    __del__ = close
+    def __del__(self) -> None:
+        self.close()
 
     def sync_ages(self) -> None:
         """Uniform S age back into the ages array (before host reads / edits)."""
