@@ -1009,7 +1009,17 @@ def _check_active(state: RenewalState, plan: _EnginePlan, active: ActiveSet) -> 
 def renewal_step(state: RenewalState, g, m, cfg: RenewalConfig, seed: int, *, plan: _EnginePlan | None = None,
                  active: ActiveSet | None = None) -> tuple[RenewalState, float]:
     """One fused tau-leap (renewal.py:483-580): one kernel launch (two under
-    EDGE_MERGE), pressure / rates materialised for inspection."""
+    EDGE_MERGE), pressure / rates materialised for inspection.
+
+    With an active set (compaction) the step is exact for the nodes it
+    processes, but the materialised `state.pressure` is specified only for
+    the listed nodes (the values the step uses): terminal nodes inside an
+    active 32-node tile may carry their gathered pressure and, under
+    EDGE_MERGE, nodes outside the active tiles read 0, where the reference
+    writes 0 for every unlisted node under PER_NODE / LANE and keeps the
+    whole-graph merge gather under EDGE_MERGE (R/renewal.py:276-302).
+    States, ages, infectivity, counts and the clock are bit-exact either
+    way."""
     cfg = as_config(cfg)
     if plan is None:
         plan = state._plan_for(g, m, cfg)
